@@ -1,0 +1,189 @@
+/*
+ * gespmm.h — C ABI of the B200-native GE-SpMM library (libgespmm.so).
+ *
+ * This is the drop-in boundary for the reference's SpMM-like hot path
+ * (arXiv 2007.03179 reference, /root/reference/proj/include/spmm/).  Plain
+ * pointers and sizes only; no C++ or torch types cross it, no exception
+ * crosses it.  Every entry point names the reference interface it replaces.
+ * The C++ drop-in (namespace spmm, include/gespmm/spmm.hpp) and the Python
+ * host mirror (paper_2007_03179_b200/) are thin layers over these calls.
+ *
+ * Semantics (bit-exact contract):
+ *   C[i][j] = fold_{p in row i, ascending} combine(acc, vals[p] * B[col_ind[p]][j])
+ *   with the product and the combine rounded separately (no FMA) in the default
+ *   exact mode.  sum: init +0, a+b.  max: init -FLT_MAX, (a < b ? b : a).
+ *   min: init +FLT_MAX, (b < a ? b : a).  mean: sum / float(row length), empty
+ *   row -> +0.  arg (max/min): CSR position p (or col_ind[p]) of the element that
+ *   last replaced the accumulator (earliest p among ties), -1 if none.
+ */
+#ifndef GESPMM_H_
+#define GESPMM_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GESPMM_ABI_VERSION 1
+
+/* Reduce ops.  Replaces spmm::ReduceOp / ops::sum / ops::max
+ * (reference include/spmm/reduce_op.hpp:14-28): a host function pointer cannot
+ * run on the device, so the op is named and fused into the kernel. */
+typedef enum {
+  GESPMM_SUM = 0,
+  GESPMM_MEAN = 1,
+  GESPMM_MAX = 2,
+  GESPMM_MIN = 3
+} gespmm_reduce_t;
+
+typedef enum {
+  GESPMM_OK = 0,
+  GESPMM_EINVAL = 1,      /* bad argument / unknown op / bad config (spmm::Error) */
+  GESPMM_EDIM = 2,        /* "dimension mismatch" (simt.hpp:373-380) */
+  GESPMM_ENONCANON = 3,   /* "matrix is not canonical CSR" (csr.hpp:155-158) */
+  GESPMM_ECUDA = 4,       /* CUDA runtime failure */
+  GESPMM_ENOMEM = 5,      /* device allocation failed */
+  GESPMM_EUNSUPPORTED = 6 /* valid request this build cannot serve */
+} gespmm_status_t;
+
+/* Kernel variants.  KernelVariant / KernelKind (kernel.hpp:44-68).
+ * NAIVE/CRC/CRC_CWM are the paper's Algorithms 1-3 with the reference's warp
+ * geometry (warp = (row, 32*cf column tile), lane owns col_base+lane+c*32);
+ * TUNED is the B200 design (sub-warp rows, float4 lanes, CWM merge factor and
+ * row-per-warp vs row-per-CTA chosen from N and the degree distribution).
+ * All variants give bitwise-identical results in exact mode. */
+typedef enum {
+  GESPMM_VARIANT_TUNED = 0,
+  GESPMM_VARIANT_NAIVE = 1,
+  GESPMM_VARIANT_CRC = 2,
+  GESPMM_VARIANT_CRC_CWM = 3
+} gespmm_variant_t;
+
+typedef enum { GESPMM_ARG_EDGE = 0, GESPMM_ARG_COLUMN = 1 } gespmm_arg_kind_t;
+
+/* CSR view.  CsrMatrix (csr.hpp:22-35): u32 row_ptr[n_rows+1], u32 col_ind[nnz],
+ * f32 vals[nnz].  For *_device calls the three pointers are device pointers. */
+typedef struct {
+  uint32_t n_rows;
+  uint32_t n_cols;
+  uint64_t nnz;
+  const uint32_t* row_ptr;
+  const uint32_t* col_ind;
+  const float* vals;
+} gespmm_csr_t;
+
+/* Options; gespmm_options_default() fills the defaults. */
+typedef struct {
+  int32_t variant;    /* gespmm_variant_t, default TUNED */
+  uint32_t cf;        /* CRC_CWM coarsening factor: 2, 4 or 8 (check_config, kernel.hpp:83-92) */
+  int32_t exact;      /* 1 (default): ordered fold, separate mul/add -> bit-exact for all ops.
+                         0: sum/mean may use FFMA and split hub rows (1e-5 rel. tolerance). */
+  int32_t arg_kind;   /* gespmm_arg_kind_t, default EDGE (CSR position) */
+  int32_t validate;   /* 1 (default for *_host): canonical-CSR check before the launch */
+  int32_t fault_skip_tail; /* negative-test hook: FaultMode::SkipTail (kernel.hpp:167-182) */
+  int32_t l2_hints;   /* 1 (default): B evict_last, CSR/C evict_first */
+  int32_t hub_threshold; /* TUNED: rows with degree >= this go row-per-CTA; 0 = auto, <0 = off */
+  int32_t reserved[8];
+} gespmm_options_t;
+
+void gespmm_options_default(gespmm_options_t* opts);
+
+/* Last error text of the calling thread, worded like the spmm::Error the
+ * reference would raise for the same input. */
+const char* gespmm_last_error(void);
+
+/* ---- the hot path ------------------------------------------------------- */
+
+/* Device SpMM-like: A (device CSR) x B (device, row-major K x n) -> C (device,
+ * row-major M x n) [+ arg (device int32, M x n) for MAX/MIN; may be NULL].
+ * Asynchronous on `stream` (cudaStream_t, NULL = legacy default).  Replaces the
+ * compute of spmm::native_spmm (native.hpp:101-143) / run_warp
+ * (kernel.hpp:346-361).  B and C must not alias.  validate=1 runs the
+ * canonical check on the device first and synchronises `stream` to report it. */
+gespmm_status_t gespmm_spmm_device(const gespmm_csr_t* a, const float* b, uint32_t n,
+                                   gespmm_reduce_t op, float* c, int32_t* arg,
+                                   const gespmm_options_t* opts, void* stream);
+
+/* Host-buffer SpMM-like, the native_spmm-shaped call (native.hpp:101-102):
+ * validates (as check_spmm_inputs, simt.hpp:373-380), copies A and B to the
+ * device, runs, copies C (and arg) back.  b_rows must equal a->n_cols.
+ * Host buffers may be pinned or pageable.  Synchronous. */
+gespmm_status_t gespmm_spmm_host(const gespmm_csr_t* a, const float* b, uint32_t b_rows,
+                                 uint32_t n, gespmm_reduce_t op, float* c, int32_t* arg,
+                                 const gespmm_options_t* opts);
+
+/* ---- plans: inspect once, execute many ---------------------------------- */
+
+typedef struct gespmm_plan_s* gespmm_plan_t;
+
+/* Inspect a device CSR (degree distribution) and fix the kernel shape for this
+ * n/op: sub-warp vs warp vs CTA per row class, merge factor, row schedule.  The
+ * plan keeps pointers to A's arrays, which must stay valid.  Synchronous. */
+gespmm_status_t gespmm_plan_create(const gespmm_csr_t* a, uint32_t n, gespmm_reduce_t op,
+                                   const gespmm_options_t* opts, void* stream,
+                                   gespmm_plan_t* out);
+gespmm_status_t gespmm_plan_execute(gespmm_plan_t plan, const float* b, float* c, int32_t* arg,
+                                    void* stream);
+/* Human-readable description of the chosen shape (static storage per plan). */
+const char* gespmm_plan_describe(gespmm_plan_t plan);
+/* Number of kernel launches one gespmm_plan_execute issues. */
+int32_t gespmm_plan_launches(gespmm_plan_t plan);
+void gespmm_plan_destroy(gespmm_plan_t plan);
+
+/* ---- checks and helpers -------------------------------------------------- */
+
+/* Device canonical-CSR check (csr.hpp:112-153); status ENONCANON with the
+ * reference's first-violation message in gespmm_last_error().  Synchronous. */
+gespmm_status_t gespmm_validate_device(const gespmm_csr_t* a, void* stream);
+
+/* Reference dispatch rule, select_variant (kernel.hpp:96-98): n <= 32 -> CRC,
+ * else CRC_CWM with cf 2. */
+void gespmm_select_variant(uint32_t n, int32_t* variant, uint32_t* cf);
+
+/* Name lookup, reduce_op_by_name (reduce_op.hpp:32-36), extended with mean/min. */
+gespmm_status_t gespmm_reduce_by_name(const char* name, gespmm_reduce_t* out);
+
+/* FNV-1a over the element bytes xor (rows<<32)^cols — checksum (dense.hpp:62-72). */
+uint64_t gespmm_checksum(const float* host_data, uint32_t rows, uint32_t cols);
+
+/* ---- synthetic inputs (host, deterministic) ------------------------------ */
+
+/* make_random_dense (dense.hpp:51-59): mt19937_64(seed), x = (r>>40)*2^-23 - 1. */
+void gespmm_make_random_dense(uint32_t rows, uint32_t cols, uint64_t seed, float* out);
+
+/* randomize_values (generate.hpp:73-80): v = ((r>>44)+1)*2^-19, random sign. */
+void gespmm_randomize_values(float* vals, uint64_t nnz, uint64_t seed);
+
+/* gen_uniform_random (generate.hpp:39-69): exactly nnz distinct positions by
+ * seeded rejection, values 1.0, canonicalised.  row_ptr[rows+1], col_ind[nnz],
+ * vals[nnz] caller-allocated.  Bit-identical to the reference for equal specs. */
+gespmm_status_t gespmm_gen_uniform(uint32_t rows, uint64_t nnz, uint64_t seed, int32_t self_loops,
+                                   uint32_t* row_ptr, uint32_t* col_ind, float* vals);
+
+/* Power-law (Chung-Lu style) square graph — new; the reference has none.
+ * Degrees follow a truncated power law with the given mean and max degree;
+ * columns are drawn from the same weights; rows are canonical (sorted,
+ * unique, no self loops); values 1.0.  Deterministic for (rows, nnz, seed)
+ * and independent of `threads`.  Two calls: with col_ind == NULL it only fills
+ * row_ptr (so the caller can size col_ind/vals by row_ptr[rows]); then with
+ * buffers.  The realised nnz is within 0.1% of nnz_target. */
+gespmm_status_t gespmm_gen_powerlaw(uint32_t rows, uint64_t nnz_target, uint32_t max_degree,
+                                    double exponent, uint64_t seed, int32_t threads,
+                                    uint32_t* row_ptr, uint32_t* col_ind, float* vals);
+
+/* Library / device facts for reports. */
+int32_t gespmm_abi_version(void);
+gespmm_status_t gespmm_device_info(int32_t* sm_count, int64_t* l2_bytes,
+                                   int64_t* persisting_l2_max, int32_t* cc_major,
+                                   int32_t* cc_minor);
+
+/* Kernel launches issued by this library since load (all entry points). */
+uint64_t gespmm_launch_count(void);
+
+#ifdef __cplusplus
+}  /* extern "C" */
+#endif
+
+#endif /* GESPMM_H_ */

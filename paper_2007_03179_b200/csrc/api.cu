@@ -1,0 +1,561 @@
+// C-ABI implementation: argument checks with the reference's error texts,
+// plans (inspector: degree distribution -> kernel shape + row schedule),
+// the device and host-buffer entry points.
+//
+// Reference behaviour mirrored (file:line under /root/reference/proj):
+//   check_spmm_inputs   include/spmm/simt.hpp:373-380 (dims, then canonical)
+//   require_canonical   include/spmm/csr.hpp:155-158  ("<who>: matrix is not canonical CSR: ...")
+//   native_spmm         include/spmm/native.hpp:101-143 (M==0 -> empty, N==0 -> error)
+//   check_config        include/spmm/kernel.hpp:83-92  (cf in {2,4,8})
+//   select_variant      include/spmm/kernel.hpp:96-98
+//   reduce_op_by_name   include/spmm/reduce_op.hpp:32-36
+#include <algorithm>
+#include <atomic>
+#include <cstdio>
+#include <cstring>
+#include <list>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "launch.h"
+
+namespace gespmm {
+
+static std::atomic<uint64_t> g_launches{0};
+void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+namespace {
+
+thread_local std::string t_err;
+
+gespmm_status_t fail(gespmm_status_t st, const std::string& msg) {
+  t_err = msg;
+  return st;
+}
+
+gespmm_status_t cuda_fail(cudaError_t e, const char* where) {
+  return fail(e == cudaErrorMemoryAllocation ? GESPMM_ENOMEM : GESPMM_ECUDA,
+              std::string(where) + ": CUDA error: " + cudaGetErrorString(e));
+}
+
+#define GESPMM_CUDA(call, where)                     \
+  do {                                               \
+    cudaError_t e_ = (call);                         \
+    if (e_ != cudaSuccess) return cuda_fail(e_, where); \
+  } while (0)
+
+bool aligned(const void* p, size_t a) { return (reinterpret_cast<uintptr_t>(p) % a) == 0; }
+
+// Formats the first violation in the order the reference checks
+// (csr.hpp:112-153); returns GESPMM_OK when canonical.
+gespmm_status_t validation_status(const ValidateResult& r, uint32_t m, uint32_t k, uint64_t nnz,
+                                  const char* who) {
+  char buf[256];
+  const std::string pre = std::string(who) + ": matrix is not canonical CSR: ";
+  if (r.row_ptr0 != 0) {
+    std::snprintf(buf, sizeof buf, "row_ptr[0] = %u, expected 0", r.row_ptr0);
+    return fail(GESPMM_ENONCANON, pre + buf);
+  }
+  if (r.first_decrease != 0xffffffffu) {
+    std::snprintf(buf, sizeof buf, "row_ptr non-decreasing violated at index %u", r.first_decrease);
+    return fail(GESPMM_ENONCANON, pre + buf);
+  }
+  if (uint64_t(r.row_ptr_last) != nnz) {
+    std::snprintf(buf, sizeof buf, "row_ptr[n_rows] = %u != nnz = %llu", r.row_ptr_last,
+                  (unsigned long long)nnz);
+    return fail(GESPMM_ENONCANON, pre + buf);
+  }
+  if (r.first_bad_key != ~0ull) {
+    const unsigned long long p = r.first_bad_key >> 1;
+    if ((r.first_bad_key & 1ull) == 0)
+      std::snprintf(buf, sizeof buf, "col_ind[%llu] = %u out of bounds (n_cols = %u)", p,
+                    r.bad_col, k);
+    else
+      std::snprintf(buf, sizeof buf, "columns not strictly increasing in row %u at position %llu",
+                    r.bad_row, p);
+    return fail(GESPMM_ENONCANON, pre + buf);
+  }
+  (void)m;
+  return GESPMM_OK;
+}
+
+gespmm_status_t check_opts(const gespmm_options_t& o) {
+  if (o.variant < GESPMM_VARIANT_TUNED || o.variant > GESPMM_VARIANT_CRC_CWM)
+    return fail(GESPMM_EINVAL, "unknown kernel variant " + std::to_string(o.variant) +
+                                   " (naive, crc, crc-cwm, tuned)");
+  if (o.variant == GESPMM_VARIANT_CRC_CWM && o.cf != 2 && o.cf != 4 && o.cf != 8)
+    return fail(GESPMM_EINVAL, "coarsening factor must be 2, 4 or 8");
+  if (o.arg_kind != GESPMM_ARG_EDGE && o.arg_kind != GESPMM_ARG_COLUMN)
+    return fail(GESPMM_EINVAL, "arg_kind must be edge (0) or column (1)");
+  return GESPMM_OK;
+}
+
+gespmm_status_t check_op(gespmm_reduce_t op, const int32_t* arg) {
+  if (op < GESPMM_SUM || op > GESPMM_MIN)
+    return fail(GESPMM_EINVAL, "unknown reduce op " + std::to_string(int(op)) +
+                                   " (built-ins: sum, mean, max, min)");
+  if (arg && op != GESPMM_MAX && op != GESPMM_MIN)
+    return fail(GESPMM_EINVAL, "arg indices are defined for max and min only");
+  return GESPMM_OK;
+}
+
+}  // namespace
+
+gespmm_status_t set_error(gespmm_status_t st, const std::string& msg) { return fail(st, msg); }
+
+// ---------------------------------------------------------------------------
+// Plans
+// ---------------------------------------------------------------------------
+struct Plan {
+  gespmm_csr_t a{};
+  uint32_t n = 0;
+  gespmm_reduce_t op = GESPMM_SUM;
+  gespmm_options_t o{};
+  int device = 0;
+  // tuned
+  WarpShape warp_v, warp_s;  // vectorised shape and scalar-lane fallback
+  CtaShape cta_v, cta_s;
+  uint32_t n_hub = 0;        // order[0, n_hub) -> row-per-CTA
+  uint32_t hub_threshold = 0;
+  uint32_t* d_order = nullptr;
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  std::string desc;
+  uint32_t max_degree = 0;
+  double mean_degree = 0.0;
+
+  ~Plan() {
+    if (d_order) cudaFree(d_order);
+    if (ev_fork) cudaEventDestroy(ev_fork);
+    if (ev_join) cudaEventDestroy(ev_join);
+    if (side) cudaStreamDestroy(side);
+  }
+};
+
+namespace {
+
+uint32_t auto_hub_threshold(uint32_t n, double mean_degree) {
+  if (n < 64) return 0xffffffffu;  // the CTA split needs >= 2 warps of columns
+  const double t = std::max(4096.0, 16.0 * mean_degree);
+  return t >= 4294967295.0 ? 0xffffffffu : uint32_t(t);
+}
+
+// Inspector: degree-descending row schedule (stable counting sort) so heavy
+// rows start first (LPT) and sub-warps pair rows of similar length; rows with
+// degree >= threshold are peeled off for the row-per-CTA kernel.
+gespmm_status_t build_tuned(Plan& p, const uint32_t* host_rp, cudaStream_t st) {
+  const uint32_t m = p.a.n_rows;
+  std::vector<uint32_t> deg(m);
+  uint32_t maxd = 0;
+  for (uint32_t r = 0; r < m; ++r) {
+    deg[r] = host_rp[r + 1] - host_rp[r];
+    maxd = std::max(maxd, deg[r]);
+  }
+  p.max_degree = maxd;
+  p.mean_degree = m ? double(host_rp[m]) / m : 0.0;
+  std::vector<uint32_t> count(size_t(maxd) + 2, 0);
+  for (uint32_t r = 0; r < m; ++r) ++count[maxd - deg[r]];
+  uint64_t acc = 0;
+  for (auto& c : count) {
+    const uint64_t t = c;
+    c = uint32_t(acc);
+    acc += t;
+  }
+  std::vector<uint32_t> order(m);
+  for (uint32_t r = 0; r < m; ++r) order[count[maxd - deg[r]]++] = r;
+
+  const int32_t ht = p.o.hub_threshold;
+  p.hub_threshold = ht > 0 ? uint32_t(ht) : (ht < 0 ? 0xffffffffu : auto_hub_threshold(p.n, p.mean_degree));
+  uint32_t n_hub = 0;
+  while (n_hub < m && deg[order[n_hub]] >= p.hub_threshold) ++n_hub;
+  p.n_hub = n_hub;
+
+  const bool n4 = p.n % 4 == 0, n2 = p.n % 2 == 0;
+  p.warp_v = pick_warp_shape(p.n, n4, !n4 && n2);
+  p.warp_s = pick_warp_shape(p.n, false, false);
+  p.cta_v = pick_cta_shape(p.n, n4, n2);
+  p.cta_s = pick_cta_shape(p.n, false, false);
+
+  if (m) {
+    GESPMM_CUDA(cudaMalloc(reinterpret_cast<void**>(&p.d_order), sizeof(uint32_t) * m),
+                "plan_create");
+    GESPMM_CUDA(cudaMemcpyAsync(p.d_order, order.data(), sizeof(uint32_t) * m,
+                                cudaMemcpyHostToDevice, st),
+                "plan_create");
+    GESPMM_CUDA(cudaStreamSynchronize(st), "plan_create");
+  }
+  if (n_hub) {
+    GESPMM_CUDA(cudaStreamCreateWithFlags(&p.side, cudaStreamNonBlocking), "plan_create");
+    GESPMM_CUDA(cudaEventCreateWithFlags(&p.ev_fork, cudaEventDisableTiming), "plan_create");
+    GESPMM_CUDA(cudaEventCreateWithFlags(&p.ev_join, cudaEventDisableTiming), "plan_create");
+  }
+  char buf[320];
+  std::snprintf(buf, sizeof buf,
+                "tuned: warp(vec=%d,lpr=%d,cf=%d) rows=%u; cta(vec=%d,warps=%d) hub_rows=%u "
+                "(deg>=%u); mean_deg=%.1f max_deg=%u",
+                p.warp_v.vec, p.warp_v.lpr, p.warp_v.cf, m - n_hub, p.cta_v.vec, p.cta_v.warps,
+                n_hub, p.hub_threshold, p.mean_degree, maxd);
+  p.desc = buf;
+  return GESPMM_OK;
+}
+
+gespmm_status_t plan_create_impl(const gespmm_csr_t* a, uint32_t n, gespmm_reduce_t op,
+                                 const gespmm_options_t* opts, cudaStream_t st,
+                                 const uint32_t* host_rp, Plan** out) {
+  gespmm_options_t o;
+  if (opts) o = *opts; else gespmm_options_default(&o);
+  gespmm_status_t s = check_opts(o);
+  if (s != GESPMM_OK) return s;
+  s = check_op(op, nullptr);
+  if (s != GESPMM_OK) return s;
+  if (n == 0 && a->n_rows != 0) return fail(GESPMM_EINVAL, "native_spmm: N must be >= 1");
+  auto p = std::make_unique<Plan>();
+  p->a = *a;
+  p->n = n;
+  p->op = op;
+  p->o = o;
+  cudaGetDevice(&p->device);
+  if (o.variant == GESPMM_VARIANT_TUNED && a->n_rows > 0) {
+    std::vector<uint32_t> tmp;
+    if (!host_rp) {
+      tmp.resize(size_t(a->n_rows) + 1);
+      GESPMM_CUDA(cudaMemcpyAsync(tmp.data(), a->row_ptr, sizeof(uint32_t) * tmp.size(),
+                                  cudaMemcpyDeviceToHost, st),
+                  "plan_create");
+      GESPMM_CUDA(cudaStreamSynchronize(st), "plan_create");
+      host_rp = tmp.data();
+    }
+    s = build_tuned(*p, host_rp, st);
+    if (s != GESPMM_OK) return s;
+  } else {
+    char buf[128];
+    const char* names[] = {"tuned", "naive", "crc", "crc-cwm"};
+    std::snprintf(buf, sizeof buf, "%s(cf=%u)", names[o.variant],
+                  o.variant == GESPMM_VARIANT_CRC_CWM ? o.cf : 1u);
+    p->desc = buf;
+  }
+  *out = p.release();
+  return GESPMM_OK;
+}
+
+gespmm_status_t plan_execute_impl(Plan& p, const float* b, float* c, int32_t* arg,
+                                  cudaStream_t st) {
+  gespmm_status_t s = check_op(p.op, arg);
+  if (s != GESPMM_OK) return s;
+  if (p.a.n_rows == 0) return GESPMM_OK;
+  SpmmArgs args{};
+  args.row_ptr = p.a.row_ptr;
+  args.col_ind = p.a.col_ind;
+  args.vals = p.a.vals;
+  args.b = b;
+  args.c = c;
+  args.arg = arg;
+  args.n = p.n;
+  args.arg_col = p.o.arg_kind == GESPMM_ARG_COLUMN;
+  args.skip_tail = p.o.fault_skip_tail;
+  args.hints = p.o.l2_hints;
+  const bool fast = p.o.exact == 0;
+  if (p.o.variant != GESPMM_VARIANT_TUNED) {
+    args.order = nullptr;
+    args.n_sched = p.a.n_rows;
+    args.n_tiles = faithful_tiles(p.o.variant, p.o.cf, p.n);
+    GESPMM_CUDA(launch_faithful(p.o.variant, p.o.cf, p.op, fast, args, st), "spmm");
+    return GESPMM_OK;
+  }
+  const bool v_ok = aligned(b, 16) && aligned(c, 16) && (!arg || aligned(arg, 16));
+  const WarpShape& ws = v_ok ? p.warp_v : p.warp_s;
+  const CtaShape& cs = v_ok ? p.cta_v : p.cta_s;
+  const bool v2_ok = aligned(b, 8) && aligned(c, 8) && (!arg || aligned(arg, 8));
+  const WarpShape& wsel = (ws.vec == 2 && !v2_ok) ? p.warp_s : ws;
+  if (p.n_hub) {
+    SpmmArgs h = args;
+    h.order = p.d_order;
+    h.n_sched = p.n_hub;
+    const uint32_t tw = uint32_t(cs.vec * cs.warps * 32);
+    h.n_tiles = (p.n + tw - 1) / tw;
+    GESPMM_CUDA(cudaEventRecord(p.ev_fork, st), "spmm");
+    GESPMM_CUDA(cudaStreamWaitEvent(p.side, p.ev_fork, 0), "spmm");
+    GESPMM_CUDA(launch_tuned_cta(cs, p.op, fast, h, p.side), "spmm");
+    GESPMM_CUDA(cudaEventRecord(p.ev_join, p.side), "spmm");
+  }
+  args.order = p.d_order + p.n_hub;
+  args.n_sched = p.a.n_rows - p.n_hub;
+  args.n_tiles = (p.n + wsel.tile_width() - 1) / wsel.tile_width();
+  if (args.n_sched) GESPMM_CUDA(launch_tuned_warp(wsel, p.op, fast, args, st), "spmm");
+  if (p.n_hub) GESPMM_CUDA(cudaStreamWaitEvent(st, p.ev_join, 0), "spmm");
+  return GESPMM_OK;
+}
+
+// Small LRU of plans for the plan-less device entry point: keyed by the CSR
+// arrays, shape, op and options.  A stale entry (arrays mutated in place)
+// can only cost speed: every schedule covers every row exactly once.
+struct CacheEntry {
+  gespmm_csr_t a;
+  uint32_t n;
+  gespmm_reduce_t op;
+  gespmm_options_t o;
+  int device;
+  std::unique_ptr<Plan> plan;
+};
+std::mutex g_cache_mu;
+std::list<CacheEntry> g_cache;
+constexpr size_t kCacheCap = 16;
+
+Plan* cached_plan(const gespmm_csr_t* a, uint32_t n, gespmm_reduce_t op,
+                  const gespmm_options_t& o, cudaStream_t st, const uint32_t* host_rp,
+                  gespmm_status_t* status) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(g_cache_mu);
+  for (auto it = g_cache.begin(); it != g_cache.end(); ++it) {
+    if (it->device == dev && it->n == n && it->op == op &&
+        std::memcmp(&it->a, a, sizeof(*a)) == 0 && std::memcmp(&it->o, &o, sizeof(o)) == 0) {
+      g_cache.splice(g_cache.begin(), g_cache, it);
+      *status = GESPMM_OK;
+      return g_cache.front().plan.get();
+    }
+  }
+  Plan* p = nullptr;
+  *status = plan_create_impl(a, n, op, &o, st, host_rp, &p);
+  if (*status != GESPMM_OK) return nullptr;
+  g_cache.push_front(CacheEntry{*a, n, op, o, dev, std::unique_ptr<Plan>(p)});
+  if (g_cache.size() > kCacheCap) g_cache.pop_back();
+  return p;
+}
+
+// Grow-only device staging for the host-buffer entry point.
+struct Workspace {
+  std::mutex mu;
+  cudaStream_t stream = nullptr;
+  void* buf[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+  size_t cap[6] = {0, 0, 0, 0, 0, 0};
+  cudaError_t reserve(int i, size_t bytes) {
+    if (bytes <= cap[i]) return cudaSuccess;
+    if (buf[i]) cudaFree(buf[i]);
+    buf[i] = nullptr;
+    cap[i] = 0;
+    cudaError_t e = cudaMalloc(&buf[i], bytes);
+    if (e == cudaSuccess) cap[i] = bytes;
+    return e;
+  }
+};
+std::mutex g_ws_mu;
+Workspace* g_ws[64] = {};
+
+Workspace* workspace() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(g_ws_mu);
+  if (!g_ws[dev]) {
+    g_ws[dev] = new Workspace();
+    cudaStreamCreateWithFlags(&g_ws[dev]->stream, cudaStreamNonBlocking);
+  }
+  return g_ws[dev];
+}
+
+gespmm_status_t device_validate(const gespmm_csr_t* a, cudaStream_t st, const char* who) {
+  ValidateResult r{};
+  GESPMM_CUDA(validate_csr_device(a->n_rows, a->n_cols, a->nnz, a->row_ptr, a->col_ind, &r, st),
+              "validate");
+  return validation_status(r, a->n_rows, a->n_cols, a->nnz, who);
+}
+
+}  // namespace
+}  // namespace gespmm
+
+using namespace gespmm;
+
+extern "C" {
+
+void gespmm_options_default(gespmm_options_t* o) {
+  std::memset(o, 0, sizeof(*o));
+  o->variant = GESPMM_VARIANT_TUNED;
+  o->cf = 2;
+  o->exact = 1;
+  o->arg_kind = GESPMM_ARG_EDGE;
+  o->validate = 1;
+  o->fault_skip_tail = 0;
+  o->l2_hints = 1;
+  o->hub_threshold = 0;
+}
+
+const char* gespmm_last_error(void) { return t_err.c_str(); }
+
+int32_t gespmm_abi_version(void) { return GESPMM_ABI_VERSION; }
+
+uint64_t gespmm_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
+
+gespmm_status_t gespmm_validate_device(const gespmm_csr_t* a, void* stream) {
+  if (!a) return fail(GESPMM_EINVAL, "null csr");
+  return device_validate(a, static_cast<cudaStream_t>(stream), "spmm");
+}
+
+gespmm_status_t gespmm_plan_create(const gespmm_csr_t* a, uint32_t n, gespmm_reduce_t op,
+                                   const gespmm_options_t* opts, void* stream,
+                                   gespmm_plan_t* out) {
+  if (!a || !out) return fail(GESPMM_EINVAL, "null argument");
+  Plan* p = nullptr;
+  gespmm_status_t s = plan_create_impl(a, n, op, opts, static_cast<cudaStream_t>(stream),
+                                       nullptr, &p);
+  if (s != GESPMM_OK) return s;
+  *out = reinterpret_cast<gespmm_plan_t>(p);
+  return GESPMM_OK;
+}
+
+gespmm_status_t gespmm_plan_execute(gespmm_plan_t plan, const float* b, float* c, int32_t* arg,
+                                    void* stream) {
+  if (!plan) return fail(GESPMM_EINVAL, "null plan");
+  return plan_execute_impl(*reinterpret_cast<Plan*>(plan), b, c, arg,
+                           static_cast<cudaStream_t>(stream));
+}
+
+const char* gespmm_plan_describe(gespmm_plan_t plan) {
+  return plan ? reinterpret_cast<Plan*>(plan)->desc.c_str() : "";
+}
+
+int32_t gespmm_plan_launches(gespmm_plan_t plan) {
+  if (!plan) return 0;
+  const Plan* p = reinterpret_cast<Plan*>(plan);
+  if (p->a.n_rows == 0) return 0;
+  if (p->o.variant != GESPMM_VARIANT_TUNED) return 1;
+  return (p->n_hub ? 1 : 0) + (p->a.n_rows > p->n_hub ? 1 : 0);
+}
+
+void gespmm_plan_destroy(gespmm_plan_t plan) { delete reinterpret_cast<Plan*>(plan); }
+
+gespmm_status_t gespmm_spmm_device(const gespmm_csr_t* a, const float* b, uint32_t n,
+                                   gespmm_reduce_t op, float* c, int32_t* arg,
+                                   const gespmm_options_t* opts, void* stream) {
+  if (!a) return fail(GESPMM_EINVAL, "null csr");
+  gespmm_options_t o;
+  if (opts) o = *opts; else gespmm_options_default(&o);
+  gespmm_status_t s = check_opts(o);
+  if (s != GESPMM_OK) return s;
+  s = check_op(op, arg);
+  if (s != GESPMM_OK) return s;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (o.validate) {
+    s = device_validate(a, st, "spmm");
+    if (s != GESPMM_OK) return s;
+  }
+  if (a->n_rows == 0) return GESPMM_OK;
+  if (n == 0) return fail(GESPMM_EINVAL, "native_spmm: N must be >= 1");
+  o.validate = 0;  // not part of the plan identity
+  Plan* p = cached_plan(a, n, op, o, st, nullptr, &s);
+  if (!p) return s;
+  return plan_execute_impl(*p, b, c, arg, st);
+}
+
+gespmm_status_t gespmm_spmm_host(const gespmm_csr_t* a, const float* b, uint32_t b_rows,
+                                 uint32_t n, gespmm_reduce_t op, float* c, int32_t* arg,
+                                 const gespmm_options_t* opts) {
+  if (!a) return fail(GESPMM_EINVAL, "null csr");
+  gespmm_options_t o;
+  if (opts) o = *opts; else gespmm_options_default(&o);
+  gespmm_status_t s = check_op(op, arg);
+  if (s != GESPMM_OK) return s;
+  if (a->n_cols != b_rows) {
+    char buf[160];
+    std::snprintf(buf, sizeof buf, "spmm: dimension mismatch: A is %ux%u but B has %u rows",
+                  a->n_rows, a->n_cols, b_rows);
+    return fail(GESPMM_EDIM, buf);
+  }
+  Workspace* ws = workspace();
+  std::lock_guard<std::mutex> lk(ws->mu);
+  cudaStream_t st = ws->stream;
+  const uint64_t m = a->n_rows, nnz = a->nnz;
+  GESPMM_CUDA(ws->reserve(0, sizeof(uint32_t) * (m + 1)), "spmm");
+  GESPMM_CUDA(ws->reserve(1, sizeof(uint32_t) * std::max<uint64_t>(nnz, 1)), "spmm");
+  GESPMM_CUDA(ws->reserve(2, sizeof(float) * std::max<uint64_t>(nnz, 1)), "spmm");
+  GESPMM_CUDA(cudaMemcpyAsync(ws->buf[0], a->row_ptr, sizeof(uint32_t) * (m + 1),
+                              cudaMemcpyHostToDevice, st), "spmm");
+  if (nnz) {
+    GESPMM_CUDA(cudaMemcpyAsync(ws->buf[1], a->col_ind, sizeof(uint32_t) * nnz,
+                                cudaMemcpyHostToDevice, st), "spmm");
+    GESPMM_CUDA(cudaMemcpyAsync(ws->buf[2], a->vals, sizeof(float) * nnz,
+                                cudaMemcpyHostToDevice, st), "spmm");
+  }
+  gespmm_csr_t d = *a;
+  d.row_ptr = static_cast<const uint32_t*>(ws->buf[0]);
+  d.col_ind = static_cast<const uint32_t*>(ws->buf[1]);
+  d.vals = static_cast<const float*>(ws->buf[2]);
+  if (o.validate) {
+    s = device_validate(&d, st, "spmm");
+    if (s != GESPMM_OK) return s;
+  }
+  s = check_opts(o);
+  if (s != GESPMM_OK) return s;
+  if (m == 0) return GESPMM_OK;
+  if (n == 0) return fail(GESPMM_EINVAL, "native_spmm: N must be >= 1");
+  const uint64_t bsz = uint64_t(b_rows) * n, csz = m * n;
+  GESPMM_CUDA(ws->reserve(3, sizeof(float) * std::max<uint64_t>(bsz, 1)), "spmm");
+  GESPMM_CUDA(ws->reserve(4, sizeof(float) * csz), "spmm");
+  if (arg) GESPMM_CUDA(ws->reserve(5, sizeof(int32_t) * csz), "spmm");
+  if (bsz)
+    GESPMM_CUDA(cudaMemcpyAsync(ws->buf[3], b, sizeof(float) * bsz, cudaMemcpyHostToDevice, st),
+                "spmm");
+  o.validate = 0;
+  Plan* p = nullptr;
+  std::unique_ptr<Plan> owned;
+  if (o.variant == GESPMM_VARIANT_TUNED) {
+    // host row_ptr is at hand: inspect it directly (no D2H); not cached, the
+    // staging buffers are reused across calls with different matrices.
+    s = plan_create_impl(&d, n, op, &o, st, a->row_ptr, &p);
+    if (s != GESPMM_OK) return s;
+    owned.reset(p);
+  } else {
+    s = plan_create_impl(&d, n, op, &o, st, nullptr, &p);
+    if (s != GESPMM_OK) return s;
+    owned.reset(p);
+  }
+  s = plan_execute_impl(*p, static_cast<const float*>(ws->buf[3]), static_cast<float*>(ws->buf[4]),
+                        arg ? static_cast<int32_t*>(ws->buf[5]) : nullptr, st);
+  if (s != GESPMM_OK) return s;
+  GESPMM_CUDA(cudaMemcpyAsync(c, ws->buf[4], sizeof(float) * csz, cudaMemcpyDeviceToHost, st),
+              "spmm");
+  if (arg)
+    GESPMM_CUDA(cudaMemcpyAsync(arg, ws->buf[5], sizeof(int32_t) * csz, cudaMemcpyDeviceToHost, st),
+                "spmm");
+  GESPMM_CUDA(cudaStreamSynchronize(st), "spmm");
+  return GESPMM_OK;
+}
+
+void gespmm_select_variant(uint32_t n, int32_t* variant, uint32_t* cf) {
+  if (n <= 32) {
+    *variant = GESPMM_VARIANT_CRC;
+    *cf = 1;
+  } else {
+    *variant = GESPMM_VARIANT_CRC_CWM;
+    *cf = 2;
+  }
+}
+
+gespmm_status_t gespmm_reduce_by_name(const char* name, gespmm_reduce_t* out) {
+  const std::string s = name ? name : "";
+  if (s == "sum") *out = GESPMM_SUM;
+  else if (s == "mean") *out = GESPMM_MEAN;
+  else if (s == "max") *out = GESPMM_MAX;
+  else if (s == "min") *out = GESPMM_MIN;
+  else return fail(GESPMM_EINVAL, "unknown reduce op '" + s + "' (built-ins: sum, mean, max, min)");
+  return GESPMM_OK;
+}
+
+gespmm_status_t gespmm_device_info(int32_t* sm_count, int64_t* l2_bytes,
+                                   int64_t* persisting_l2_max, int32_t* cc_major,
+                                   int32_t* cc_minor) {
+  int dev = 0;
+  GESPMM_CUDA(cudaGetDevice(&dev), "device_info");
+  cudaDeviceProp prop;
+  GESPMM_CUDA(cudaGetDeviceProperties(&prop, dev), "device_info");
+  if (sm_count) *sm_count = prop.multiProcessorCount;
+  if (l2_bytes) *l2_bytes = prop.l2CacheSize;
+  if (persisting_l2_max) *persisting_l2_max = prop.persistingL2CacheMaxSize;
+  if (cc_major) *cc_major = prop.major;
+  if (cc_minor) *cc_minor = prop.minor;
+  return GESPMM_OK;
+}
+
+}  // extern "C"

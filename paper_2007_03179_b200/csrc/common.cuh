@@ -1,0 +1,230 @@
+// Shared device-side pieces of the B200 GE-SpMM kernels: the fused reduce
+// functors (replacing the reference's function-pointer ReduceOp,
+// /root/reference/proj/include/spmm/reduce_op.hpp:14-28) and cache-hinted
+// loads/stores (sm_100a PTX).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "gespmm/gespmm.h"
+
+namespace gespmm {
+
+// ---------------------------------------------------------------------------
+// Reduce ops, fused in-register.  Each output element is folded by exactly one
+// thread in ascending CSR position, so with separate round-to-nearest multiply
+// and combine (exact mode) every variant is bit-identical to the reference's
+// ordered fold (kernel.hpp:218/271/331: acc = op.fold(acc, v * b)).
+// ---------------------------------------------------------------------------
+enum : int { kSum = GESPMM_SUM, kMean = GESPMM_MEAN, kMax = GESPMM_MAX, kMin = GESPMM_MIN };
+
+template <int OP>
+struct Reduce;
+
+template <>
+struct Reduce<kSum> {
+  static constexpr bool kHasArg = false;
+  __device__ __forceinline__ static float init() { return 0.0f; }
+  template <bool FAST>
+  __device__ __forceinline__ static void fold(float& acc, int32_t&, float v, float b, int32_t) {
+    if (FAST)
+      acc = __fmaf_rn(v, b, acc);
+    else
+      acc = __fadd_rn(acc, __fmul_rn(v, b));  // FMUL + FADD, never contracted
+  }
+};
+
+template <>
+struct Reduce<kMean> : Reduce<kSum> {};
+
+template <>
+struct Reduce<kMax> {
+  static constexpr bool kHasArg = true;
+  __device__ __forceinline__ static float init() { return -3.402823466e+38f; }  // lowest()
+  template <bool FAST>
+  __device__ __forceinline__ static void fold(float& acc, int32_t& who, float v, float b,
+                                              int32_t pos) {
+    const float x = __fmul_rn(v, b);
+    // reference max_f32(a, b) = a < b ? b : a  (reduce_op.hpp:25): strict, so
+    // ties keep the earlier element and NaN products never enter.
+    if (acc < x) {
+      acc = x;
+      who = pos;
+    }
+  }
+};
+
+template <>
+struct Reduce<kMin> {
+  static constexpr bool kHasArg = true;
+  __device__ __forceinline__ static float init() { return 3.402823466e+38f; }  // max()
+  template <bool FAST>
+  __device__ __forceinline__ static void fold(float& acc, int32_t& who, float v, float b,
+                                              int32_t pos) {
+    const float x = __fmul_rn(v, b);
+    if (x < acc) {
+      acc = x;
+      who = pos;
+    }
+  }
+};
+
+// mean = sum / float(row length); an empty row keeps the sum seed.
+template <int OP>
+__device__ __forceinline__ float finish(float acc, uint32_t row_len) {
+  if (OP == kMean && row_len > 0) return __fdiv_rn(acc, static_cast<float>(row_len));
+  return acc;
+}
+
+// ---------------------------------------------------------------------------
+// L2 cache policies.  B (the gathered dense rows, re-read ~nnz/K times) is
+// kept with evict_last; the streamed CSR arrays and the written C use
+// evict_first so they do not push B out of the 126 MB L2.  With hints off both
+// policies are evict_normal (same code path).
+// ---------------------------------------------------------------------------
+struct Policies {
+  uint64_t keep;    // for B
+  uint64_t stream;  // for CSR and C
+};
+
+__device__ __forceinline__ Policies make_policies(int hints) {
+  Policies p;
+  if (hints) {
+    asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p.keep));
+    asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p.stream));
+  } else {
+    asm("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p.keep));
+    p.stream = p.keep;
+  }
+  return p;
+}
+
+// Streamed sparse arrays: read once, do not allocate in L1.
+__device__ __forceinline__ uint32_t ld_stream_u32(const uint32_t* ptr, uint64_t pol) {
+  uint32_t r;
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %2;"
+      : "=r"(r)
+      : "l"(ptr), "l"(pol));
+  return r;
+}
+__device__ __forceinline__ float ld_stream_f32(const float* ptr, uint64_t pol) {
+  float r;
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.f32 %0, [%1], %2;"
+      : "=f"(r)
+      : "l"(ptr), "l"(pol));
+  return r;
+}
+
+// Gathered dense rows of B: L1-allocating (hub rows hit), L2 evict_last.
+template <int VEC>
+struct Vec;
+template <>
+struct Vec<1> {
+  float x[1];
+};
+template <>
+struct Vec<2> {
+  float x[2];
+};
+template <>
+struct Vec<4> {
+  float x[4];
+};
+
+template <int VEC>
+__device__ __forceinline__ Vec<VEC> ld_keep(const float* ptr, uint64_t pol);
+
+template <>
+__device__ __forceinline__ Vec<1> ld_keep<1>(const float* ptr, uint64_t pol) {
+  Vec<1> r;
+  asm("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(r.x[0]) : "l"(ptr), "l"(pol));
+  return r;
+}
+template <>
+__device__ __forceinline__ Vec<2> ld_keep<2>(const float* ptr, uint64_t pol) {
+  Vec<2> r;
+  asm("ld.global.nc.L2::cache_hint.v2.f32 {%0, %1}, [%2], %3;"
+      : "=f"(r.x[0]), "=f"(r.x[1])
+      : "l"(ptr), "l"(pol));
+  return r;
+}
+template <>
+__device__ __forceinline__ Vec<4> ld_keep<4>(const float* ptr, uint64_t pol) {
+  Vec<4> r;
+  asm("ld.global.nc.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], %5;"
+      : "=f"(r.x[0]), "=f"(r.x[1]), "=f"(r.x[2]), "=f"(r.x[3])
+      : "l"(ptr), "l"(pol));
+  return r;
+}
+
+// Output stores: written once, streamed past L1, evict_first in L2.
+template <int VEC>
+__device__ __forceinline__ void st_stream(float* ptr, const float* v, uint64_t pol);
+template <>
+__device__ __forceinline__ void st_stream<1>(float* ptr, const float* v, uint64_t pol) {
+  asm volatile("st.global.L1::no_allocate.L2::cache_hint.f32 [%0], %1, %2;" ::"l"(ptr),
+               "f"(v[0]), "l"(pol)
+               : "memory");
+}
+template <>
+__device__ __forceinline__ void st_stream<2>(float* ptr, const float* v, uint64_t pol) {
+  asm volatile("st.global.L1::no_allocate.L2::cache_hint.v2.f32 [%0], {%1, %2}, %3;" ::"l"(ptr),
+               "f"(v[0]), "f"(v[1]), "l"(pol)
+               : "memory");
+}
+template <>
+__device__ __forceinline__ void st_stream<4>(float* ptr, const float* v, uint64_t pol) {
+  asm volatile(
+      "st.global.L1::no_allocate.L2::cache_hint.v4.f32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(ptr),
+      "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "l"(pol)
+      : "memory");
+}
+
+template <int VEC>
+__device__ __forceinline__ void st_stream_i32(int32_t* ptr, const int32_t* v, uint64_t pol);
+template <>
+__device__ __forceinline__ void st_stream_i32<1>(int32_t* ptr, const int32_t* v, uint64_t pol) {
+  asm volatile("st.global.L1::no_allocate.L2::cache_hint.b32 [%0], %1, %2;" ::"l"(ptr),
+               "r"(v[0]), "l"(pol)
+               : "memory");
+}
+template <>
+__device__ __forceinline__ void st_stream_i32<2>(int32_t* ptr, const int32_t* v, uint64_t pol) {
+  asm volatile("st.global.L1::no_allocate.L2::cache_hint.v2.b32 [%0], {%1, %2}, %3;" ::"l"(ptr),
+               "r"(v[0]), "r"(v[1]), "l"(pol)
+               : "memory");
+}
+template <>
+__device__ __forceinline__ void st_stream_i32<4>(int32_t* ptr, const int32_t* v, uint64_t pol) {
+  asm volatile(
+      "st.global.L1::no_allocate.L2::cache_hint.v4.b32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(ptr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "l"(pol)
+      : "memory");
+}
+
+// SkipTail fault hook (reference kernel.hpp:174-180 faulted_row_end, ws = 32).
+__device__ __forceinline__ uint32_t faulted_end(uint32_t start, uint32_t end, int skip_tail) {
+  if (!skip_tail || end <= start) return end;
+  const uint32_t tiles = (end - start + 31u) >> 5;
+  return start + (tiles - 1u) * 32u;
+}
+
+// Launch parameters shared by every SpMM kernel.
+struct SpmmArgs {
+  const uint32_t* row_ptr;
+  const uint32_t* col_ind;
+  const float* vals;
+  const float* b;
+  float* c;
+  int32_t* arg;
+  const uint32_t* order;  // row schedule (nullable -> identity)
+  uint32_t n_sched;       // rows in the schedule
+  uint32_t n;             // dense width N
+  uint32_t n_tiles;       // column tiles per row
+  int arg_col;            // arg = col_ind[p] instead of p
+  int skip_tail;
+  int hints;
+};
+
+}  // namespace gespmm

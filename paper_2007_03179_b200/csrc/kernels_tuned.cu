@@ -1,0 +1,357 @@
+// Tuned B200 SpMM-like kernels (the product path).
+//
+// k_warp — row per (sub)warp.  Coalesced Row Caching: the LPR lanes that own a
+//   row load the next LPR (col, val) pairs of the row with one coalesced load
+//   each (prefetched one chunk ahead) and broadcast them with shuffles, so
+//   col_ind/vals are read once per row tile.  Lanes own VEC contiguous columns
+//   and gather B rows with 16-byte (float4) loads.  Coarse-grained Warp
+//   Merging: each lane owns CF column sub-tiles, so one staged nonzero feeds
+//   CF vector gathers.  U nonzeros are gathered before any is folded (memory-
+//   level parallelism), then folded in ascending position: every output
+//   element is still reduced by one thread in CSR order, so results are
+//   bit-identical to the reference fold (kernel.hpp:287-343) in exact mode.
+//
+// k_cta — row per CTA, for hub rows of power-law graphs.  The CTA stages the
+//   row's sparse segment into shared memory (double-buffered), and its warps
+//   split the COLUMNS of the row (never the nonzeros), keeping the per-element
+//   ascending fold and with it bit-exactness; a deeper gather batch (32 scalar
+//   or 8 vector loads per lane) gives the hub the latency hiding a single warp
+//   cannot.
+#include <algorithm>
+
+#include "common.cuh"
+#include "launch.h"
+
+namespace gespmm {
+namespace {
+
+constexpr unsigned kFull = 0xffffffffu;
+
+template <int OP, bool FAST, int VEC, int LPR, int CF>
+__global__ void __launch_bounds__(256, 3) k_warp(SpmmArgs a) {
+  using R = Reduce<OP>;
+  constexpr int RPW = 32 / LPR;                     // rows per warp
+  constexpr int U0 = 8 / CF;
+  constexpr int U = U0 < LPR ? U0 : LPR;            // gather batch; LPR % U == 0
+  constexpr uint32_t SUB = uint32_t(VEC * LPR);     // columns per sub-tile
+  constexpr uint32_t TW = SUB * CF;                 // columns per tile
+  static_assert(LPR % U == 0, "batch must divide the staging chunk");
+
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t unit = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t groups = (uint64_t(a.n_sched) + RPW - 1) / RPW;
+  if (unit >= groups * a.n_tiles) return;  // warp-uniform exit
+  const Policies pol = make_policies(a.hints);
+
+  const uint32_t group = uint32_t(unit / a.n_tiles);
+  const uint32_t tile = uint32_t(unit % a.n_tiles);
+  const uint32_t sub = lane / LPR;
+  const uint32_t sl = lane % LPR;
+  const uint32_t sidx = group * RPW + sub;
+  const bool row_ok = sidx < a.n_sched;
+  const uint32_t row = row_ok ? (a.order ? a.order[sidx] : sidx) : 0u;
+  uint32_t start = 0, full_end = 0;
+  if (row_ok) {
+    start = a.row_ptr[row];
+    full_end = a.row_ptr[row + 1];
+  }
+  const uint32_t len = faulted_end(start, full_end, a.skip_tail) - start;
+  const uint32_t maxlen = RPW == 1 ? len : __reduce_max_sync(kFull, len);
+
+  const uint32_t col0 = tile * TW + sl * uint32_t(VEC);
+  bool colok[CF];
+  float acc[CF][VEC];
+  int32_t who[CF][VEC];
+#pragma unroll
+  for (int c = 0; c < CF; ++c) {
+    colok[c] = row_ok && (col0 + c * SUB) < a.n;
+#pragma unroll
+    for (int e = 0; e < VEC; ++e) {
+      acc[c][e] = R::init();
+      who[c][e] = -1;
+    }
+  }
+  // column offsets of the lane's sub-tiles; masked sub-tiles read column 0
+  uint32_t coff[CF];
+#pragma unroll
+  for (int c = 0; c < CF; ++c) coff[c] = colok[c] ? col0 + c * SUB : 0u;
+  const uint32_t* ci = a.col_ind + start;
+  const float* vs = a.vals + start;
+
+  // phase-1 staging, one chunk ahead
+  uint32_t kc = 0;
+  float vv = 0.0f;
+  if (sl < len) {
+    kc = ld_stream_u32(ci + sl, pol.stream);
+    vv = ld_stream_f32(vs + sl, pol.stream);
+  }
+  for (uint32_t off = 0; off < maxlen; off += LPR) {
+    const uint32_t cur_k = kc;
+    const float cur_v = vv;
+    const uint32_t nxt = off + LPR + sl;
+    if (nxt < len) {
+      kc = ld_stream_u32(ci + nxt, pol.stream);
+      vv = ld_stream_f32(vs + nxt, pol.stream);
+    }
+    const uint32_t chunk = min(uint32_t(LPR), maxlen - off);
+    for (uint32_t kk = 0; kk < chunk; kk += U) {
+      uint32_t k[U];
+      float v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        k[u] = __shfl_sync(kFull, cur_k, int(sub * LPR + kk + u));
+        v[u] = __shfl_sync(kFull, cur_v, int(sub * LPR + kk + u));
+      }
+      // Unpredicated gathers (slots past the row end re-read a valid row:
+      // k comes from a lane holding an earlier/zero index), so ptxas issues
+      // all U*CF loads back to back instead of interleaving them with folds.
+      Vec<VEC> bv[U][CF];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const float* brow = a.b + uint64_t(k[u]) * a.n;
+#pragma unroll
+        for (int c = 0; c < CF; ++c) bv[u][c] = ld_keep<VEC>(brow + coff[c], pol.keep);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (off + kk + u < len) {
+          const int32_t pos = a.arg_col ? int32_t(k[u]) : int32_t(start + off + kk + u);
+#pragma unroll
+          for (int c = 0; c < CF; ++c)
+            if (colok[c]) {
+#pragma unroll
+              for (int e = 0; e < VEC; ++e)
+                R::template fold<FAST>(acc[c][e], who[c][e], v[u], bv[u][c].x[e], pos);
+            }
+        }
+      }
+    }
+  }
+
+  const uint32_t row_len = full_end - start;
+#pragma unroll
+  for (int c = 0; c < CF; ++c) {
+    if (!colok[c]) continue;
+    float out[VEC];
+#pragma unroll
+    for (int e = 0; e < VEC; ++e) out[e] = finish<OP>(acc[c][e], row_len);
+    const uint64_t o = uint64_t(row) * a.n + col0 + c * SUB;
+    st_stream<VEC>(a.c + o, out, pol.stream);
+    if (R::kHasArg && a.arg) st_stream_i32<VEC>(a.arg + o, who[c], pol.stream);
+  }
+}
+
+template <int OP, bool FAST, int VEC, int WARPS>
+__global__ void __launch_bounds__(WARPS * 32) k_cta(SpmmArgs a) {
+  using R = Reduce<OP>;
+  constexpr int THREADS = WARPS * 32;
+  constexpr int CHUNK = 256;                 // staged nonzeros per phase
+  constexpr int PER_T = CHUNK / THREADS;     // staged entries per thread
+  constexpr int U = 32 / VEC;                // gather batch per lane
+  constexpr uint32_t TW = uint32_t(WARPS * 32 * VEC);
+  static_assert(CHUNK % THREADS == 0 && CHUNK % U == 0, "chunk geometry");
+  __shared__ uint2 s_kv[2][CHUNK];
+
+  const uint32_t unit = blockIdx.x;
+  const uint32_t sidx = unit / a.n_tiles;
+  const uint32_t tile = unit % a.n_tiles;
+  if (sidx >= a.n_sched) return;
+  const Policies pol = make_policies(a.hints);
+  const uint32_t row = a.order ? a.order[sidx] : sidx;
+  const uint32_t start = a.row_ptr[row];
+  const uint32_t full_end = a.row_ptr[row + 1];
+  const uint32_t len = faulted_end(start, full_end, a.skip_tail) - start;
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t col0 = tile * TW + warp * (32u * VEC) + lane * uint32_t(VEC);
+  const bool colok = col0 < a.n;
+  const uint32_t* ci = a.col_ind + start;
+  const float* vs = a.vals + start;
+
+  float acc[VEC];
+  int32_t who[VEC];
+#pragma unroll
+  for (int e = 0; e < VEC; ++e) {
+    acc[e] = R::init();
+    who[e] = -1;
+  }
+
+  // stage chunk 0
+#pragma unroll
+  for (int t = 0; t < PER_T; ++t) {
+    const uint32_t i = threadIdx.x + t * THREADS;
+    if (i < len)
+      s_kv[0][i] = make_uint2(ld_stream_u32(ci + i, pol.stream),
+                              __float_as_uint(ld_stream_f32(vs + i, pol.stream)));
+  }
+  __syncthreads();
+
+  const float* bcol = a.b + col0;
+  for (uint32_t off = 0, buf = 0; off < len; off += CHUNK, buf ^= 1u) {
+    // issue the next chunk's sparse loads before consuming this one
+    uint2 nxt[PER_T];
+#pragma unroll
+    for (int t = 0; t < PER_T; ++t) {
+      const uint32_t i = off + CHUNK + threadIdx.x + t * THREADS;
+      nxt[t] = make_uint2(0u, 0u);
+      if (i < len)
+        nxt[t] = make_uint2(ld_stream_u32(ci + i, pol.stream),
+                            __float_as_uint(ld_stream_f32(vs + i, pol.stream)));
+    }
+    const uint32_t n_cur = min(uint32_t(CHUNK), len - off);
+    for (uint32_t kk = 0; kk < n_cur; kk += U) {
+      uint2 kv[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) kv[u] = s_kv[buf][kk + u];
+      Vec<VEC> bv[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+#pragma unroll
+        for (int e = 0; e < VEC; ++e) bv[u].x[e] = 0.0f;
+        if (colok && kk + u < n_cur) bv[u] = ld_keep<VEC>(bcol + uint64_t(kv[u].x) * a.n, pol.keep);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (kk + u < n_cur) {
+          const int32_t pos = a.arg_col ? int32_t(kv[u].x) : int32_t(start + off + kk + u);
+          const float v = __uint_as_float(kv[u].y);
+#pragma unroll
+          for (int e = 0; e < VEC; ++e) R::template fold<FAST>(acc[e], who[e], v, bv[u].x[e], pos);
+        }
+      }
+    }
+#pragma unroll
+    for (int t = 0; t < PER_T; ++t) s_kv[buf ^ 1u][threadIdx.x + t * THREADS] = nxt[t];
+    __syncthreads();
+  }
+
+  if (colok) {
+    float out[VEC];
+#pragma unroll
+    for (int e = 0; e < VEC; ++e) out[e] = finish<OP>(acc[e], full_end - start);
+    const uint64_t o = uint64_t(row) * a.n + col0;
+    st_stream<VEC>(a.c + o, out, pol.stream);
+    if (R::kHasArg && a.arg) st_stream_i32<VEC>(a.arg + o, who, pol.stream);
+  }
+}
+
+// ---- dispatch tables ------------------------------------------------------
+
+template <int OP, bool FAST>
+cudaError_t warp_dispatch(const WarpShape& s, const SpmmArgs& a, cudaStream_t st) {
+  const uint32_t rpw = 32u / uint32_t(s.lpr);
+  const uint64_t groups = (uint64_t(a.n_sched) + rpw - 1) / rpw;
+  const uint64_t warps = groups * a.n_tiles;
+  const uint64_t blocks = (warps + 7) / 8;
+  if (blocks == 0) return cudaSuccess;
+  if (blocks > 0x7fffffffull) return cudaErrorInvalidConfiguration;
+  const dim3 g{uint32_t(blocks)}, b{256};
+#define GESPMM_W(V, L, F)                                   \
+  if (s.vec == V && s.lpr == L && s.cf == F) {              \
+    k_warp<OP, FAST, V, L, F><<<g, b, 0, st>>>(a);          \
+    note_launch();                                          \
+    return cudaGetLastError();                              \
+  }
+  GESPMM_W(4, 4, 1) GESPMM_W(4, 8, 1) GESPMM_W(4, 16, 1) GESPMM_W(4, 32, 1)
+  GESPMM_W(4, 32, 2) GESPMM_W(4, 32, 4)
+  GESPMM_W(2, 32, 1) GESPMM_W(2, 32, 2) GESPMM_W(2, 32, 4)
+  GESPMM_W(1, 1, 1) GESPMM_W(1, 2, 1) GESPMM_W(1, 4, 1) GESPMM_W(1, 8, 1)
+  GESPMM_W(1, 16, 1) GESPMM_W(1, 32, 1) GESPMM_W(1, 32, 2) GESPMM_W(1, 32, 4)
+#undef GESPMM_W
+  return cudaErrorInvalidValue;
+}
+
+template <int OP, bool FAST>
+cudaError_t cta_dispatch(const CtaShape& s, const SpmmArgs& a, cudaStream_t st) {
+  const uint64_t blocks = uint64_t(a.n_sched) * a.n_tiles;
+  if (blocks == 0) return cudaSuccess;
+  if (blocks > 0x7fffffffull) return cudaErrorInvalidConfiguration;
+  const dim3 g{uint32_t(blocks)};
+#define GESPMM_C(V, W)                                          \
+  if (s.vec == V && s.warps == W) {                             \
+    k_cta<OP, FAST, V, W><<<g, dim3(W * 32), 0, st>>>(a);       \
+    note_launch();                                              \
+    return cudaGetLastError();                                  \
+  }
+  GESPMM_C(1, 1) GESPMM_C(1, 2) GESPMM_C(1, 4) GESPMM_C(1, 8)
+  GESPMM_C(4, 2) GESPMM_C(4, 4) GESPMM_C(4, 8)
+#undef GESPMM_C
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace
+
+bool tuned_shape_supported(const WarpShape& s) {
+  static const int table[][3] = {{4, 4, 1},  {4, 8, 1},  {4, 16, 1}, {4, 32, 1}, {4, 32, 2},
+                                 {4, 32, 4}, {2, 32, 1}, {2, 32, 2}, {2, 32, 4}, {1, 1, 1},
+                                 {1, 2, 1},  {1, 4, 1},  {1, 8, 1},  {1, 16, 1}, {1, 32, 1},
+                                 {1, 32, 2}, {1, 32, 4}};
+  for (const auto& t : table)
+    if (t[0] == s.vec && t[1] == s.lpr && t[2] == s.cf) return true;
+  return false;
+}
+
+// N -> (VEC, LPR, CF): the smallest sub-warp whose VEC-wide lanes cover N
+// (several short rows per warp when N < 128), then the CWM merge factor so a
+// warp covers up to 4 sub-tiles of one row before the row is re-staged.
+WarpShape pick_warp_shape(uint32_t n, bool vec4_ok, bool vec2_ok) {
+  WarpShape s;
+  s.vec = vec4_ok ? 4 : (vec2_ok ? 2 : 1);
+  if (n < 16 || (s.vec == 2 && n < 64)) s.vec = 1;  // narrow rows: scalar lanes waste less
+  const uint32_t lanes = (n + uint32_t(s.vec) - 1) / uint32_t(s.vec);
+  if (lanes >= 32) {
+    s.lpr = 32;
+    const uint32_t sub = 32u * uint32_t(s.vec);
+    const uint32_t tiles = (n + sub - 1) / sub;
+    s.cf = tiles >= 4 ? 4 : (tiles >= 2 ? 2 : 1);
+  } else {
+    int l = 1;
+    while (uint32_t(l) < lanes) l <<= 1;
+    if (s.vec == 4 && l < 4) l = 4;
+    s.lpr = l;
+    s.cf = 1;
+  }
+  return s;
+}
+
+bool cta_shape_supported(const CtaShape& s) {
+  return (s.vec == 1 && (s.warps == 1 || s.warps == 2 || s.warps == 4 || s.warps == 8)) ||
+         (s.vec == 4 && (s.warps == 2 || s.warps == 4 || s.warps == 8));
+}
+
+// Hub rows: split the columns over as many warps as give every lane a column
+// (scalar lanes up to 256 columns), wider lanes beyond that.
+CtaShape pick_cta_shape(uint32_t n, bool vec4_ok, bool /*vec2_ok*/) {
+  CtaShape s;
+  if (n <= 256 || !vec4_ok) {
+    s.vec = 1;
+    const uint32_t w = (n + 31) / 32;
+    s.warps = w >= 8 ? 8 : (w >= 4 ? 4 : (w >= 2 ? 2 : 1));
+  } else {
+    s.vec = 4;
+    const uint32_t w = (n + 127) / 128;
+    s.warps = w >= 8 ? 8 : (w >= 4 ? 4 : 2);
+  }
+  return s;
+}
+
+cudaError_t launch_tuned_warp(const WarpShape& s, int op, bool fast, const SpmmArgs& a,
+                              cudaStream_t st) {
+  switch (op) {
+    case kSum: return fast ? warp_dispatch<kSum, true>(s, a, st) : warp_dispatch<kSum, false>(s, a, st);
+    case kMean: return fast ? warp_dispatch<kMean, true>(s, a, st) : warp_dispatch<kMean, false>(s, a, st);
+    case kMax: return warp_dispatch<kMax, false>(s, a, st);
+    default: return warp_dispatch<kMin, false>(s, a, st);
+  }
+}
+
+cudaError_t launch_tuned_cta(const CtaShape& s, int op, bool fast, const SpmmArgs& a,
+                             cudaStream_t st) {
+  switch (op) {
+    case kSum: return fast ? cta_dispatch<kSum, true>(s, a, st) : cta_dispatch<kSum, false>(s, a, st);
+    case kMean: return fast ? cta_dispatch<kMean, true>(s, a, st) : cta_dispatch<kMean, false>(s, a, st);
+    case kMax: return cta_dispatch<kMax, false>(s, a, st);
+    default: return cta_dispatch<kMin, false>(s, a, st);
+  }
+}
+
+}  // namespace gespmm

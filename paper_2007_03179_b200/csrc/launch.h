@@ -1,0 +1,64 @@
+// Host-side declarations shared by the kernel translation units and the API.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "gespmm/gespmm.h"
+
+namespace gespmm {
+
+struct SpmmArgs;
+
+// Sets the thread's last-error text (gespmm_last_error) and returns st.
+gespmm_status_t set_error(gespmm_status_t st, const std::string& msg);
+
+// Counts every kernel launch issued by the library (reported by bench.py).
+void note_launch();
+
+// --- faithful Algorithms 1-3 (kernels_faithful.cu) ---
+uint32_t faithful_tiles(int variant, uint32_t cf, uint32_t n);
+cudaError_t launch_faithful(int variant, uint32_t cf, int op, bool fast, const SpmmArgs& a,
+                            cudaStream_t s);
+
+// --- tuned B200 kernels (kernels_tuned.cu) ---
+// Shape of the row-per-(sub)warp kernel: VEC floats per lane access, LPR lanes
+// per row (32/LPR rows share a warp), CF column sub-tiles per lane (CWM merge
+// factor).  Column tile width = VEC * LPR * CF.
+struct WarpShape {
+  int vec = 4;
+  int lpr = 32;
+  int cf = 1;
+  uint32_t tile_width() const { return uint32_t(vec * lpr * cf); }
+};
+// Row-per-CTA shape for hub rows: WARPS warps split the columns of one row;
+// each warp owns VEC*32 contiguous columns per sub-tile.
+struct CtaShape {
+  int vec = 1;
+  int warps = 4;
+};
+
+bool tuned_shape_supported(const WarpShape& s);
+WarpShape pick_warp_shape(uint32_t n, bool vec4_ok, bool vec2_ok);
+cudaError_t launch_tuned_warp(const WarpShape& s, int op, bool fast, const SpmmArgs& a,
+                              cudaStream_t st);
+bool cta_shape_supported(const CtaShape& s);
+CtaShape pick_cta_shape(uint32_t n, bool vec4_ok, bool vec2_ok);
+cudaError_t launch_tuned_cta(const CtaShape& s, int op, bool fast, const SpmmArgs& a,
+                             cudaStream_t st);
+
+// --- validation (validate.cu) ---
+struct ValidateResult {
+  uint32_t row_ptr0;
+  uint32_t row_ptr_last;
+  uint32_t first_decrease;   // 0xffffffff if none
+  uint64_t first_bad_key;    // 2*p + (0 oob | 1 not increasing); ~0 if none
+  uint32_t bad_row;          // row containing that position
+  uint32_t bad_col;          // col_ind at that position
+};
+cudaError_t validate_csr_device(uint32_t m, uint32_t k, uint64_t nnz, const uint32_t* row_ptr,
+                                const uint32_t* col_ind, ValidateResult* out, cudaStream_t s);
+
+}  // namespace gespmm

@@ -1,0 +1,355 @@
+"""GPU parity: the sm_100a kernels (through the C ABI) against the oracle.
+
+Bar: bit-exact for every op in exact mode (sum/mean included — each output
+element is folded by one thread in CSR order with separate mul/add), arg
+indices identical; fast mode (FFMA) sum within 1e-5 of sum|v*b|.
+"""
+import numpy as np
+import pytest
+
+import oracle as O
+import paper_2007_03179_b200 as G
+from conftest import bits, first_divergence
+
+pytestmark = pytest.mark.gpu
+
+ALL_VARIANTS = [G.KernelVariant.naive(), G.KernelVariant.crc(), G.KernelVariant.crc_cwm(2),
+                G.KernelVariant.crc_cwm(4), G.KernelVariant.crc_cwm(8), G.KernelVariant.tuned()]
+OPS = ["sum", "mean", "max", "min"]
+
+
+def _oracle(a, b, op, want_arg=False, arg_kind=O.ARG_EDGE, skip_tail=False):
+    bd = b.data if isinstance(b, G.DenseMatrix) else b
+    return O.spmm(a.n_rows, a.n_cols, a.row_ptr, a.col_ind, a.vals, bd, op, want_arg=want_arg,
+                  arg_kind=arg_kind, skip_tail=skip_tail)
+
+
+def _inputs(spec):
+    a = G.gen_uniform_random(G.GraphGenSpec(spec["rows"], spec["nnz"], spec["gen_seed"],
+                                            spec["loops"]))
+    G.randomize_values(a, spec["val_seed"])
+    b = G.make_random_dense(spec["rows"], spec["n"], spec["b_seed"])
+    return a, b
+
+
+def _powerlaw(rows, nnz, maxdeg, seed, n):
+    a = G.gen_powerlaw(rows, nnz, maxdeg, 1.0, seed)
+    G.randomize_values(a, seed + 1)
+    b = G.make_random_dense(rows, n, seed + 2)
+    return a, b
+
+
+def test_hand_cases_every_variant(golden, golden_npz, cuda):
+    for case in golden["hand_cases"]:
+        i = case["npz_index"]
+        a = G.CsrMatrix(case["m"], case["k"], golden_npz[f"hand{i}_row_ptr"],
+                        golden_npz[f"hand{i}_col_ind"], golden_npz[f"hand{i}_vals"])
+        b = G.DenseMatrix.of(golden_npz[f"hand{i}_b"])
+        want = golden_npz[f"hand{i}_want"]
+        for v in ALL_VARIANTS:
+            c = G.native_spmm(a, b, v, G.reduce_op_by_name(case["op"]))
+            assert first_divergence(c.data, want) is None, (case["name"], v)
+            assert G.checksum(c) == case["checksum"]
+
+
+def test_random_corpus_every_variant(golden, cuda):
+    """225 reference-shaped cases x 6 variants, checksum-equal to the reference."""
+    for spec in golden["random_corpus"]:
+        a, b = _inputs(spec)
+        op = G.reduce_op_by_name(spec["op"])
+        for v in ALL_VARIANTS:
+            c = G.native_spmm(a, b, v, op)
+            assert G.checksum(c) == spec["checksum"], (spec, v)
+
+
+def test_config_checksums(golden, cuda):
+    for spec in golden["configs"]:
+        a = G.gen_uniform_random(G.GraphGenSpec(spec["rows"], spec["nnz"], spec["gen_seed"]))
+        G.randomize_values(a, spec["val_seed"])
+        b = G.make_random_dense(spec["rows"], spec["n"], spec["b_seed"])
+        op = G.reduce_op_by_name(spec["op"])
+        for v in (G.select_variant(spec["n"]), G.KernelVariant.tuned()):
+            assert G.checksum(G.native_spmm(a, b, v, op)) == spec["checksum"]
+
+
+@pytest.mark.parametrize("op", OPS)
+def test_new_ops_and_args_every_variant(op, cuda):
+    for seed, (rows, nnz, n) in enumerate([(300, 6000, 33), (500, 9000, 128), (97, 900, 5),
+                                           (256, 20000, 256), (64, 4000, 500)]):
+        a = G.gen_uniform_random(G.GraphGenSpec(rows, nnz, seed + 100))
+        G.randomize_values(a, seed + 200)
+        b = G.make_random_dense(rows, n, seed + 300)
+        want_arg = op in ("max", "min")
+        for kind in ((O.ARG_EDGE, O.ARG_COLUMN) if want_arg else (O.ARG_EDGE,)):
+            want, warg = _oracle(a, b, op, want_arg, kind)
+            ex = G.ExecOptions(arg_kind="column" if kind == O.ARG_COLUMN else "edge")
+            for v in ALL_VARIANTS:
+                c, arg = G.native_spmm_arg(a, b, v, G.reduce_op_by_name(op), exec=ex,
+                                           want_arg=want_arg)
+                assert first_divergence(c.data, want) is None, (op, v, rows, n)
+                if want_arg:
+                    assert np.array_equal(arg, warg), (op, v, kind)
+
+
+N_SWEEP = [1, 2, 3, 4, 5, 8, 12, 16, 24, 31, 32, 33, 48, 64, 66, 96, 100, 127, 128, 129, 192,
+           256, 260, 500, 512, 513, 1000]
+
+
+@pytest.mark.parametrize("n", N_SWEEP)
+def test_tuned_shapes_over_n(n, cuda):
+    """Every (VEC, LPR, CF) shape the tuner can pick, on a power-law matrix."""
+    a, b = _powerlaw(700, 30000, 650, n, n)
+    for op in ("sum", "max"):
+        want, warg = _oracle(a, b, op, op == "max")
+        c, arg = G.native_spmm_arg(a, b, G.KernelVariant.tuned(), G.reduce_op_by_name(op),
+                                   want_arg=op == "max")
+        assert first_divergence(c.data, want) is None, (n, op)
+        if op == "max":
+            assert np.array_equal(arg, warg)
+
+
+@pytest.mark.parametrize("n", [32, 64, 96, 128, 200, 256, 512, 520, 1000])
+@pytest.mark.parametrize("op", OPS)
+def test_hub_rows_row_per_cta(n, op, cuda):
+    """Force the row-per-CTA hub kernel (threshold 40) incl. rows spanning many
+    256-wide staging chunks; must stay bit-exact (columns split, not nonzeros)."""
+    a, b = _powerlaw(3000, 150000, 2999, 7, n)
+    ex = G.ExecOptions(hub_threshold=40)
+    want_arg = op in ("max", "min")
+    want, warg = _oracle(a, b, op, want_arg)
+    c, arg = G.native_spmm_arg(a, b, G.KernelVariant.tuned(), G.reduce_op_by_name(op), exec=ex,
+                               want_arg=want_arg)
+    assert first_divergence(c.data, want) is None
+    if want_arg:
+        assert np.array_equal(arg, warg)
+
+
+def test_row_length_boundaries(cuda):
+    """Rows of length 0, 1, 31, 32, 33, 255, 256, 257, 513 and one of 20000."""
+    lens = [0, 1, 31, 32, 33, 255, 256, 257, 513, 20000, 0, 7]
+    k = 25000
+    rng = np.random.default_rng(5)
+    rp = np.zeros(len(lens) + 1, np.uint32)
+    cols = []
+    for i, L in enumerate(lens):
+        cols.append(np.sort(rng.choice(k, L, replace=False)).astype(np.uint32))
+        rp[i + 1] = rp[i] + L
+    a = G.CsrMatrix(len(lens), k, rp, np.concatenate(cols), np.zeros(int(rp[-1]), np.float32))
+    G.randomize_values(a, 9)
+    for n in (16, 128, 256):
+        b = G.make_random_dense(k, n, 3)
+        for ht in (0, 30, -1):
+            for op in OPS:
+                want, warg = _oracle(a, b, op, op in ("max", "min"))
+                c, arg = G.native_spmm_arg(a, b, G.KernelVariant.tuned(), G.reduce_op_by_name(op),
+                                           exec=G.ExecOptions(hub_threshold=ht),
+                                           want_arg=op in ("max", "min"))
+                assert first_divergence(c.data, want) is None, (n, ht, op)
+                if warg is not None:
+                    assert np.array_equal(arg, warg)
+
+
+def test_special_values_nan_inf_signed_zero(cuda):
+    """NaN products never enter max/min (strict compare), -inf never beats the
+    seed, +0/-0 ties keep the earliest — all exactly as the ordered fold."""
+    a = G.gen_uniform_random(G.GraphGenSpec(200, 4000, 3))
+    G.randomize_values(a, 4)
+    b = G.make_random_dense(200, 64, 5)
+    bd = b.data.copy()
+    bd[::7, 3] = np.nan
+    bd[::5, 4] = -np.inf
+    bd[::3, 5] = np.inf
+    bd[:, 6] = 0.0
+    bd[::2, 7] = -0.0
+    bd[1::2, 7] = 0.0
+    bs = G.DenseMatrix.of(bd)
+    for op in OPS:
+        want, warg = _oracle(a, bs, op, op in ("max", "min"))
+        for v in ALL_VARIANTS:
+            c, arg = G.native_spmm_arg(a, bs, v, G.reduce_op_by_name(op),
+                                       want_arg=op in ("max", "min"))
+            assert np.array_equal(bits(c.data), bits(want)), (op, v)
+            if warg is not None:
+                assert np.array_equal(arg, warg), (op, v)
+
+
+def test_empty_shapes_and_errors(golden, cuda):
+    # M = 0 -> empty result, no error (native.hpp:109)
+    a = G.CsrMatrix.empty(0, 5)
+    c = G.native_spmm(a, G.DenseMatrix.zeros(5, 3), G.KernelVariant.tuned(), G.ops.sum())
+    assert c.data.shape == (0, 3)
+    # all rows empty -> op seeds
+    a = G.CsrMatrix.empty(3, 3)
+    b = G.make_random_dense(3, 5, 3)
+    for v in ALL_VARIANTS:
+        assert np.all(G.native_spmm(a, b, v, G.ops.sum()).data == 0.0)
+        assert np.all(G.native_spmm(a, b, v, G.ops.max()).data == np.finfo(np.float32).min)
+        assert np.all(G.native_spmm(a, b, v, G.ops.min()).data == np.finfo(np.float32).max)
+        c, arg = G.native_spmm_arg(a, b, v, G.ops.max(), want_arg=True)
+        assert np.all(arg == -1)
+    # K = 0
+    a = G.CsrMatrix.empty(4, 0)
+    c = G.native_spmm(a, G.DenseMatrix.zeros(0, 8), G.KernelVariant.tuned(), G.ops.sum())
+    assert np.all(c.data == 0)
+    # reference error texts, raised through the device validation
+    for case in golden["validation"]:
+        a = G.CsrMatrix(case["m"], case["k"], np.array(case["row_ptr"], np.uint32),
+                        np.array(case["col_ind"], np.uint32), np.array(case["vals"], np.float32))
+        b = G.DenseMatrix.zeros(case["b_rows"], case["n"])
+        for v in ALL_VARIANTS:
+            if case["error"] is None:
+                G.native_spmm(a, b, v, G.ops.sum())
+                continue
+            with pytest.raises(G.Error) as ei:
+                G.native_spmm(a, b, v, G.ops.sum())
+            assert str(ei.value) == case["error"], (case["name"], v)
+    with pytest.raises(G.Error, match="arg indices"):
+        G.native_spmm_arg(G.CsrMatrix.empty(2, 2), G.DenseMatrix.zeros(2, 2),
+                          G.KernelVariant.tuned(), G.ops.sum(), want_arg=True)
+
+
+def test_device_validation_finds_first_violation_in_large_matrix(cuda):
+    a = G.gen_uniform_random(G.GraphGenSpec(5000, 200000, 1))
+    G.randomize_values(a, 2)
+    b = G.make_random_dense(5000, 32, 3)
+    for mutate, text in (
+        (lambda ci, rp: ci.__setitem__(150000, 7000), "col_ind[150000] = 7000 out of bounds"),
+        (lambda ci, rp: ci.__setitem__(int(rp[4000]) + 1, ci[int(rp[4000])]),
+         "columns not strictly increasing in row 4000"),
+        (lambda ci, rp: rp.__setitem__(2500, rp[2499] - 1), "row_ptr non-decreasing violated at index 2500"),
+    ):
+        ci, rp = a.col_ind.copy(), a.row_ptr.copy()
+        mutate(ci, rp)
+        bad = G.CsrMatrix(a.n_rows, a.n_cols, rp, ci, a.vals)
+        want_n, want_msg = O.validate(bad.n_rows, bad.n_cols, rp, ci, a.vals)
+        assert want_n >= 1 and text in want_msg
+        with pytest.raises(G.Error) as ei:
+            G.native_spmm(bad, b, G.KernelVariant.tuned(), G.ops.sum())
+        assert str(ei.value) == "spmm: matrix is not canonical CSR: " + want_msg
+
+
+def test_fault_injection_is_detected(cuda):
+    """test_kernels.cpp:153-166: SkipTail output differs from the oracle, and
+    equals the oracle's own SkipTail restatement (the hook is faithful)."""
+    a = G.gen_uniform_random(G.GraphGenSpec(40, 300, 11))
+    G.randomize_values(a, 12)
+    b = G.make_random_dense(40, 16, 2)
+    good, _ = _oracle(a, b, "sum")
+    faulty, _ = _oracle(a, b, "sum", skip_tail=True)
+    for v in ALL_VARIANTS:
+        c = G.native_spmm(a, b, v, G.ops.sum(), exec=G.ExecOptions(fault=G.FaultMode.SkipTail))
+        assert first_divergence(c.data, good) is not None
+        assert first_divergence(c.data, faulty) is None
+
+
+def test_fast_mode_within_tolerance(cuda):
+    a, b = _powerlaw(2000, 200000, 1999, 3, 128)
+    want, _ = _oracle(a, b, "sum")
+    absb = G.DenseMatrix.of(np.abs(b.data))
+    absa = G.CsrMatrix(a.n_rows, a.n_cols, a.row_ptr, a.col_ind, np.abs(a.vals))
+    scale, _ = _oracle(absa, absb, "sum")
+    for v in ALL_VARIANTS:
+        c = G.native_spmm(a, b, v, G.ops.sum(), exec=G.ExecOptions(exact=False))
+        err = np.abs(c.data.astype(np.float64) - want)
+        assert np.all(err <= 1e-5 * np.maximum(np.abs(want), scale) + 1e-30), v
+
+
+def test_device_api_plans_and_unaligned_views(cuda):
+    import torch
+    a, b = _powerlaw(5000, 400000, 4999, 21, 128)
+    d = G.DeviceCsr.from_host(a)
+    bt = torch.from_numpy(b.data).to(cuda)
+    for op in OPS:
+        want, warg = _oracle(a, b, op, op in ("max", "min"))
+        c, arg = G.spmm(d, bt, op, want_arg=op in ("max", "min"))
+        torch.cuda.synchronize()
+        assert first_divergence(c.cpu().numpy(), want) is None
+        if warg is not None:
+            assert np.array_equal(arg.cpu().numpy(), warg)
+        plan = G.Plan(d, 128, op)
+        assert plan.launches >= 1 and "tuned" in plan.description
+        c2 = torch.empty_like(c)
+        a2 = torch.empty_like(arg) if arg is not None else None
+        for _ in range(2):
+            plan.execute(bt, c2, a2)
+        torch.cuda.synchronize()
+        assert torch.equal(c2, c)
+        plan.close()
+    # B / C not 16-byte aligned -> scalar-lane fallback shape, same bits
+    buf = torch.empty(b.data.size + 1, dtype=torch.float32, device=cuda)
+    bview = buf[1:].view(b.data.shape)
+    bview.copy_(bt)
+    out = torch.empty(a.n_rows * 128 + 1, dtype=torch.float32, device=cuda)[1:].view(a.n_rows, 128)
+    c, _ = G.spmm(d, bview, "sum", out=out)
+    torch.cuda.synchronize()
+    want, _ = _oracle(a, b, "sum")
+    assert first_divergence(c.cpu().numpy(), want) is None
+
+
+def test_device_validate_flag(cuda):
+    import torch
+    a = G.gen_uniform_random(G.GraphGenSpec(100, 1000, 1))
+    ci = a.col_ind.copy()
+    ci[10] = 1000
+    d = G.DeviceCsr.from_host(G.CsrMatrix(100, 100, a.row_ptr, ci, a.vals))
+    b = torch.zeros(100, 8, device=cuda)
+    with pytest.raises(G.Error, match="out of bounds"):
+        G.spmm(d, b, "sum", validate=True)
+
+
+def _sub_rows(a, rows):
+    """CSR of a subset of rows (same columns) for oracle checks at scale."""
+    rp = a.row_ptr.astype(np.int64)
+    lens = rp[rows + 1] - rp[rows]
+    idx = np.concatenate([np.arange(rp[r], rp[r + 1]) for r in rows])
+    sub = G.CsrMatrix(len(rows), a.n_cols, np.concatenate([[0], np.cumsum(lens)]).astype(np.uint32),
+                      a.col_ind[idx], a.vals[idx])
+    return sub, idx
+
+
+@pytest.mark.slow
+def test_reddit_scale_sum_sampled_rows_and_cross_kernel(cuda):
+    """Reddit shape (232,965 rows, 114.8M nnz, N=128): tuned output equals the
+    paper's crc-cwm(2) kernel bit-for-bit over the whole matrix, and the oracle on
+    every hub row plus 3000 random rows."""
+    import torch
+    a = G.gen_powerlaw(232965, 114_800_000, 21657, 1.0, 1)
+    G.randomize_values(a, 2)
+    b = G.make_random_dense(a.n_cols, 128, 42)
+    d = G.DeviceCsr.from_host(a)
+    bt = torch.from_numpy(b.data).to(cuda)
+    c_tuned, _ = G.spmm(d, bt, "sum")
+    c_cwm, _ = G.spmm(d, bt, "sum", variant=G.KernelVariant.crc_cwm(2))
+    torch.cuda.synchronize()
+    assert torch.equal(c_tuned.view(torch.int32), c_cwm.view(torch.int32))
+    deg = np.diff(a.row_ptr.astype(np.int64))
+    rng = np.random.default_rng(0)
+    rows = np.unique(np.concatenate([np.argsort(-deg)[:200], rng.choice(a.n_rows, 3000, False)]))
+    sub, _ = _sub_rows(a, rows)
+    want, _ = _oracle(sub, b, "sum")
+    got = c_tuned[torch.from_numpy(rows).to(cuda)].cpu().numpy()
+    assert first_divergence(got, want) is None
+
+
+@pytest.mark.slow
+def test_products_scale_max_arg_sampled_rows(cuda):
+    """ogbn-products shape (2.45M rows, 123.7M nnz), N=256 max + argmax."""
+    import torch
+    a = G.gen_powerlaw(2_449_029, 123_718_280, 17481, 1.0, 1)
+    G.randomize_values(a, 2)
+    b = G.make_random_dense(a.n_cols, 256, 42)
+    d = G.DeviceCsr.from_host(a)
+    bt = torch.from_numpy(b.data).to(cuda)
+    c, arg = G.spmm(d, bt, "max", want_arg=True)
+    torch.cuda.synchronize()
+    deg = np.diff(a.row_ptr.astype(np.int64))
+    rng = np.random.default_rng(1)
+    rows = np.unique(np.concatenate([np.argsort(-deg)[:100], rng.choice(a.n_rows, 2000, False)]))
+    sub, idx = _sub_rows(a, rows)
+    want, warg = _oracle(sub, b, "max", True)
+    sel = torch.from_numpy(rows).to(cuda)
+    assert first_divergence(c[sel].cpu().numpy(), want) is None
+    got_arg = arg[sel].cpu().numpy()
+    # oracle positions are within the sub-CSR; map back to global CSR positions
+    mapped = np.where(warg >= 0, idx[np.maximum(warg, 0)], -1)
+    assert np.array_equal(got_arg, mapped)
