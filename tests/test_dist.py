@@ -1,0 +1,87 @@
+"""CPU, world_size 2 over gloo: the multi-GPU plumbing (nnz-balanced shards,
+B broadcast once, variable-height C row all-gather) with the oracle as the
+per-shard compute — the CUDA path replaces only that callable on the box."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import oracle as O
+import paper_2007_03179_b200 as G
+from paper_2007_03179_b200 import dist as D
+
+
+def test_partition_rows_balances_nnz_and_covers_all_rows():
+    a = G.gen_powerlaw(20000, 800000, 5000, 1.0, 3)
+    for parts in (1, 2, 3, 4, 8):
+        b = D.partition_rows(a.row_ptr, parts)
+        assert b[0] == 0 and b[-1] == a.n_rows and len(b) == parts + 1
+        assert all(b[i] <= b[i + 1] for i in range(parts))
+        # each shard within one max-degree row of the ideal split
+        loads = np.diff(a.row_ptr.astype(np.int64)[b])
+        assert loads.sum() == a.nnz()
+        assert loads.max() - a.nnz() / parts <= 5000
+    assert D.shard_balance(a.row_ptr, D.partition_rows(a.row_ptr, 8)) < 1.06
+
+
+def test_partition_edge_cases():
+    rp = np.array([0, 0, 0, 10, 10], np.uint32)  # one heavy row, empty rows
+    b = D.partition_rows(rp, 4)
+    assert b[0] == 0 and b[-1] == 4 and sorted(b) == b
+    empty = D.partition_rows(np.zeros(1, np.uint32), 3)
+    assert empty == [0, 0, 0, 0]
+    with pytest.raises(ValueError):
+        D.partition_rows(rp, 0)
+
+
+def test_shard_csr_rebases_rows():
+    a = G.gen_uniform_random(G.GraphGenSpec(50, 600, 2))
+    s = D.shard_csr(a, 10, 30)
+    assert s.n_rows == 20 and s.row_ptr[0] == 0
+    assert s.nnz() == int(a.row_ptr[30] - a.row_ptr[10])
+    assert np.array_equal(s.col_ind, a.col_ind[a.row_ptr[10]:a.row_ptr[30]])
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, op, result_dir):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    a = G.gen_powerlaw(3000, 90000, 1500, 1.0, 11)
+    G.randomize_values(a, 12)
+    if rank == 0:
+        b = torch.from_numpy(G.make_random_dense(3000, 24, 13).data.copy())
+    else:
+        b = torch.zeros(3000, 24)
+
+    def compute(shard, bt):
+        c, _ = O.spmm(shard.n_rows, shard.n_cols, shard.row_ptr, shard.col_ind, shard.vals,
+                      bt.numpy(), op)
+        return torch.from_numpy(c)
+
+    full, info = D.distributed_spmm(a, b, rank, world, compute)
+    np.save(os.path.join(result_dir, f"rank{rank}.npy"), full.numpy())
+    np.save(os.path.join(result_dir, f"b{rank}.npy"), b.numpy())
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("op", ["sum", "max"])
+def test_two_rank_gloo_spmm_equals_single_process(tmp_path, op):
+    world = 2
+    mp.spawn(_worker, args=(world, _free_port(), op, str(tmp_path)), nprocs=world, join=True)
+    a = G.gen_powerlaw(3000, 90000, 1500, 1.0, 11)
+    G.randomize_values(a, 12)
+    b = G.make_random_dense(3000, 24, 13)
+    want, _ = O.spmm(a.n_rows, a.n_cols, a.row_ptr, a.col_ind, a.vals, b.data, op)
+    for r in range(world):
+        got = np.load(tmp_path / f"rank{r}.npy")
+        assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
+        assert np.array_equal(np.load(tmp_path / f"b{r}.npy"), b.data)  # broadcast reached rank 1
