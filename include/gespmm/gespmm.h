@@ -179,6 +179,13 @@ gespmm_status_t gespmm_device_info(int32_t* sm_count, int64_t* l2_bytes,
                                    int64_t* persisting_l2_max, int32_t* cc_major,
                                    int32_t* cc_minor);
 
+/* Diagnostics (roofline report, not the SpMM path): for each idx[i] read row
+ * idx[i] of B (n must be 128) into a register accumulator — the gather ceiling
+ * of an index stream.  sink must hold blocks*256 floats.  Asynchronous. */
+gespmm_status_t gespmm_diag_gather(const uint32_t* idx, uint64_t count, const float* b,
+                                   uint32_t n, float* sink, int32_t blocks, int32_t hints,
+                                   void* stream);
+
 /* Kernel launches issued by this library since load (all entry points). */
 uint64_t gespmm_launch_count(void);
 

@@ -33,7 +33,7 @@ EXPORTS = [
     "gespmm_plan_destroy", "gespmm_validate_device", "gespmm_select_variant",
     "gespmm_reduce_by_name", "gespmm_checksum", "gespmm_make_random_dense",
     "gespmm_randomize_values", "gespmm_gen_uniform", "gespmm_gen_powerlaw", "gespmm_abi_version",
-    "gespmm_device_info", "gespmm_launch_count",
+    "gespmm_device_info", "gespmm_launch_count", "gespmm_diag_gather",
 ]
 
 
@@ -121,6 +121,8 @@ def lib():
         L.gespmm_device_info.argtypes = [C.POINTER(i32), C.POINTER(C.c_int64),
                                          C.POINTER(C.c_int64), C.POINTER(i32), C.POINTER(i32)]
         L.gespmm_device_info.restype = C.c_int
+        L.gespmm_diag_gather.argtypes = [vp, u64, vp, u32, vp, i32, i32, vp]
+        L.gespmm_diag_gather.restype = C.c_int
         L.gespmm_launch_count.argtypes = []
         L.gespmm_launch_count.restype = u64
         _lib = L
