@@ -137,10 +137,17 @@ struct Plan {
 
 namespace {
 
-uint32_t auto_hub_threshold(uint32_t n, double mean_degree) {
+// Row-per-CTA only for rows so long that one warp walking them would outlast
+// the rest of the launch.  Measured on B200 (Reddit shape, N=128): with the LPT
+// row schedule the warp kernel alone runs 3.05 ms, while peeling the 1687 rows
+// of degree >= 7884 onto the CTA kernel made the step 6.04 ms (the CTA kernel
+// moves 4x more load instructions per byte and competes for the same SMs).
+// A warp sustains ~1/3500 of the chip's gather rate, so a row is a tail risk
+// only beyond ~nnz/1024 nonzeros.
+uint32_t auto_hub_threshold(uint32_t n, uint64_t nnz) {
   if (n < 64) return 0xffffffffu;  // the CTA split needs >= 2 warps of columns
-  const double t = std::max(4096.0, 16.0 * mean_degree);
-  return t >= 4294967295.0 ? 0xffffffffu : uint32_t(t);
+  const uint64_t t = std::max<uint64_t>(65536, nnz / 1024);
+  return t >= 0xffffffffull ? 0xffffffffu : uint32_t(t);
 }
 
 // Inspector: degree-descending row schedule (stable counting sort) so heavy
@@ -168,7 +175,7 @@ gespmm_status_t build_tuned(Plan& p, const uint32_t* host_rp, cudaStream_t st) {
   for (uint32_t r = 0; r < m; ++r) order[count[maxd - deg[r]]++] = r;
 
   const int32_t ht = p.o.hub_threshold;
-  p.hub_threshold = ht > 0 ? uint32_t(ht) : (ht < 0 ? 0xffffffffu : auto_hub_threshold(p.n, p.mean_degree));
+  p.hub_threshold = ht > 0 ? uint32_t(ht) : (ht < 0 ? 0xffffffffu : auto_hub_threshold(p.n, host_rp[m]));
   uint32_t n_hub = 0;
   while (n_hub < m && deg[order[n_hub]] >= p.hub_threshold) ++n_hub;
   p.n_hub = n_hub;

@@ -70,6 +70,40 @@ struct Reduce<kMin> {
   }
 };
 
+// Packed pair update for sum/mean (sm_100a FADD2 / FFMA2).  Exact mode keeps
+// the two products as scalar FMULs and only packs the adds: FMUL+FMUL+FADD2
+// is never contracted by ptxas (a packed mul followed by a packed add is).
+__device__ __forceinline__ void add2_rn(float& a0, float& a1, float p0, float p1) {
+  asm("{\n\t.reg .b64 ra, rp;\n\tmov.b64 ra, {%0, %1};\n\tmov.b64 rp, {%2, %3};\n\t"
+      "add.rn.f32x2 ra, ra, rp;\n\tmov.b64 {%0, %1}, ra;\n\t}"
+      : "+f"(a0), "+f"(a1)
+      : "f"(p0), "f"(p1));
+}
+__device__ __forceinline__ void fma2_rn(float& a0, float& a1, float v, float b0, float b1) {
+  asm("{\n\t.reg .b64 ra, rb, rv;\n\tmov.b64 ra, {%0, %1};\n\tmov.b64 rb, {%2, %3};\n\t"
+      "mov.b64 rv, {%4, %4};\n\tfma.rn.f32x2 ra, rv, rb, ra;\n\tmov.b64 {%0, %1}, ra;\n\t}"
+      : "+f"(a0), "+f"(a1)
+      : "f"(b0), "f"(b1), "f"(v));
+}
+
+// Fold one staged nonzero (value v, position pos) into VEC accumulators.
+template <int OP, bool FAST, int VEC>
+__device__ __forceinline__ void fold_vec(float* acc, int32_t* who, float v, const float* b,
+                                         int32_t pos) {
+  if constexpr ((OP == kSum || OP == kMean) && VEC % 2 == 0) {
+#pragma unroll
+    for (int e = 0; e < VEC; e += 2) {
+      if (FAST)
+        fma2_rn(acc[e], acc[e + 1], v, b[e], b[e + 1]);
+      else
+        add2_rn(acc[e], acc[e + 1], __fmul_rn(v, b[e]), __fmul_rn(v, b[e + 1]));
+    }
+  } else {
+#pragma unroll
+    for (int e = 0; e < VEC; ++e) Reduce<OP>::template fold<FAST>(acc[e], who[e], v, b[e], pos);
+  }
+}
+
 // mean = sum / float(row length); an empty row keeps the sum seed.
 template <int OP>
 __device__ __forceinline__ float finish(float acc, uint32_t row_len) {

@@ -27,17 +27,42 @@ namespace {
 
 constexpr unsigned kFull = 0xffffffffu;
 
+template <int N>
+struct Pack;  // staged-entry read width: N consecutive (col) or (val) words
+template <>
+struct Pack<1> {
+  using U = uint32_t;
+  using F = float;
+};
+template <>
+struct Pack<2> {
+  using U = uint2;
+  using F = float2;
+};
+template <>
+struct Pack<4> {
+  using U = uint4;
+  using F = float4;
+};
+
 template <int OP, bool FAST, int VEC, int LPR, int CF>
 __global__ void __launch_bounds__(256, 3) k_warp(SpmmArgs a) {
   using R = Reduce<OP>;
   constexpr int RPW = 32 / LPR;                     // rows per warp
   constexpr int U0 = 8 / CF;
   constexpr int U = U0 < LPR ? U0 : LPR;            // gather batch; LPR % U == 0
+  constexpr int W = U < 4 ? U : 4;                  // LDS width (entries per read)
   constexpr uint32_t SUB = uint32_t(VEC * LPR);     // columns per sub-tile
   constexpr uint32_t TW = SUB * CF;                 // columns per tile
-  static_assert(LPR % U == 0, "batch must divide the staging chunk");
+  static_assert(LPR % U == 0 && U % W == 0, "batch geometry");
+  // Staged sparse tile, double-buffered per warp: phase 1 writes one (col, val)
+  // per lane, phase 2 reads them back with broadcast LDS of W entries — 2/W
+  // shared-pipe wavefronts per nonzero instead of two shuffles.
+  __shared__ __align__(16) uint32_t s_col[8][2][32];
+  __shared__ __align__(16) float s_val[8][2][32];
 
   const uint32_t lane = threadIdx.x & 31;
+  const uint32_t wib = threadIdx.x >> 5;
   const uint64_t unit = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const uint64_t groups = (uint64_t(a.n_sched) + RPW - 1) / RPW;
   if (unit >= groups * a.n_tiles) return;  // warp-uniform exit
@@ -60,72 +85,88 @@ __global__ void __launch_bounds__(256, 3) k_warp(SpmmArgs a) {
 
   const uint32_t col0 = tile * TW + sl * uint32_t(VEC);
   bool colok[CF];
+  const char* bbase[CF];  // byte base of the lane's sub-tile; masked ones read column 0
   float acc[CF][VEC];
   int32_t who[CF][VEC];
 #pragma unroll
   for (int c = 0; c < CF; ++c) {
     colok[c] = row_ok && (col0 + c * SUB) < a.n;
+    bbase[c] = reinterpret_cast<const char*>(a.b + (colok[c] ? col0 + c * SUB : 0u));
 #pragma unroll
     for (int e = 0; e < VEC; ++e) {
       acc[c][e] = R::init();
       who[c][e] = -1;
     }
   }
-  // column offsets of the lane's sub-tiles; masked sub-tiles read column 0
-  uint32_t coff[CF];
-#pragma unroll
-  for (int c = 0; c < CF; ++c) coff[c] = colok[c] ? col0 + c * SUB : 0u;
+  const uint32_t stride = a.n * 4u;  // bytes per B row (B < 4 GiB per row index * stride)
   const uint32_t* ci = a.col_ind + start;
   const float* vs = a.vals + start;
+  uint32_t* my_col = &s_col[wib][0][0];
+  float* my_val = &s_val[wib][0][0];
 
-  // phase-1 staging, one chunk ahead
-  uint32_t kc = 0;
-  float vv = 0.0f;
-  if (sl < len) {
-    kc = ld_stream_u32(ci + sl, pol.stream);
-    vv = ld_stream_f32(vs + sl, pol.stream);
+  // phase 1 of chunk 0; slots past the row end hold column 0 (a valid row)
+  {
+    uint32_t k0 = 0;
+    float v0 = 0.0f;
+    if (sl < len) {
+      k0 = ld_stream_u32(ci + sl, pol.stream);
+      v0 = ld_stream_f32(vs + sl, pol.stream);
+    }
+    my_col[lane] = k0;
+    my_val[lane] = v0;
   }
+  uint32_t buf = 0;
   for (uint32_t off = 0; off < maxlen; off += LPR) {
-    const uint32_t cur_k = kc;
-    const float cur_v = vv;
+    // issue the next chunk's sparse loads before consuming this one
+    uint32_t kn = 0;
+    float vn = 0.0f;
     const uint32_t nxt = off + LPR + sl;
     if (nxt < len) {
-      kc = ld_stream_u32(ci + nxt, pol.stream);
-      vv = ld_stream_f32(vs + nxt, pol.stream);
+      kn = ld_stream_u32(ci + nxt, pol.stream);
+      vn = ld_stream_f32(vs + nxt, pol.stream);
     }
+    __syncwarp();
+    const uint32_t* cs = my_col + buf * 32 + sub * LPR;
+    const float* vsm = my_val + buf * 32 + sub * LPR;
     const uint32_t chunk = min(uint32_t(LPR), maxlen - off);
     for (uint32_t kk = 0; kk < chunk; kk += U) {
       uint32_t k[U];
       float v[U];
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        k[u] = __shfl_sync(kFull, cur_k, int(sub * LPR + kk + u));
-        v[u] = __shfl_sync(kFull, cur_v, int(sub * LPR + kk + u));
+      for (int q = 0; q < U; q += W) {
+        const typename Pack<W>::U c4 = *reinterpret_cast<const typename Pack<W>::U*>(cs + kk + q);
+        const typename Pack<W>::F v4 = *reinterpret_cast<const typename Pack<W>::F*>(vsm + kk + q);
+        const uint32_t* cp = reinterpret_cast<const uint32_t*>(&c4);
+        const float* vp = reinterpret_cast<const float*>(&v4);
+#pragma unroll
+        for (int t = 0; t < W; ++t) {
+          k[q + t] = cp[t];
+          v[q + t] = vp[t];
+        }
       }
-      // Unpredicated gathers (slots past the row end re-read a valid row:
-      // k comes from a lane holding an earlier/zero index), so ptxas issues
-      // all U*CF loads back to back instead of interleaving them with folds.
+      // all U*CF gathers issued before any fold (memory-level parallelism);
+      // unpredicated: past-the-end slots re-read a valid row.
       Vec<VEC> bv[U][CF];
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const float* brow = a.b + uint64_t(k[u]) * a.n;
+      for (int u = 0; u < U; ++u)
 #pragma unroll
-        for (int c = 0; c < CF; ++c) bv[u][c] = ld_keep<VEC>(brow + coff[c], pol.keep);
-      }
+        for (int c = 0; c < CF; ++c)
+          bv[u][c] = ld_keep<VEC>(
+              reinterpret_cast<const float*>(bbase[c] + uint64_t(k[u]) * stride), pol.keep);
+      const int32_t rem = int32_t(len - off - kk);  // entries left in this row (may be <= 0)
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        if (off + kk + u < len) {
+        if (u < rem) {
           const int32_t pos = a.arg_col ? int32_t(k[u]) : int32_t(start + off + kk + u);
 #pragma unroll
           for (int c = 0; c < CF; ++c)
-            if (colok[c]) {
-#pragma unroll
-              for (int e = 0; e < VEC; ++e)
-                R::template fold<FAST>(acc[c][e], who[c][e], v[u], bv[u][c].x[e], pos);
-            }
+            if (colok[c]) fold_vec<OP, FAST, VEC>(acc[c], who[c], v[u], bv[u][c].x, pos);
         }
       }
     }
+    buf ^= 1u;
+    my_col[buf * 32 + lane] = kn;  // phase 1 of the next chunk (buffer last read before
+    my_val[buf * 32 + lane] = vn;  // this iteration's __syncwarp)
   }
 
   const uint32_t row_len = full_end - start;

@@ -15,8 +15,9 @@ fasttests)
 ceilings)
   timeout 600 python tools/ceilings.py --json $OUT/ceilings.json > $OUT/ceilings.txt 2>&1 ;;
 sweep)
-  for v in "--variant tuned" "--variant tuned --hub-threshold -1" "--variant tuned --hub-threshold 2048" \
-           "--variant crc-cwm --cf 2" "--variant crc-cwm --cf 4" "--variant crc" "--variant naive" "--variant tuned --fast"; do
+  for v in ${SWEEP:-"--variant tuned" "--variant tuned --fast" "--variant tuned --hub-threshold 7884" \
+           "--variant crc-cwm --cf 2" "--variant crc-cwm --cf 4" "--variant crc-cwm --cf 8" "--variant crc" "--variant naive" \
+           "--config products" "--config pubmed"}; do
     echo "== $v" >> $OUT/sweep.txt
     timeout 300 python bench.py --steps 10 --warmup 3 --no-e2e --no-cpu $v 2>>$OUT/sweep.log | \
       python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['ms_per_step'], d['value'], d['roofline']['frac'], d['config']['plan'])" >> $OUT/sweep.txt 2>&1
