@@ -312,7 +312,8 @@ def run_ours(args, cfg):
     d = G.DeviceCsr.from_host(shard, dev)
     c = torch.empty((shard.n_rows, n), dtype=torch.float32, device=dev)
     arg = torch.empty((shard.n_rows, n), dtype=torch.int32, device=dev) if want_arg else None
-    ex = G.ExecOptions(hub_threshold=args.hub_threshold, exact=not args.fast)
+    ex = G.ExecOptions(hub_threshold=args.hub_threshold, exact=not args.fast,
+                       l2_persist=args.l2_persist, l2_hints=not args.no_hints)
     variant = G.variant_by_name(args.variant, args.cf)
     plan = G.Plan(d, n, op, variant=variant, exec=ex)
     log(f"[bench] rank {rank}: rows [{info.lo},{info.hi}) nnz {shard.nnz()} plan: {plan.description}")
@@ -378,7 +379,8 @@ def run_ours(args, cfg):
         csr = _lib.Csr(shard.n_rows, shard.n_cols, shard.nnz(), rp_h.data_ptr(), ci_h.data_ptr(),
                        v_h.data_ptr())
         o = _lib.default_options(variant=int(variant.kind), cf=args.cf,
-                                 hub_threshold=args.hub_threshold, exact=int(not args.fast))
+                                 hub_threshold=args.hub_threshold, exact=int(not args.fast),
+                                 l2_persist=int(args.l2_persist), l2_hints=int(not args.no_hints))
         L = _lib.lib()
 
         def host_call():
@@ -460,6 +462,8 @@ def main():
     p.add_argument("--cf", type=int, default=2)
     p.add_argument("--hub-threshold", type=int, default=0)
     p.add_argument("--fast", action="store_true", help="FFMA sum (1e-5 tolerance) instead of exact")
+    p.add_argument("--l2-persist", action="store_true", help="L2 access-policy window on B")
+    p.add_argument("--no-hints", action="store_true", help="evict_normal instead of L2 hints")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
     args = p.parse_args()

@@ -85,7 +85,9 @@ typedef struct {
   int32_t fault_skip_tail; /* negative-test hook: FaultMode::SkipTail (kernel.hpp:167-182) */
   int32_t l2_hints;   /* 1 (default): B evict_last, CSR/C evict_first */
   int32_t hub_threshold; /* TUNED: rows with degree >= this go row-per-CTA; 0 = auto, <0 = off */
-  int32_t reserved[8];
+  int32_t l2_persist; /* 1: launch with an L2 access-policy window marking B persisting
+                         (sets the device's persisting-L2 limit to its maximum); default 0 */
+  int32_t reserved[7];
 } gespmm_options_t;
 
 void gespmm_options_default(gespmm_options_t* opts);

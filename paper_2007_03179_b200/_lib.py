@@ -46,7 +46,8 @@ class Options(C.Structure):
     _fields_ = [("variant", C.c_int32), ("cf", C.c_uint32), ("exact", C.c_int32),
                 ("arg_kind", C.c_int32), ("validate", C.c_int32),
                 ("fault_skip_tail", C.c_int32), ("l2_hints", C.c_int32),
-                ("hub_threshold", C.c_int32), ("reserved", C.c_int32 * 8)]
+                ("hub_threshold", C.c_int32), ("l2_persist", C.c_int32),
+                ("reserved", C.c_int32 * 7)]
 
 
 _lock = threading.Lock()

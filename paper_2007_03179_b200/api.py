@@ -290,6 +290,7 @@ class ExecOptions:
     arg_kind: str = "edge"          # "edge" (CSR position p) or "column" (col_ind[p])
     l2_hints: bool = True
     hub_threshold: int = 0          # 0 auto, <0 off
+    l2_persist: bool = False        # L2 access-policy window marking B persisting
 
 
 def _options(variant: KernelVariant, ex: ExecOptions, validate: bool = True) -> _lib.Options:
@@ -297,7 +298,8 @@ def _options(variant: KernelVariant, ex: ExecOptions, validate: bool = True) -> 
                            exact=int(ex.exact),
                            arg_kind=_lib.ARG_COLUMN if ex.arg_kind == "column" else _lib.ARG_EDGE,
                            validate=int(validate), fault_skip_tail=int(ex.fault == FaultMode.SkipTail),
-                           l2_hints=int(ex.l2_hints), hub_threshold=ex.hub_threshold)
+                           l2_hints=int(ex.l2_hints), hub_threshold=ex.hub_threshold,
+                           l2_persist=int(ex.l2_persist))
 
 
 # ---------------------------------------------------------------------------

@@ -248,6 +248,34 @@ gespmm_status_t plan_create_impl(const gespmm_csr_t* a, uint32_t n, gespmm_reduc
   return GESPMM_OK;
 }
 
+// Persisting-L2 set-aside, raised once per device to the hardware maximum
+// when a plan asks for it (opt-in: this is device-wide state).
+struct PersistLimits {
+  size_t max_window = 0;
+  size_t set_aside = 0;
+};
+std::mutex g_persist_mu;
+PersistLimits g_persist[64];
+bool g_persist_init[64] = {};
+
+PersistLimits persist_limits(int dev) {
+  std::lock_guard<std::mutex> lk(g_persist_mu);
+  if (dev < 0 || dev >= 64) return {};
+  if (!g_persist_init[dev]) {
+    int max_persist = 0, max_window = 0;
+    cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, dev);
+    cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, dev);
+    if (max_persist > 0 && cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, size_t(max_persist)) == cudaSuccess) {
+      size_t got = 0;
+      cudaDeviceGetLimit(&got, cudaLimitPersistingL2CacheSize);
+      g_persist[dev].set_aside = got;
+    }
+    g_persist[dev].max_window = size_t(max_window);
+    g_persist_init[dev] = true;
+  }
+  return g_persist[dev];
+}
+
 gespmm_status_t plan_execute_impl(Plan& p, const float* b, float* c, int32_t* arg,
                                   cudaStream_t st) {
   gespmm_status_t s = check_op(p.op, arg);
@@ -291,7 +319,21 @@ gespmm_status_t plan_execute_impl(Plan& p, const float* b, float* c, int32_t* ar
   args.order = p.d_order + p.n_hub;
   args.n_sched = p.a.n_rows - p.n_hub;
   args.n_tiles = (p.n + wsel.tile_width() - 1) / wsel.tile_width();
-  if (args.n_sched) GESPMM_CUDA(launch_tuned_warp(wsel, p.op, fast, args, st), "spmm");
+  cudaAccessPolicyWindow win{};
+  const cudaAccessPolicyWindow* winp = nullptr;
+  if (p.o.l2_persist) {
+    const size_t b_bytes = size_t(p.a.n_cols) * p.n * sizeof(float);
+    const PersistLimits lim = persist_limits(p.device);
+    if (lim.max_window > 0 && lim.set_aside > 0 && b_bytes > 0) {
+      win.base_ptr = const_cast<float*>(b);
+      win.num_bytes = std::min(b_bytes, lim.max_window);
+      win.hitRatio = float(std::min(1.0, double(lim.set_aside) / double(win.num_bytes)));
+      win.hitProp = cudaAccessPropertyPersisting;
+      win.missProp = cudaAccessPropertyStreaming;
+      winp = &win;
+    }
+  }
+  if (args.n_sched) GESPMM_CUDA(launch_tuned_warp(wsel, p.op, fast, args, st, winp), "spmm");
   if (p.n_hub) GESPMM_CUDA(cudaStreamWaitEvent(st, p.ev_join, 0), "spmm");
   return GESPMM_OK;
 }
@@ -387,6 +429,7 @@ void gespmm_options_default(gespmm_options_t* o) {
   o->fault_skip_tail = 0;
   o->l2_hints = 1;
   o->hub_threshold = 0;
+  o->l2_persist = 0;
 }
 
 const char* gespmm_last_error(void) { return t_err.c_str(); }

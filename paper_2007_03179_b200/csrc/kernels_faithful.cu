@@ -12,6 +12,7 @@ namespace gespmm {
 namespace {
 
 constexpr int kWarpsPerBlock = 8;  // KernelConfig::warps_per_block (kernel.hpp:79)
+constexpr int kBatch = 4;          // nonzeros gathered per batch in every variant
 
 // Algorithm 1 (kernel.hpp:197-224): per nonzero, warp-uniform loads of the
 // column index and value, then one unit-stride B load per lane.
@@ -31,13 +32,25 @@ __global__ void __launch_bounds__(256) k_naive(SpmmArgs a) {
   const uint32_t end = faulted_end(start, full_end, a.skip_tail);
   float acc = R::init();
   int32_t who = -1;
-  for (uint32_t p = start; p < end; ++p) {
-    const uint32_t k = __ldg(a.col_ind + p);
-    const float v = __ldg(a.vals + p);
-    if (active) {
-      const float bv = ld_keep<1>(a.b + uint64_t(k) * a.n + col, pol.keep).x[0];
-      R::template fold<FAST>(acc, who, v, bv, a.arg_col ? int32_t(k) : int32_t(p));
+  // Batches of kBatch nonzeros: the B loads of a batch are issued before any
+  // fold (the same memory-level parallelism every variant gets, so the
+  // ablation compares the algorithms, not the compiler's scheduling).
+  const float* bcol = a.b + (active ? col : 0u);
+  for (uint32_t p = start; p < end; p += kBatch) {
+    uint32_t k[kBatch];
+    float v[kBatch], bv[kBatch];
+#pragma unroll
+    for (int u = 0; u < kBatch; ++u) {
+      const uint32_t q = min(p + u, end - 1);  // past-the-end slots re-read the last entry
+      k[u] = __ldg(a.col_ind + q);             // warp-uniform (broadcast) loads
+      v[u] = __ldg(a.vals + q);
     }
+#pragma unroll
+    for (int u = 0; u < kBatch; ++u) bv[u] = ld_keep<1>(bcol + uint64_t(k[u]) * a.n, pol.keep).x[0];
+#pragma unroll
+    for (int u = 0; u < kBatch; ++u)
+      if (active && p + u < end)
+        R::template fold<FAST>(acc, who, v[u], bv[u], a.arg_col ? int32_t(k[u]) : int32_t(p + u));
   }
   if (active) {
     const uint64_t o = uint64_t(row) * a.n + col;
@@ -82,17 +95,27 @@ __global__ void __launch_bounds__(256) k_crc(SpmmArgs a) {
       s_val[wib][lane] = ld_stream_f32(a.vals + ptr + lane, pol.stream);
     }
     __syncwarp();
-    for (uint32_t kk = 0; kk < tile_n; ++kk) {  // phase 2
-      const uint32_t k = s_col[wib][kk];
-      const float v = s_val[wib][kk];
-      const float* brow = a.b + uint64_t(k) * a.n;
-      const int32_t pos = a.arg_col ? int32_t(k) : int32_t(ptr + kk);
+    for (uint32_t kk = 0; kk < tile_n; kk += kBatch) {  // phase 2, kBatch at a time
+      float bv[kBatch][CF];
 #pragma unroll
-      for (int c = 0; c < CF; ++c) {
-        const uint32_t col = col_base + c * 32u + lane;
-        if (col < a.n) {
-          const float bv = ld_keep<1>(brow + col, pol.keep).x[0];
-          R::template fold<FAST>(acc[c], who[c], v, bv, pos);
+      for (int u = 0; u < kBatch; ++u) {
+        const uint32_t k = s_col[wib][min(kk + u, tile_n - 1)];
+        const float* brow = a.b + uint64_t(k) * a.n;
+#pragma unroll
+        for (int c = 0; c < CF; ++c) {
+          const uint32_t col = col_base + c * 32u + lane;
+          bv[u][c] = ld_keep<1>(brow + (col < a.n ? col : 0u), pol.keep).x[0];
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kBatch; ++u) {
+        if (kk + u < tile_n) {
+          const uint32_t k = s_col[wib][kk + u];
+          const float v = s_val[wib][kk + u];
+          const int32_t pos = a.arg_col ? int32_t(k) : int32_t(ptr + kk + u);
+#pragma unroll
+          for (int c = 0; c < CF; ++c)
+            if (col_base + c * 32u + lane < a.n) R::template fold<FAST>(acc[c], who[c], v, bv[u][c], pos);
         }
       }
     }

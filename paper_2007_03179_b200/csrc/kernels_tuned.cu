@@ -45,8 +45,10 @@ struct Pack<4> {
   using F = float4;
 };
 
+constexpr int kWarpBlock = 4;  // warps per CTA: 72-register kernel -> 7 CTAs = 28 warps/SM
+
 template <int OP, bool FAST, int VEC, int LPR, int CF>
-__global__ void __launch_bounds__(256, 3) k_warp(SpmmArgs a) {
+__global__ void __launch_bounds__(32 * kWarpBlock, 7) k_warp(SpmmArgs a) {
   using R = Reduce<OP>;
   constexpr int RPW = 32 / LPR;                     // rows per warp
   constexpr int U0 = 8 / CF;
@@ -58,8 +60,8 @@ __global__ void __launch_bounds__(256, 3) k_warp(SpmmArgs a) {
   // Staged sparse tile, double-buffered per warp: phase 1 writes one (col, val)
   // per lane, phase 2 reads them back with broadcast LDS of W entries — 2/W
   // shared-pipe wavefronts per nonzero instead of two shuffles.
-  __shared__ __align__(16) uint32_t s_col[8][2][32];
-  __shared__ __align__(16) float s_val[8][2][32];
+  __shared__ __align__(16) uint32_t s_col[kWarpBlock][2][32];
+  __shared__ __align__(16) float s_val[kWarpBlock][2][32];
 
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t wib = threadIdx.x >> 5;
@@ -277,20 +279,40 @@ __global__ void __launch_bounds__(WARPS * 32) k_cta(SpmmArgs a) {
 
 // ---- dispatch tables ------------------------------------------------------
 
+template <class K>
+cudaError_t launch_ex(K kernel, dim3 g, dim3 b, cudaStream_t st, const SpmmArgs& a,
+                      const cudaAccessPolicyWindow* window) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = g;
+  cfg.blockDim = b;
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  cfg.numAttrs = 0;
+  if (window) {
+    attr[0].id = cudaLaunchAttributeAccessPolicyWindow;
+    attr[0].val.accessPolicyWindow = *window;
+    cfg.numAttrs = 1;
+  }
+  cfg.attrs = attr;
+  return cudaLaunchKernelEx(&cfg, kernel, a);
+}
+
 template <int OP, bool FAST>
-cudaError_t warp_dispatch(const WarpShape& s, const SpmmArgs& a, cudaStream_t st) {
+cudaError_t warp_dispatch(const WarpShape& s, const SpmmArgs& a, cudaStream_t st,
+                          const cudaAccessPolicyWindow* window) {
   const uint32_t rpw = 32u / uint32_t(s.lpr);
   const uint64_t groups = (uint64_t(a.n_sched) + rpw - 1) / rpw;
   const uint64_t warps = groups * a.n_tiles;
-  const uint64_t blocks = (warps + 7) / 8;
+  const uint64_t blocks = (warps + kWarpBlock - 1) / kWarpBlock;
   if (blocks == 0) return cudaSuccess;
   if (blocks > 0x7fffffffull) return cudaErrorInvalidConfiguration;
-  const dim3 g{uint32_t(blocks)}, b{256};
-#define GESPMM_W(V, L, F)                                   \
-  if (s.vec == V && s.lpr == L && s.cf == F) {              \
-    k_warp<OP, FAST, V, L, F><<<g, b, 0, st>>>(a);          \
-    note_launch();                                          \
-    return cudaGetLastError();                              \
+  const dim3 g{uint32_t(blocks)}, b{32 * kWarpBlock};
+#define GESPMM_W(V, L, F)                                              \
+  if (s.vec == V && s.lpr == L && s.cf == F) {                         \
+    const cudaError_t e = launch_ex(k_warp<OP, FAST, V, L, F>, g, b, st, a, window); \
+    note_launch();                                                     \
+    return e;                                                          \
   }
   GESPMM_W(4, 4, 1) GESPMM_W(4, 8, 1) GESPMM_W(4, 16, 1) GESPMM_W(4, 32, 1)
   GESPMM_W(4, 32, 2) GESPMM_W(4, 32, 4)
@@ -376,12 +398,12 @@ CtaShape pick_cta_shape(uint32_t n, bool vec4_ok, bool /*vec2_ok*/) {
 }
 
 cudaError_t launch_tuned_warp(const WarpShape& s, int op, bool fast, const SpmmArgs& a,
-                              cudaStream_t st) {
+                              cudaStream_t st, const cudaAccessPolicyWindow* w) {
   switch (op) {
-    case kSum: return fast ? warp_dispatch<kSum, true>(s, a, st) : warp_dispatch<kSum, false>(s, a, st);
-    case kMean: return fast ? warp_dispatch<kMean, true>(s, a, st) : warp_dispatch<kMean, false>(s, a, st);
-    case kMax: return warp_dispatch<kMax, false>(s, a, st);
-    default: return warp_dispatch<kMin, false>(s, a, st);
+    case kSum: return fast ? warp_dispatch<kSum, true>(s, a, st, w) : warp_dispatch<kSum, false>(s, a, st, w);
+    case kMean: return fast ? warp_dispatch<kMean, true>(s, a, st, w) : warp_dispatch<kMean, false>(s, a, st, w);
+    case kMax: return warp_dispatch<kMax, false>(s, a, st, w);
+    default: return warp_dispatch<kMin, false>(s, a, st, w);
   }
 }
 

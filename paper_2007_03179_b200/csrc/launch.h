@@ -42,8 +42,9 @@ struct CtaShape {
 
 bool tuned_shape_supported(const WarpShape& s);
 WarpShape pick_warp_shape(uint32_t n, bool vec4_ok, bool vec2_ok);
+// `window` (nullable): L2 access-policy window attached to the launch.
 cudaError_t launch_tuned_warp(const WarpShape& s, int op, bool fast, const SpmmArgs& a,
-                              cudaStream_t st);
+                              cudaStream_t st, const cudaAccessPolicyWindow* window = nullptr);
 bool cta_shape_supported(const CtaShape& s);
 CtaShape pick_cta_shape(uint32_t n, bool vec4_ok, bool vec2_ok);
 cudaError_t launch_tuned_cta(const CtaShape& s, int op, bool fast, const SpmmArgs& a,
