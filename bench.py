@@ -451,13 +451,77 @@ def run_ours(args, cfg):
     return 0
 
 
+def run_gcn(args):
+    """BASELINE config 5: two-layer GCN on the Reddit shape, hidden 256 — one
+    full-batch training step (2 SpMM with A, 2 with A^T, 4 GEMMs, SGD) per step;
+    under torchrun the nodes are row-sharded and each layer all-gathers."""
+    import torch
+    from paper_2007_03179_b200 import gcn
+    import paper_2007_03179_b200 as G
+
+    world, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    cfg = CONFIGS["reddit"]
+    a = make_inputs(cfg)
+    gcfg = gcn.GCNConfig(in_features=602, hidden=256, classes=41)
+    adj, info = gcn.build_adjacency(a, dev, rank, world, G.ExecOptions(exact=not args.fast))
+    h, y = gcn.synthetic_features(a.n_rows, gcfg.in_features, gcfg.classes)
+    ht = torch.from_numpy(h[info.lo:info.hi]).to(dev)
+    yt = torch.from_numpy(y[info.lo:info.hi]).to(dev)
+    model = gcn.GCN(gcfg, dev)
+    info_arg = info if world > 1 else None
+    for _ in range(args.warmup):
+        model.step(ht, yt, adj, info_arg, a.n_rows)
+    torch.cuda.synchronize()
+    st = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches0 = G.launch_count()
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+    e0.record(st)
+    for _ in range(args.steps):
+        loss = model.step(ht, yt, adj, info_arg, a.n_rows)
+    e1.record(st)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    flops = gcn.spmm_flops_per_step(a.nnz(), gcfg)
+    if rank == 0:
+        print(json.dumps({
+            "metric": "GCN 2-layer training step (Reddit shape, hidden 256): SpMM GFLOP/s "
+                      "(4 SpMMs per step) over the whole step time",
+            "value": round(flops * args.steps / (ms * 1e-3) / 1e9, 3), "unit": "GFLOP/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(ms / args.steps, 3), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": "two-layer GCN, Reddit-shaped power-law graph, features 602, "
+                                   "hidden 256, classes 41, full batch, SGD",
+                       "parallelism": f"row-shard x{world}, per-layer all-gather"},
+            "loss": round(float(loss.item()), 6),
+            "gpu_launches": G.launch_count() - launches0}), flush=True)
+    adj.close()
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+    return 0
+
+
 def main():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
     p.add_argument("--steps", type=int, default=50)
     p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    p.add_argument("--config", choices=sorted(CONFIGS), default="reddit")
+    p.add_argument("--config", choices=sorted(CONFIGS) + ["gcn"], default="reddit")
     p.add_argument("--variant", default="tuned", choices=["tuned", "naive", "crc", "crc-cwm"])
     p.add_argument("--cf", type=int, default=2)
     p.add_argument("--hub-threshold", type=int, default=0)
@@ -470,6 +534,8 @@ def main():
     if args.warmup < 3:
         log("[bench] warmup raised to 3 (timing rules)")
         args.warmup = 3
+    if args.config == "gcn":
+        return run_gcn(args)
     cfg = CONFIGS[args.config]
     if args.impl == "reference":
         return run_reference(args, cfg)

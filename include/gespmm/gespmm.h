@@ -134,6 +134,16 @@ const char* gespmm_plan_describe(gespmm_plan_t plan);
 int32_t gespmm_plan_launches(gespmm_plan_t plan);
 void gespmm_plan_destroy(gespmm_plan_t plan);
 
+/* ---- format helpers ------------------------------------------------------ */
+
+/* A^T of a device CSR, as canonical CSR on the device: t_row_ptr[n_cols+1],
+ * t_col_ind[nnz], t_vals[nnz] (caller-allocated).  Deterministic (stable radix
+ * sort by column keeps rows ascending).  The device counterpart of the
+ * reference's to_coo -> from_coo round trip (csr.hpp:58-104); feeds the GCN
+ * backward SpMM.  Asynchronous on `stream`. */
+gespmm_status_t gespmm_csr_transpose_device(const gespmm_csr_t* a, uint32_t* t_row_ptr,
+                                            uint32_t* t_col_ind, float* t_vals, void* stream);
+
 /* ---- checks and helpers -------------------------------------------------- */
 
 /* Device canonical-CSR check (csr.hpp:112-153); status ENONCANON with the

@@ -28,7 +28,8 @@ NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
 CXX_FLAGS = ["-O3", "-std=c++17", "-fPIC", "-ffp-contract=off", "-Wall", "-Wextra",
              "-I", INCLUDE, "-I", CSRC, "-I", "/usr/local/cuda/include"]
 
-CU_SOURCES = ["api.cu", "validate.cu", "kernels_faithful.cu", "kernels_tuned.cu", "diag.cu"]
+CU_SOURCES = ["api.cu", "validate.cu", "kernels_faithful.cu", "kernels_tuned.cu", "diag.cu",
+              "transpose.cu"]
 CXX_SOURCES = ["gen.cpp"]
 HEADERS = ["common.cuh", "launch.h"]
 

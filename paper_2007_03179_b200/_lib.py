@@ -34,6 +34,7 @@ EXPORTS = [
     "gespmm_reduce_by_name", "gespmm_checksum", "gespmm_make_random_dense",
     "gespmm_randomize_values", "gespmm_gen_uniform", "gespmm_gen_powerlaw", "gespmm_abi_version",
     "gespmm_device_info", "gespmm_launch_count", "gespmm_diag_gather",
+    "gespmm_csr_transpose_device",
 ]
 
 
@@ -124,6 +125,8 @@ def lib():
         L.gespmm_device_info.restype = C.c_int
         L.gespmm_diag_gather.argtypes = [vp, u64, vp, u32, vp, i32, i32, vp]
         L.gespmm_diag_gather.restype = C.c_int
+        L.gespmm_csr_transpose_device.argtypes = [C.POINTER(Csr), vp, vp, vp, vp]
+        L.gespmm_csr_transpose_device.restype = C.c_int
         L.gespmm_launch_count.argtypes = []
         L.gespmm_launch_count.restype = u64
         _lib = L

@@ -456,6 +456,24 @@ class DeviceCsr:
     def nnz(self) -> int:
         return int(self.col_ind.numel())
 
+    def transpose(self, stream=None) -> "DeviceCsr":
+        """A^T as a canonical device CSR (gespmm_csr_transpose_device)."""
+        import torch
+        dev = self.row_ptr.device
+        rp = torch.empty(self.n_cols + 1, dtype=torch.int32, device=dev)
+        ci = torch.empty(max(self.nnz(), 1), dtype=torch.int32, device=dev)
+        v = torch.empty(max(self.nnz(), 1), dtype=torch.float32, device=dev)
+        csr = self.c_struct()
+        _check(lib().gespmm_csr_transpose_device(C.byref(csr), rp.data_ptr(), ci.data_ptr(),
+                                                 v.data_ptr(), _stream_ptr(stream)))
+        return DeviceCsr(self.n_cols, self.n_rows, rp, ci[: self.nnz()], v[: self.nnz()])
+
+    def to_host(self) -> CsrMatrix:
+        return CsrMatrix(self.n_rows, self.n_cols,
+                         self.row_ptr.cpu().numpy().view(np.uint32).copy(),
+                         self.col_ind.cpu().numpy().view(np.uint32).copy(),
+                         self.vals.cpu().numpy().copy())
+
     def c_struct(self) -> Csr:
         return Csr(self.n_rows, self.n_cols, self.nnz(), self.row_ptr.data_ptr(),
                    self.col_ind.data_ptr() if self.nnz() else None,

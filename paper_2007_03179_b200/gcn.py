@@ -1,0 +1,178 @@
+"""Two-layer GCN on the GE-SpMM kernels (BASELINE.json config 5).
+
+    Z1 = A · (H W1),  H1 = relu(Z1),  Z2 = A · (H1 W2),  loss = CE(Z2[train], y)
+
+Aggregation is the tuned SpMM (sum); its backward is the SpMM with A^T
+(built once on the device by gespmm_csr_transpose_device).  The dense
+transforms are plain torch matmuls (cuBLAS — library GEMMs).  The paper's
+integration into GNN frameworks (§IV-B) is exactly this: SpMM-like as
+an autograd op.
+
+Multi-GPU (one process per GPU): nodes are row-sharded by nnz
+(dist.partition_rows); rank r holds rows [lo, hi) of A and of A^T.  Each layer
+all-gathers the transformed features before aggregating (forward) and the
+incoming gradient before the A^T aggregation (backward) — the per-layer NCCL
+all-gather of the north_star; weight gradients are all-reduced.
+"""
+from __future__ import annotations
+
+import dataclasses
+from typing import Dict, Optional, Tuple
+
+import numpy as np
+
+from . import api
+from .api import CsrMatrix, DeviceCsr, ExecOptions, Plan
+from . import dist as D
+
+
+class Adjacency:
+    """A (rows lo..hi of the graph) and A^T (rows lo..hi of the transpose) on
+    one device, with cached plans per feature width."""
+
+    def __init__(self, a_rows: DeviceCsr, at_rows: DeviceCsr, exec: ExecOptions = ExecOptions()):
+        self.a, self.at = a_rows, at_rows
+        self.exec = exec
+        self._plans: Dict[Tuple[bool, int], Plan] = {}
+
+    def plan(self, transposed: bool, n: int) -> Plan:
+        key = (transposed, n)
+        if key not in self._plans:
+            self._plans[key] = Plan(self.at if transposed else self.a, n, "sum", exec=self.exec)
+        return self._plans[key]
+
+    def close(self):
+        for p in self._plans.values():
+            p.close()
+        self._plans.clear()
+
+
+def build_adjacency(a: CsrMatrix, device, rank: int = 0, world: int = 1,
+                    exec: ExecOptions = ExecOptions()):
+    """Shard A by nnz-balanced rows; build A^T on the device from the full A and
+    keep the same node range of it.  Returns (Adjacency, ShardInfo)."""
+    import torch
+    bounds = D.partition_rows(a.row_ptr, world)
+    info = D.ShardInfo(rank, world, bounds)
+    full = DeviceCsr.from_host(a, device)
+    at_full = full.transpose()
+    torch.cuda.synchronize(device)
+    if world == 1:
+        return Adjacency(full, at_full, exec), info
+    a_loc = DeviceCsr.from_host(D.shard_csr(a, info.lo, info.hi), device)
+    at_host = at_full.to_host()
+    at_loc = DeviceCsr.from_host(D.shard_csr(at_host, info.lo, info.hi), device)
+    del full, at_full
+    return Adjacency(a_loc, at_loc, exec), info
+
+
+def _gather(x, info: Optional[D.ShardInfo]):
+    if info is None or info.world == 1:
+        return x
+    return D.allgather_rows(x.contiguous(), info)
+
+
+class _Aggregate:
+    """torch.autograd.Function: Y_local = A_local · gather(X_local); dX_local = A^T_local · gather(dY_local)."""
+
+    @staticmethod
+    def make():
+        import torch
+
+        class Aggregate(torch.autograd.Function):
+            @staticmethod
+            def forward(ctx, x, adj: Adjacency, info):
+                x_full = _gather(x, info).contiguous()
+                out = torch.empty((adj.a.n_rows, x.shape[1]), dtype=x.dtype, device=x.device)
+                adj.plan(False, x.shape[1]).execute(x_full, out)
+                ctx.adj, ctx.info = adj, info
+                return out
+
+            @staticmethod
+            def backward(ctx, grad):
+                g_full = _gather(grad.contiguous(), ctx.info).contiguous()
+                adj = ctx.adj
+                out = torch.empty((adj.at.n_rows, grad.shape[1]), dtype=grad.dtype,
+                                  device=grad.device)
+                adj.plan(True, grad.shape[1]).execute(g_full, out)
+                return out, None, None
+
+        return Aggregate
+
+
+_AGG = None
+
+
+def aggregate(x, adj: Adjacency, info: Optional[D.ShardInfo] = None):
+    global _AGG
+    if _AGG is None:
+        _AGG = _Aggregate.make()
+    return _AGG.apply(x, adj, info)
+
+
+@dataclasses.dataclass
+class GCNConfig:
+    in_features: int = 602     # Reddit
+    hidden: int = 256          # BASELINE config 5
+    classes: int = 41
+    lr: float = 0.01
+    seed: int = 0
+
+
+class GCN:
+    """Two GCN layers with explicit parameters (no nn.Module magic needed)."""
+
+    def __init__(self, cfg: GCNConfig, device):
+        import torch
+        g = torch.Generator(device="cpu").manual_seed(cfg.seed)
+        s1 = (6.0 / (cfg.in_features + cfg.hidden)) ** 0.5
+        s2 = (6.0 / (cfg.hidden + cfg.classes)) ** 0.5
+        self.w1 = ((torch.rand(cfg.in_features, cfg.hidden, generator=g) * 2 - 1) * s1).to(device)
+        self.w2 = ((torch.rand(cfg.hidden, cfg.classes, generator=g) * 2 - 1) * s2).to(device)
+        self.w1.requires_grad_(True)
+        self.w2.requires_grad_(True)
+        self.cfg = cfg
+
+    def params(self):
+        return [self.w1, self.w2]
+
+    def forward(self, h, adj: Adjacency, info=None):
+        import torch
+        z1 = aggregate(h @ self.w1, adj, info)
+        h1 = torch.relu(z1)
+        return aggregate(h1 @ self.w2, adj, info)
+
+    def step(self, h, labels, adj: Adjacency, info=None, n_total: Optional[int] = None):
+        """One full-batch training step (forward, backward, SGD); returns the loss."""
+        import torch
+        import torch.nn.functional as F
+        logits = self.forward(h, adj, info)
+        n_total = n_total if n_total is not None else h.shape[0]
+        loss = F.cross_entropy(logits, labels, reduction="sum") / n_total
+        for p in self.params():
+            p.grad = None
+        loss.backward()
+        if info is not None and info.world > 1:
+            import torch.distributed as dist
+            for p in self.params():
+                dist.all_reduce(p.grad)
+            lt = loss.detach().clone()
+            dist.all_reduce(lt)
+            loss = lt
+        with torch.no_grad():
+            for p in self.params():
+                p -= self.cfg.lr * p.grad
+        return loss.detach()
+
+
+def synthetic_features(m: int, f: int, classes: int, seed: int = 3):
+    """Deterministic node features (reference make_random_dense) and labels."""
+    h = api.make_random_dense(m, f, seed).data
+    rng = np.random.default_rng(seed)
+    y = rng.integers(0, classes, m).astype(np.int64)
+    return h, y
+
+
+def spmm_flops_per_step(nnz: int, cfg: GCNConfig) -> int:
+    """4 SpMMs per step: A·X1 (hidden), A·X2 (classes), and the two A^T ones."""
+    return 2 * nnz * (2 * cfg.hidden + 2 * cfg.classes)
