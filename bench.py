@@ -438,6 +438,9 @@ def run_ours(args, cfg):
                          "algorithmic_bytes": alg_bytes, "unique_cols": uniq,
                          "model": "4(M+1)+8nnz+4UN+4MN[+4MN arg], per step"},
             "gpu_launches": int(launches),
+            "step_ms": {"min": round(min(per_step_ms), 4),
+                        "median": round(statistics.median(per_step_ms), 4),
+                        "max": round(max(per_step_ms), 4)},
             "launches_per_step": plan.launches,
             "clocks": clocks,
             "e2e": e2e,
