@@ -339,7 +339,8 @@ def run_ours(args, cfg):
         time.sleep(0.1)
     launches0 = G.launch_count()
     for i in range(args.steps):
-        l2_flush.zero_()  # outside the events: L2 flushed between steps
+        if not args.no_flush:
+            l2_flush.zero_()  # outside the events: L2 flushed between steps
         starts[i].record(stream)
         step()
         ends[i].record(stream)
@@ -347,6 +348,7 @@ def run_ours(args, cfg):
     launches = G.launch_count() - launches0
     clocks = sampler.stop() if sampler else None
     per_step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    log("[bench] per-step ms: " + " ".join(f"{x:.3f}" for x in per_step_ms))
     total_ms = float(sum(per_step_ms))
     if world > 1:
         import torch.distributed as dist
@@ -469,7 +471,7 @@ def run_gcn(args):
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=dev)
     cfg = CONFIGS["reddit"]
-    a = make_inputs(cfg)
+    a = gcn.normalize_adjacency(make_inputs(cfg))  # D^-1/2 (A + I) D^-1/2
     gcfg = gcn.GCNConfig(in_features=602, hidden=256, classes=41)
     adj, info = gcn.build_adjacency(a, dev, rank, world, G.ExecOptions(exact=not args.fast))
     h, y = gcn.synthetic_features(a.n_rows, gcfg.in_features, gcfg.classes)
@@ -531,6 +533,7 @@ def main():
     p.add_argument("--fast", action="store_true", help="FFMA sum (1e-5 tolerance) instead of exact")
     p.add_argument("--l2-persist", action="store_true", help="L2 access-policy window on B")
     p.add_argument("--no-hints", action="store_true", help="evict_normal instead of L2 hints")
+    p.add_argument("--no-flush", action="store_true", help="skip the L2 flush between steps")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
     args = p.parse_args()

@@ -165,6 +165,38 @@ class GCN:
         return loss.detach()
 
 
+def normalize_adjacency(a: CsrMatrix, add_self_loops: bool = True) -> CsrMatrix:
+    """GCN propagation matrix D^-1/2 (A + I) D^-1/2 on A's pattern (values
+    ignored), as a canonical CSR (Kipf & Welling; the normalisation GE-SpMM's
+    GCN experiments use through PyG/DGL, §V-E)."""
+    m = a.n_rows
+    rp = a.row_ptr.astype(np.int64)
+    rows = np.repeat(np.arange(m, dtype=np.int64), np.diff(rp))
+    cols = a.col_ind.astype(np.int64)
+    if add_self_loops and m == a.n_cols:
+        # insert (i, i) where missing, keeping rows sorted (vectorised merge)
+        has = np.zeros(m, bool)
+        has[rows[cols == rows]] = True
+        need = ~has
+        before = np.bincount(rows[cols < rows], minlength=m)         # entries left of the diagonal
+        shift = np.concatenate([[0], np.cumsum(need)])               # inserted before row i
+        new_pos = np.arange(len(rows)) + shift[rows] + (need[rows] & (cols > rows))
+        diag_rows = np.nonzero(need)[0]
+        diag_pos = rp[diag_rows] + before[diag_rows] + shift[diag_rows]
+        total = len(rows) + len(diag_rows)
+        r2 = np.empty(total, np.int64)
+        c2 = np.empty(total, np.int64)
+        r2[new_pos], c2[new_pos] = rows, cols
+        r2[diag_pos], c2[diag_pos] = diag_rows, diag_rows
+        rows, cols = r2, c2
+    deg_r = np.bincount(rows, minlength=m).astype(np.float64)
+    deg_c = np.bincount(cols, minlength=a.n_cols).astype(np.float64)
+    vals = (1.0 / np.sqrt(deg_r[rows] * deg_c[cols])).astype(np.float32)
+    new_rp = np.zeros(m + 1, np.int64)
+    np.add.at(new_rp, rows + 1, 1)
+    return CsrMatrix(m, a.n_cols, np.cumsum(new_rp).astype(np.uint32), cols.astype(np.uint32), vals)
+
+
 def synthetic_features(m: int, f: int, classes: int, seed: int = 3):
     """Deterministic node features (reference make_random_dense) and labels."""
     h = api.make_random_dense(m, f, seed).data

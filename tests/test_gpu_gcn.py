@@ -81,9 +81,8 @@ def _dense_reference_step(a, h, y, w1, w2):
 
 def test_gcn_step_matches_dense_float64_reference(cuda):
     import torch
-    a = G.gen_powerlaw(1500, 60000, 1000, 1.0, 4)
-    G.randomize_values(a, 5)
-    cfg = gcn.GCNConfig(in_features=24, hidden=64, classes=7, lr=0.1)
+    a = gcn.normalize_adjacency(G.gen_powerlaw(1500, 60000, 1000, 1.0, 4))
+    cfg = gcn.GCNConfig(in_features=24, hidden=64, classes=7, lr=0.5)
     h, y = gcn.synthetic_features(a.n_rows, cfg.in_features, cfg.classes)
     adj, info = gcn.build_adjacency(a, cuda)
     model = gcn.GCN(cfg, cuda)
@@ -98,6 +97,7 @@ def test_gcn_step_matches_dense_float64_reference(cuda):
     g1 = (w1_before - model.w1.detach()) / cfg.lr
     assert torch.allclose(g1.double().cpu(), g1_ref, rtol=2e-3, atol=1e-5)
     # a few steps reduce the loss
-    losses = [model.step(ht, yt, adj).item() for _ in range(5)]
+    losses = [model.step(ht, yt, adj).item() for _ in range(10)]
     assert losses[-1] < loss.item()
+    assert np.isfinite(losses).all()
     adj.close()
