@@ -375,12 +375,15 @@ Plan* cached_plan(const gespmm_csr_t* a, uint32_t n, gespmm_reduce_t op,
   return p;
 }
 
-// Grow-only device staging for the host-buffer entry point.
+// Grow-only device staging for the host-buffer entry point: buffers, a
+// compute stream and copy-in / copy-out streams with per-chunk events.
+constexpr int kMaxChunks = 16;
 struct Workspace {
   std::mutex mu;
-  cudaStream_t stream = nullptr;
-  void* buf[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
-  size_t cap[6] = {0, 0, 0, 0, 0, 0};
+  cudaStream_t stream = nullptr, in = nullptr, out = nullptr;
+  cudaEvent_t ev_b = nullptr, ev_in[kMaxChunks] = {}, ev_done[kMaxChunks] = {};
+  void* buf[7] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+  size_t cap[7] = {0, 0, 0, 0, 0, 0, 0};
   cudaError_t reserve(int i, size_t bytes) {
     if (bytes <= cap[i]) return cudaSuccess;
     if (buf[i]) cudaFree(buf[i]);
@@ -399,10 +402,34 @@ Workspace* workspace() {
   cudaGetDevice(&dev);
   std::lock_guard<std::mutex> lk(g_ws_mu);
   if (!g_ws[dev]) {
-    g_ws[dev] = new Workspace();
-    cudaStreamCreateWithFlags(&g_ws[dev]->stream, cudaStreamNonBlocking);
+    auto* w = new Workspace();
+    cudaStreamCreateWithFlags(&w->stream, cudaStreamNonBlocking);
+    cudaStreamCreateWithFlags(&w->in, cudaStreamNonBlocking);
+    cudaStreamCreateWithFlags(&w->out, cudaStreamNonBlocking);
+    cudaEventCreateWithFlags(&w->ev_b, cudaEventDisableTiming);
+    for (int i = 0; i < kMaxChunks; ++i) {
+      cudaEventCreateWithFlags(&w->ev_in[i], cudaEventDisableTiming);
+      cudaEventCreateWithFlags(&w->ev_done[i], cudaEventDisableTiming);
+    }
+    g_ws[dev] = w;
   }
   return g_ws[dev];
+}
+
+// Host-side row_ptr checks (csr.hpp:118-131 order): row_ptr[0], monotonicity,
+// row_ptr[M] == nnz.  Column checks run on the device per row block.
+gespmm_status_t host_rowptr_status(const gespmm_csr_t* a, const char* who) {
+  ValidateResult r{};
+  r.row_ptr0 = a->row_ptr[0];
+  r.row_ptr_last = a->row_ptr[a->n_rows];
+  r.first_decrease = 0xffffffffu;
+  for (uint32_t i = 1; i <= a->n_rows; ++i)
+    if (a->row_ptr[i] < a->row_ptr[i - 1]) {
+      r.first_decrease = i;
+      break;
+    }
+  r.first_bad_key = ~0ull;
+  return validation_status(r, a->n_rows, a->n_cols, a->nnz, who);
 }
 
 gespmm_status_t device_validate(const gespmm_csr_t* a, cudaStream_t st, const char* who) {
@@ -502,6 +529,11 @@ gespmm_status_t gespmm_spmm_device(const gespmm_csr_t* a, const float* b, uint32
 gespmm_status_t gespmm_spmm_host(const gespmm_csr_t* a, const float* b, uint32_t b_rows,
                                  uint32_t n, gespmm_reduce_t op, float* c, int32_t* arg,
                                  const gespmm_options_t* opts) {
+  // Row-block pipeline: B and row_ptr go first; then for each nnz-balanced
+  // row block its col_ind/vals H2D (copy-in stream) -> column validation +
+  // kernel (compute stream) -> C rows D2H (copy-out stream), so the kernels and
+  // the D2H hide under the CSR upload.  On an error status the contents of c
+  // (and arg) are unspecified.
   if (!a) return fail(GESPMM_EINVAL, "null csr");
   gespmm_options_t o;
   if (opts) o = *opts; else gespmm_options_default(&o);
@@ -513,63 +545,195 @@ gespmm_status_t gespmm_spmm_host(const gespmm_csr_t* a, const float* b, uint32_t
                   a->n_rows, a->n_cols, b_rows);
     return fail(GESPMM_EDIM, buf);
   }
-  Workspace* ws = workspace();
-  std::lock_guard<std::mutex> lk(ws->mu);
-  cudaStream_t st = ws->stream;
-  const uint64_t m = a->n_rows, nnz = a->nnz;
-  GESPMM_CUDA(ws->reserve(0, sizeof(uint32_t) * (m + 1)), "spmm");
-  GESPMM_CUDA(ws->reserve(1, sizeof(uint32_t) * std::max<uint64_t>(nnz, 1)), "spmm");
-  GESPMM_CUDA(ws->reserve(2, sizeof(float) * std::max<uint64_t>(nnz, 1)), "spmm");
-  GESPMM_CUDA(cudaMemcpyAsync(ws->buf[0], a->row_ptr, sizeof(uint32_t) * (m + 1),
-                              cudaMemcpyHostToDevice, st), "spmm");
-  if (nnz) {
-    GESPMM_CUDA(cudaMemcpyAsync(ws->buf[1], a->col_ind, sizeof(uint32_t) * nnz,
-                                cudaMemcpyHostToDevice, st), "spmm");
-    GESPMM_CUDA(cudaMemcpyAsync(ws->buf[2], a->vals, sizeof(float) * nnz,
-                                cudaMemcpyHostToDevice, st), "spmm");
-  }
-  gespmm_csr_t d = *a;
-  d.row_ptr = static_cast<const uint32_t*>(ws->buf[0]);
-  d.col_ind = static_cast<const uint32_t*>(ws->buf[1]);
-  d.vals = static_cast<const float*>(ws->buf[2]);
   if (o.validate) {
-    s = device_validate(&d, st, "spmm");
+    s = host_rowptr_status(a, "spmm");
     if (s != GESPMM_OK) return s;
   }
   s = check_opts(o);
   if (s != GESPMM_OK) return s;
+  const uint64_t m = a->n_rows, nnz = a->nnz;
   if (m == 0) return GESPMM_OK;
-  if (n == 0) return fail(GESPMM_EINVAL, "native_spmm: N must be >= 1");
+  if (n == 0) {
+    // the reference validates columns before reporting N (native.hpp:103-110)
+    if (o.validate && nnz) {
+      Workspace* ws0 = workspace();
+      std::lock_guard<std::mutex> lk0(ws0->mu);
+      GESPMM_CUDA(ws0->reserve(0, sizeof(uint32_t) * (m + 1)), "spmm");
+      GESPMM_CUDA(ws0->reserve(1, sizeof(uint32_t) * nnz), "spmm");
+      GESPMM_CUDA(cudaMemcpyAsync(ws0->buf[0], a->row_ptr, sizeof(uint32_t) * (m + 1),
+                                  cudaMemcpyHostToDevice, ws0->stream), "spmm");
+      GESPMM_CUDA(cudaMemcpyAsync(ws0->buf[1], a->col_ind, sizeof(uint32_t) * nnz,
+                                  cudaMemcpyHostToDevice, ws0->stream), "spmm");
+      gespmm_csr_t d0 = *a;
+      d0.row_ptr = static_cast<const uint32_t*>(ws0->buf[0]);
+      d0.col_ind = static_cast<const uint32_t*>(ws0->buf[1]);
+      s = device_validate(&d0, ws0->stream, "spmm");
+      if (s != GESPMM_OK) return s;
+    }
+    return fail(GESPMM_EINVAL, "native_spmm: N must be >= 1");
+  }
+  Workspace* ws = workspace();
+  std::lock_guard<std::mutex> lk(ws->mu);
   const uint64_t bsz = uint64_t(b_rows) * n, csz = m * n;
+  GESPMM_CUDA(ws->reserve(0, sizeof(uint32_t) * (m + 1)), "spmm");
+  GESPMM_CUDA(ws->reserve(1, sizeof(uint32_t) * std::max<uint64_t>(nnz, 1)), "spmm");
+  GESPMM_CUDA(ws->reserve(2, sizeof(float) * std::max<uint64_t>(nnz, 1)), "spmm");
   GESPMM_CUDA(ws->reserve(3, sizeof(float) * std::max<uint64_t>(bsz, 1)), "spmm");
   GESPMM_CUDA(ws->reserve(4, sizeof(float) * csz), "spmm");
   if (arg) GESPMM_CUDA(ws->reserve(5, sizeof(int32_t) * csz), "spmm");
+  GESPMM_CUDA(ws->reserve(6, sizeof(uint32_t) * m), "spmm");
+  auto* d_rp = static_cast<uint32_t*>(ws->buf[0]);
+  auto* d_ci = static_cast<uint32_t*>(ws->buf[1]);
+  auto* d_v = static_cast<float*>(ws->buf[2]);
+  auto* d_b = static_cast<float*>(ws->buf[3]);
+  auto* d_c = static_cast<float*>(ws->buf[4]);
+  auto* d_arg = arg ? static_cast<int32_t*>(ws->buf[5]) : nullptr;
+  auto* d_order = static_cast<uint32_t*>(ws->buf[6]);
+
+  // ---- copy-in stream: row_ptr, B first (every block needs them)
+  GESPMM_CUDA(cudaMemcpyAsync(d_rp, a->row_ptr, sizeof(uint32_t) * (m + 1),
+                              cudaMemcpyHostToDevice, ws->in), "spmm");
   if (bsz)
-    GESPMM_CUDA(cudaMemcpyAsync(ws->buf[3], b, sizeof(float) * bsz, cudaMemcpyHostToDevice, st),
+    GESPMM_CUDA(cudaMemcpyAsync(d_b, b, sizeof(float) * bsz, cudaMemcpyHostToDevice, ws->in),
                 "spmm");
-  o.validate = 0;
-  Plan* p = nullptr;
-  std::unique_ptr<Plan> owned;
-  if (o.variant == GESPMM_VARIANT_TUNED) {
-    // host row_ptr is at hand: inspect it directly (no D2H); not cached, the
-    // staging buffers are reused across calls with different matrices.
-    s = plan_create_impl(&d, n, op, &o, st, a->row_ptr, &p);
-    if (s != GESPMM_OK) return s;
-    owned.reset(p);
-  } else {
-    s = plan_create_impl(&d, n, op, &o, st, nullptr, &p);
-    if (s != GESPMM_OK) return s;
-    owned.reset(p);
+
+  // ---- row blocks balanced by nnz (binary search on the host row_ptr)
+  const int chunks = nnz >= (uint64_t(8) << 20) ? 8 : 1;
+  uint32_t bound[kMaxChunks + 1];
+  bound[0] = 0;
+  for (int i = 1; i < chunks; ++i) {
+    const uint64_t target = nnz * uint64_t(i) / uint64_t(chunks);
+    const uint32_t* it = std::lower_bound(a->row_ptr, a->row_ptr + m + 1, uint32_t(target));
+    bound[i] = std::max<uint32_t>(bound[i - 1], uint32_t(std::min<uint64_t>(it - a->row_ptr, m)));
   }
-  s = plan_execute_impl(*p, static_cast<const float*>(ws->buf[3]), static_cast<float*>(ws->buf[4]),
-                        arg ? static_cast<int32_t*>(ws->buf[5]) : nullptr, st);
-  if (s != GESPMM_OK) return s;
-  GESPMM_CUDA(cudaMemcpyAsync(c, ws->buf[4], sizeof(float) * csz, cudaMemcpyDeviceToHost, st),
-              "spmm");
-  if (arg)
-    GESPMM_CUDA(cudaMemcpyAsync(arg, ws->buf[5], sizeof(int32_t) * csz, cudaMemcpyDeviceToHost, st),
-                "spmm");
-  GESPMM_CUDA(cudaStreamSynchronize(st), "spmm");
+  bound[chunks] = uint32_t(m);
+
+  // ---- schedule (tuned): per block, local rows in descending degree (LPT);
+  //      rows at or above the hub threshold first, for the row-per-CTA kernel
+  const bool tuned = o.variant == GESPMM_VARIANT_TUNED;
+  uint32_t hub_count[kMaxChunks] = {};
+  WarpShape wv{}, wsc{};
+  CtaShape cv{}, csc{};
+  if (tuned) {
+    const int32_t ht = o.hub_threshold;
+    const uint32_t hub_t = ht > 0 ? uint32_t(ht) : (ht < 0 ? 0xffffffffu : auto_hub_threshold(n, nnz));
+    std::vector<uint32_t> order(m);
+    uint32_t maxd = 0;
+    for (uint64_t r = 0; r < m; ++r) maxd = std::max(maxd, a->row_ptr[r + 1] - a->row_ptr[r]);
+    std::vector<uint32_t> count(size_t(maxd) + 2);
+    for (int ch = 0; ch < chunks; ++ch) {
+      std::fill(count.begin(), count.end(), 0u);
+      const uint32_t lo = bound[ch], hi = bound[ch + 1];
+      for (uint32_t r = lo; r < hi; ++r) ++count[maxd - (a->row_ptr[r + 1] - a->row_ptr[r])];
+      uint32_t acc = lo;
+      for (auto& cnt : count) {
+        const uint32_t t = cnt;
+        cnt = acc;
+        acc += t;
+      }
+      for (uint32_t r = lo; r < hi; ++r) {
+        const uint32_t d = a->row_ptr[r + 1] - a->row_ptr[r];
+        order[count[maxd - d]++] = r - lo;  // local id within the block
+        if (d >= hub_t) ++hub_count[ch];
+      }
+    }
+    GESPMM_CUDA(cudaMemcpyAsync(d_order, order.data(), sizeof(uint32_t) * m,
+                                cudaMemcpyHostToDevice, ws->in), "spmm");
+    // order[] lives in a host vector: wait for that copy before it goes away
+    GESPMM_CUDA(cudaStreamSynchronize(ws->in), "spmm");
+    const bool n4 = n % 4 == 0, n2 = n % 2 == 0;
+    wv = pick_warp_shape(n, n4, !n4 && n2);
+    wsc = pick_warp_shape(n, false, false);
+    cv = pick_cta_shape(n, n4, n2);
+    csc = pick_cta_shape(n, false, false);
+  }
+  GESPMM_CUDA(cudaEventRecord(ws->ev_b, ws->in), "spmm");
+  GESPMM_CUDA(cudaStreamWaitEvent(ws->stream, ws->ev_b, 0), "spmm");
+  ColCheck* cc = nullptr;
+  if (o.validate && nnz) GESPMM_CUDA(colcheck_begin(&cc, ws->stream), "spmm");
+
+  const bool fast = o.exact == 0;
+  for (int ch = 0; ch < chunks; ++ch) {
+    const uint32_t lo = bound[ch], hi = bound[ch + 1];
+    const uint64_t ps = a->row_ptr[lo], pe = a->row_ptr[hi];
+    if (pe > ps) {
+      GESPMM_CUDA(cudaMemcpyAsync(d_ci + ps, a->col_ind + ps, sizeof(uint32_t) * (pe - ps),
+                                  cudaMemcpyHostToDevice, ws->in), "spmm");
+      GESPMM_CUDA(cudaMemcpyAsync(d_v + ps, a->vals + ps, sizeof(float) * (pe - ps),
+                                  cudaMemcpyHostToDevice, ws->in), "spmm");
+    }
+    GESPMM_CUDA(cudaEventRecord(ws->ev_in[ch], ws->in), "spmm");
+    GESPMM_CUDA(cudaStreamWaitEvent(ws->stream, ws->ev_in[ch], 0), "spmm");
+    if (cc) GESPMM_CUDA(colcheck_rows(cc, d_rp + lo, hi - lo, d_ci, a->n_cols, nnz, ws->stream),
+                        "spmm");
+    SpmmArgs args{};
+    args.row_ptr = d_rp + lo;  // positions stay global; rows and outputs are block-local
+    args.col_ind = d_ci;
+    args.vals = d_v;
+    args.b = d_b;
+    args.c = d_c + uint64_t(lo) * n;
+    args.arg = d_arg ? d_arg + uint64_t(lo) * n : nullptr;
+    args.n = n;
+    args.arg_col = o.arg_kind == GESPMM_ARG_COLUMN;
+    args.skip_tail = o.fault_skip_tail;
+    args.hints = o.l2_hints;
+    if (hi > lo) {
+      if (!tuned) {
+        args.order = nullptr;
+        args.n_sched = hi - lo;
+        args.n_tiles = faithful_tiles(o.variant, o.cf, n);
+        GESPMM_CUDA(launch_faithful(o.variant, o.cf, op, fast, args, ws->stream), "spmm");
+      } else {
+        const bool v_ok = aligned(args.c, 16) && (!args.arg || aligned(args.arg, 16));
+        const WarpShape& w = v_ok ? wv : wsc;
+        const CtaShape& cs = v_ok ? cv : csc;
+        const bool v2 = aligned(args.c, 8) && (!args.arg || aligned(args.arg, 8));
+        const WarpShape& wsel = (w.vec == 2 && !v2) ? wsc : w;
+        const uint32_t nh = hub_count[ch];
+        if (nh) {
+          SpmmArgs h = args;
+          h.order = d_order + lo;
+          h.n_sched = nh;
+          const uint32_t tw = uint32_t(cs.vec * cs.warps * 32);
+          h.n_tiles = (n + tw - 1) / tw;
+          GESPMM_CUDA(launch_tuned_cta(cs, op, fast, h, ws->stream), "spmm");
+        }
+        args.order = d_order + lo + nh;
+        args.n_sched = hi - lo - nh;
+        args.n_tiles = (n + wsel.tile_width() - 1) / wsel.tile_width();
+        if (args.n_sched) GESPMM_CUDA(launch_tuned_warp(wsel, op, fast, args, ws->stream), "spmm");
+      }
+    }
+    GESPMM_CUDA(cudaEventRecord(ws->ev_done[ch], ws->stream), "spmm");
+    GESPMM_CUDA(cudaStreamWaitEvent(ws->out, ws->ev_done[ch], 0), "spmm");
+    const uint64_t rows = hi - lo;
+    if (rows) {
+      GESPMM_CUDA(cudaMemcpyAsync(c + uint64_t(lo) * n, d_c + uint64_t(lo) * n,
+                                  sizeof(float) * rows * n, cudaMemcpyDeviceToHost, ws->out),
+                  "spmm");
+      if (arg)
+        GESPMM_CUDA(cudaMemcpyAsync(arg + uint64_t(lo) * n, d_arg + uint64_t(lo) * n,
+                                    sizeof(int32_t) * rows * n, cudaMemcpyDeviceToHost, ws->out),
+                    "spmm");
+    }
+  }
+  if (cc) {
+    uint64_t key = ~0ull;
+    uint32_t brow = 0, bcol = 0;
+    GESPMM_CUDA(colcheck_end(cc, d_rp, d_ci, uint32_t(m), &key, &brow, &bcol, ws->stream), "spmm");
+    GESPMM_CUDA(cudaStreamSynchronize(ws->out), "spmm");
+    ValidateResult r{};
+    r.row_ptr0 = 0;
+    r.row_ptr_last = uint32_t(nnz);
+    r.first_decrease = 0xffffffffu;
+    r.first_bad_key = key;
+    r.bad_row = brow;
+    r.bad_col = bcol;
+    s = validation_status(r, a->n_rows, a->n_cols, nnz, "spmm");
+    if (s != GESPMM_OK) return s;
+  }
+  GESPMM_CUDA(cudaStreamSynchronize(ws->stream), "spmm");
+  GESPMM_CUDA(cudaStreamSynchronize(ws->out), "spmm");
   return GESPMM_OK;
 }
 

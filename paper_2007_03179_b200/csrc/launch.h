@@ -62,4 +62,15 @@ struct ValidateResult {
 cudaError_t validate_csr_device(uint32_t m, uint32_t k, uint64_t nnz, const uint32_t* row_ptr,
                                 const uint32_t* col_ind, ValidateResult* out, cudaStream_t s);
 
+// Chunked column check: begin, one call per row block (row_ptr_chunk points at
+// the block's first row_ptr entry; positions stay global), end (locates the
+// first violation's row, synchronises `st`, frees).
+struct ColCheck;
+cudaError_t colcheck_begin(ColCheck** out, cudaStream_t st);
+cudaError_t colcheck_rows(ColCheck* c, const uint32_t* row_ptr_chunk, uint32_t m_chunk,
+                          const uint32_t* col_ind, uint32_t k, uint64_t usable, cudaStream_t st);
+cudaError_t colcheck_end(ColCheck* c, const uint32_t* row_ptr, const uint32_t* col_ind, uint32_t m,
+                         uint64_t* first_bad_key, uint32_t* bad_row, uint32_t* bad_col,
+                         cudaStream_t st);
+
 }  // namespace gespmm

@@ -105,4 +105,55 @@ cudaError_t validate_csr_device(uint32_t m, uint32_t k, uint64_t nnz, const uint
   return e;
 }
 
+// ---- chunked column check (the host pipeline validates row blocks as their
+// col_ind arrives; row_ptr itself is checked on the host) --------------------
+struct ColCheck {
+  Scratch* s = nullptr;
+};
+
+cudaError_t colcheck_begin(ColCheck** out, cudaStream_t st) {
+  auto* c = new ColCheck();
+  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&c->s), sizeof(Scratch), st);
+  if (e == cudaSuccess) {
+    static const Scratch init{0xffffffffu, 0u, ~0ull, 0u, 0u};
+    e = cudaMemcpyAsync(c->s, &init, sizeof(init), cudaMemcpyHostToDevice, st);
+  }
+  if (e != cudaSuccess) {
+    delete c;
+    return e;
+  }
+  *out = c;
+  return cudaSuccess;
+}
+
+cudaError_t colcheck_rows(ColCheck* c, const uint32_t* row_ptr_chunk, uint32_t m_chunk,
+                          const uint32_t* col_ind, uint32_t k, uint64_t usable, cudaStream_t st) {
+  if (m_chunk == 0) return cudaSuccess;
+  uint64_t blocks = (uint64_t(m_chunk) + 7) / 8;
+  if (blocks > 148ull * 16) blocks = 148ull * 16;
+  k_check_cols<<<uint32_t(blocks), 256, 0, st>>>(row_ptr_chunk, col_ind, m_chunk, k, usable, c->s);
+  note_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t colcheck_end(ColCheck* c, const uint32_t* row_ptr, const uint32_t* col_ind, uint32_t m,
+                         uint64_t* first_bad_key, uint32_t* bad_row, uint32_t* bad_col,
+                         cudaStream_t st) {
+  Scratch host{};
+  cudaError_t e = cudaSuccess;
+  if (m > 0) {
+    k_locate<<<1, 32, 0, st>>>(row_ptr, col_ind, m, c->s);
+    note_launch();
+    e = cudaGetLastError();
+  }
+  if (e == cudaSuccess) e = cudaMemcpyAsync(&host, c->s, sizeof(host), cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  cudaFreeAsync(c->s, st);
+  delete c;
+  *first_bad_key = e == cudaSuccess ? host.first_bad_key : ~0ull;
+  *bad_row = host.bad_row;
+  *bad_col = host.bad_col;
+  return e;
+}
+
 }  // namespace gespmm
