@@ -394,14 +394,18 @@ def run_ours(args, cfg):
                 raise RuntimeError(_lib.last_error())
 
         host_call()
-        e2e_steps = max(2, min(5, args.steps))
+        e2e_steps = max(3, min(10, args.steps))
         if world > 1:
             import torch.distributed as dist
             dist.barrier()
+        e2e_each = []
         t0 = time.perf_counter()
         for _ in range(e2e_steps):
+            t1 = time.perf_counter()
             host_call()
+            e2e_each.append(1e3 * (time.perf_counter() - t1))
         e2e_s = time.perf_counter() - t0
+        log("[bench] e2e per-step ms: " + " ".join(f"{x:.2f}" for x in e2e_each))
         if world > 1:
             import torch.distributed as dist
             t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
@@ -412,7 +416,11 @@ def run_ours(args, cfg):
         e2e = {"value": round(total_flops * e2e_steps / e2e_s / 1e9, 3), "unit": "GFLOP/s",
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                "ms_per_step": round(1e3 * e2e_s / e2e_steps, 3), "steps": e2e_steps,
-               "path": "gespmm_spmm_host (validate + H2D + plan + kernels + D2H)"}
+               "step_ms": {"min": round(min(e2e_each), 3),
+                           "median": round(statistics.median(e2e_each), 3),
+                           "max": round(max(e2e_each), 3)},
+               "path": "gespmm_spmm_host: row_ptr+B H2D, then 8 nnz-balanced row blocks pipelined "
+                       "(CSR H2D | validate+kernel | C D2H on three streams)"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:

@@ -11,6 +11,8 @@
 //   reduce_op_by_name   include/spmm/reduce_op.hpp:32-36
 #include <algorithm>
 #include <atomic>
+#include <chrono>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <list>
@@ -416,6 +418,22 @@ Workspace* workspace() {
   return g_ws[dev];
 }
 
+// GESPMM_TRACE=1: host-side phase timestamps of the host entry point (stderr).
+struct Trace {
+  bool on = false;
+  std::chrono::steady_clock::time_point t0;
+  Trace() {
+    const char* e = std::getenv("GESPMM_TRACE");
+    on = e && e[0] == '1';
+    t0 = std::chrono::steady_clock::now();
+  }
+  void mark(const char* what) const {
+    if (!on) return;
+    const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    std::fprintf(stderr, "[gespmm] %8.3f ms  %s\n", ms, what);
+  }
+};
+
 // Host-side row_ptr checks (csr.hpp:118-131 order): row_ptr[0], monotonicity,
 // row_ptr[M] == nnz.  Column checks run on the device per row block.
 gespmm_status_t host_rowptr_status(const gespmm_csr_t* a, const char* who) {
@@ -535,6 +553,7 @@ gespmm_status_t gespmm_spmm_host(const gespmm_csr_t* a, const float* b, uint32_t
   // the D2H hide under the CSR upload.  On an error status the contents of c
   // (and arg) are unspecified.
   if (!a) return fail(GESPMM_EINVAL, "null csr");
+  const Trace tr;
   gespmm_options_t o;
   if (opts) o = *opts; else gespmm_options_default(&o);
   gespmm_status_t s = check_op(op, arg);
@@ -546,6 +565,7 @@ gespmm_status_t gespmm_spmm_host(const gespmm_csr_t* a, const float* b, uint32_t
     return fail(GESPMM_EDIM, buf);
   }
   if (o.validate) {
+    tr.mark("enter");
     s = host_rowptr_status(a, "spmm");
     if (s != GESPMM_OK) return s;
   }
@@ -589,6 +609,7 @@ gespmm_status_t gespmm_spmm_host(const gespmm_csr_t* a, const float* b, uint32_t
   auto* d_c = static_cast<float*>(ws->buf[4]);
   auto* d_arg = arg ? static_cast<int32_t*>(ws->buf[5]) : nullptr;
   auto* d_order = static_cast<uint32_t*>(ws->buf[6]);
+  tr.mark("workspace ready");
 
   // ---- copy-in stream: row_ptr, B first (every block needs them)
   GESPMM_CUDA(cudaMemcpyAsync(d_rp, a->row_ptr, sizeof(uint32_t) * (m + 1),
@@ -647,6 +668,7 @@ gespmm_status_t gespmm_spmm_host(const gespmm_csr_t* a, const float* b, uint32_t
     cv = pick_cta_shape(n, n4, n2);
     csc = pick_cta_shape(n, false, false);
   }
+  tr.mark("row_ptr+B enqueued, schedule built");
   GESPMM_CUDA(cudaEventRecord(ws->ev_b, ws->in), "spmm");
   GESPMM_CUDA(cudaStreamWaitEvent(ws->stream, ws->ev_b, 0), "spmm");
   ColCheck* cc = nullptr;
@@ -717,6 +739,7 @@ gespmm_status_t gespmm_spmm_host(const gespmm_csr_t* a, const float* b, uint32_t
                     "spmm");
     }
   }
+  tr.mark("all blocks enqueued");
   if (cc) {
     uint64_t key = ~0ull;
     uint32_t brow = 0, bcol = 0;
@@ -732,8 +755,10 @@ gespmm_status_t gespmm_spmm_host(const gespmm_csr_t* a, const float* b, uint32_t
     s = validation_status(r, a->n_rows, a->n_cols, nnz, "spmm");
     if (s != GESPMM_OK) return s;
   }
+  tr.mark("validation done");
   GESPMM_CUDA(cudaStreamSynchronize(ws->stream), "spmm");
   GESPMM_CUDA(cudaStreamSynchronize(ws->out), "spmm");
+  tr.mark("done");
   return GESPMM_OK;
 }
 
