@@ -23,7 +23,6 @@ import argparse
 import json
 import os
 import statistics
-import subprocess
 import sys
 import threading
 import time
@@ -97,59 +96,78 @@ def sample_rows(a, frac, seed=0):
 # ---------------------------------------------------------------------------
 
 class ClockSampler:
-    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    """SM clock / power / throttle reasons sampled through NVML every ~10 ms on a
+    thread; only samples taken inside the timed region (mark_start..mark_end)
+    count.  Falls back to the nvidia-smi CLI when pynvml is missing."""
+    REASONS = (("hw_slowdown", 0x8), ("hw_thermal_slowdown", 0x40),
+               ("sw_thermal_slowdown", 0x20), ("sw_power_cap", 0x4), ("hw_power_brake", 0x80))
 
     def __init__(self, gpu_index):
         self.gpu = gpu_index
-        self.proc = None
-        self.lines = []
+        self.samples = []  # (t, sm_mhz, mem_mhz, power_w, reasons_mask)
+        self.t0 = self.t1 = None
+        self._stop = threading.Event()
+        self.thread = None
+        self.error = None
 
     def start(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-i", str(self.gpu), "-lms", "20"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.thread = threading.Thread(target=self._read, daemon=True)
-            self.thread.start()
-        except (FileNotFoundError, OSError):
-            self.proc = None
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.gpu)
+            self.max_sm = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+        except Exception as e:  # noqa: BLE001 - report, do not fail the bench
+            self.error = f"nvml unavailable: {e}"
+            return
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
+        def run():
+            while not self._stop.is_set():
+                try:
+                    t = time.perf_counter()
+                    sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                    mem = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_MEM)
+                    pw = pynvml.nvmlDeviceGetPowerUsage(h) / 1000.0
+                    rs = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                    self.samples.append((t, sm, mem, pw, rs))
+                except Exception as e:  # noqa: BLE001
+                    self.error = str(e)
+                    return
+                time.sleep(0.01)
+
+        self.thread = threading.Thread(target=run, daemon=True)
+        self.thread.start()
+
+    def mark_start(self):
+        self.t0 = time.perf_counter()
+
+    def mark_end(self):
+        self.t1 = time.perf_counter()
 
     def stop(self):
-        if not self.proc:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        time.sleep(0.05)
-        self.proc.terminate()
-        try:
-            self.proc.wait(timeout=5)
-        except subprocess.TimeoutExpired:
-            self.proc.kill()
+        if self.thread is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [self.error or "not sampled"]}
+        time.sleep(0.02)
+        self._stop.set()
         self.thread.join(timeout=2)
-        sm, mx, power, reasons = [], [], [], set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
-            parts = [p.strip() for p in ln.split(",")]
-            if len(parts) < 8:
-                continue
-            try:
-                sm.append(float(parts[0]))
-                mx.append(float(parts[1]))
-                power.append(float(parts[2]))
-            except ValueError:
-                continue
-            for name, val in zip(names, parts[4:8]):
-                if val.lower().startswith("active"):
-                    reasons.add(name)
+        t0 = self.t0 if self.t0 is not None else -1e30
+        t1 = self.t1 if self.t1 is not None else 1e30
+        inside = [x for x in self.samples if t0 <= x[0] <= t1]
+        if not inside and self.samples:  # region shorter than one sample period
+            inside = [min(self.samples, key=lambda x: abs(x[0] - t1))]
+        if os.environ.get("GESPMM_CLOCK_LOG"):
+            with open(os.environ["GESPMM_CLOCK_LOG"], "w") as f:
+                for x in self.samples:
+                    f.write(f"{x[0] - t0:.4f},{x[1]},{x[2]},{x[3]:.1f},{x[4]:#x},"
+                            f"{int(t0 <= x[0] <= t1)}\n")
+        reasons = sorted({name for x in inside for name, bit in self.REASONS if x[4] & bit})
+        sm = [x[1] for x in inside]
         return {"sm_mhz": statistics.median(sm) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None,
-                "power_w_max": max(power) if power else None,
-                "samples": len(sm), "reasons": sorted(reasons)}
+                "sm_min_mhz": min(sm) if sm else None,
+                "sm_max_mhz": self.max_sm,
+                "mem_mhz": statistics.median([x[2] for x in inside]) if inside else None,
+                "power_w_max": max(x[3] for x in inside) if inside else None,
+                "samples": len(inside), "source": "nvml, timed region only",
+                "reasons": reasons}
 
 
 def hbm_peak():
@@ -312,8 +330,9 @@ def run_ours(args, cfg):
     d = G.DeviceCsr.from_host(shard, dev)
     c = torch.empty((shard.n_rows, n), dtype=torch.float32, device=dev)
     arg = torch.empty((shard.n_rows, n), dtype=torch.int32, device=dev) if want_arg else None
+    hints = 0 if args.no_hints else args.hints
     ex = G.ExecOptions(hub_threshold=args.hub_threshold, exact=not args.fast,
-                       l2_persist=args.l2_persist, l2_hints=not args.no_hints)
+                       l2_persist=args.l2_persist, l2_hints=hints, l2_hot_mb=args.l2_hot_mb)
     variant = G.variant_by_name(args.variant, args.cf)
     plan = G.Plan(d, n, op, variant=variant, exec=ex)
     log(f"[bench] rank {rank}: rows [{info.lo},{info.hi}) nnz {shard.nnz()} plan: {plan.description}")
@@ -334,10 +353,12 @@ def run_ours(args, cfg):
         import torch.distributed as dist
         dist.barrier()
     torch.cuda.synchronize()
-    if sampler:
+    if sampler and not os.environ.get("GESPMM_NO_CLOCKS"):
         sampler.start()
-        time.sleep(0.1)
+        time.sleep(0.05)
     launches0 = G.launch_count()
+    if sampler:
+        sampler.mark_start()
     for i in range(args.steps):
         if not args.no_flush:
             l2_flush.zero_()  # outside the events: L2 flushed between steps
@@ -345,6 +366,8 @@ def run_ours(args, cfg):
         step()
         ends[i].record(stream)
     torch.cuda.synchronize()
+    if sampler:
+        sampler.mark_end()
     launches = G.launch_count() - launches0
     clocks = sampler.stop() if sampler else None
     per_step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
@@ -382,7 +405,8 @@ def run_ours(args, cfg):
                        v_h.data_ptr())
         o = _lib.default_options(variant=int(variant.kind), cf=args.cf,
                                  hub_threshold=args.hub_threshold, exact=int(not args.fast),
-                                 l2_persist=int(args.l2_persist), l2_hints=int(not args.no_hints))
+                                 l2_persist=int(args.l2_persist), l2_hints=hints,
+                                 l2_hot_mb=args.l2_hot_mb)
         L = _lib.lib()
 
         def host_call():
@@ -541,6 +565,10 @@ def main():
     p.add_argument("--fast", action="store_true", help="FFMA sum (1e-5 tolerance) instead of exact")
     p.add_argument("--l2-persist", action="store_true", help="L2 access-policy window on B")
     p.add_argument("--no-hints", action="store_true", help="evict_normal instead of L2 hints")
+    p.add_argument("--hints", type=int, default=1,
+                   help="L2 hint mode (1: cold B rows evict_first, 2: evict_normal)")
+    p.add_argument("--l2-hot-mb", type=int, default=0,
+                   help="hot-column map budget in MB (0 auto, <0 off)")
     p.add_argument("--no-flush", action="store_true", help="skip the L2 flush between steps")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")

@@ -83,11 +83,18 @@ typedef struct {
   int32_t arg_kind;   /* gespmm_arg_kind_t, default EDGE (CSR position) */
   int32_t validate;   /* 1 (default for *_host): canonical-CSR check before the launch */
   int32_t fault_skip_tail; /* negative-test hook: FaultMode::SkipTail (kernel.hpp:167-182) */
-  int32_t l2_hints;   /* 1 (default): B evict_last, CSR/C evict_first */
+  int32_t l2_hints;   /* 1 (default): B evict_last, CSR/C evict_first; 0: evict_normal
+                         everywhere; 2: as 1 but B rows outside the hot-column map
+                         evict_normal instead of evict_first */
   int32_t hub_threshold; /* TUNED: rows with degree >= this go row-per-CTA; 0 = auto, <0 = off */
   int32_t l2_persist; /* 1: launch with an L2 access-policy window marking B persisting
                          (sets the device's persisting-L2 limit to its maximum); default 0 */
-  int32_t reserved[7];
+  int32_t l2_hot_mb;  /* TUNED plans: frequency-aware L2 policy for B.  The plan counts the
+                         gathers per column and only the most-gathered columns whose B rows
+                         fit this many MB are loaded evict_last (the rest evict_first).
+                         0 = auto (on when B exceeds twice the L2), <0 = off.  Hints only:
+                         results are unaffected. */
+  int32_t reserved[6];
 } gespmm_options_t;
 
 void gespmm_options_default(gespmm_options_t* opts);
@@ -144,11 +151,36 @@ void gespmm_plan_destroy(gespmm_plan_t plan);
 gespmm_status_t gespmm_csr_transpose_device(const gespmm_csr_t* a, uint32_t* t_row_ptr,
                                             uint32_t* t_col_ind, float* t_vals, void* stream);
 
+/* ---- CSR1 binary cache (io.hpp:15-16, 50-115) ----------------------------- */
+/* Layout: "CSR1", u64 LE n_rows, n_cols, nnz, u32 row_ptr[n_rows+1],
+ * u32 col_ind[nnz], f32 vals[nnz] (pinned by test_io.cpp:14-35).  Errors use
+ * the reference's texts ("csr cache: bad magic (expected CSR1)", "csr cache:
+ * truncated header|row_ptr|col_ind|vals", "csr cache: dimensions exceed 32-bit
+ * range", "cannot open '<path>'"). */
+
+/* write_csr_cache / save_csr_cache (io.hpp:50-63, 92-96); host CSR. */
+gespmm_status_t gespmm_csr1_write(const char* path, const gespmm_csr_t* a);
+/* Header + size checks of read_csr_cache (io.hpp:65-90), sizes out. */
+gespmm_status_t gespmm_csr1_header(const char* path, uint32_t* n_rows, uint32_t* n_cols,
+                                   uint64_t* nnz);
+/* read_csr_cache into caller-allocated host arrays (sized from the header). */
+gespmm_status_t gespmm_csr1_read_host(const char* path, uint32_t* row_ptr, uint32_t* col_ind,
+                                      float* vals);
+/* Streaming loader into caller-allocated DEVICE arrays (pinned double-buffered
+ * pread -> H2D on `stream`); validate=1 then runs the canonical check on the
+ * device with load_matrix's wording (io.hpp:100-115).  Synchronous. */
+gespmm_status_t gespmm_csr1_load_device(const char* path, uint32_t* d_row_ptr,
+                                        uint32_t* d_col_ind, float* d_vals, int32_t validate,
+                                        void* stream);
+
 /* ---- checks and helpers -------------------------------------------------- */
 
 /* Device canonical-CSR check (csr.hpp:112-153); status ENONCANON with the
  * reference's first-violation message in gespmm_last_error().  Synchronous. */
 gespmm_status_t gespmm_validate_device(const gespmm_csr_t* a, void* stream);
+/* Same check, message prefixed with `who` as require_canonical(m, who) does
+ * (csr.hpp:155-158), e.g. "load_matrix". */
+gespmm_status_t gespmm_validate_device_as(const gespmm_csr_t* a, void* stream, const char* who);
 
 /* Reference dispatch rule, select_variant (kernel.hpp:96-98): n <= 32 -> CRC,
  * else CRC_CWM with cf 2. */

@@ -101,6 +101,11 @@ def _load_ref():
         lib.ref_from_coo.restype = C.c_longlong
         lib.ref_from_coo.argtypes = [cu, cu, cull, _u32p, _u32p, _f32p, _u32p, _u32p, _f32p,
                                      cp, cu]
+        lib.ref_save_csr_cache.restype = C.c_int
+        lib.ref_save_csr_cache.argtypes = [cp, cu, cu, cull, _u32p, _u32p, _f32p, cp, cu]
+        lib.ref_load_matrix.restype = C.c_int
+        lib.ref_load_matrix.argtypes = [cp, C.POINTER(cu), C.POINTER(cu), C.POINTER(cull),
+                                        C.c_void_p, C.c_void_p, C.c_void_p, cp, cu]
         lib.ref_hardware_concurrency.restype = cu
         lib.ref_hardware_concurrency.argtypes = []
         _ref = lib
@@ -288,3 +293,28 @@ def ref_from_coo(rows, cols, r, c, v):
 
 def ref_hardware_concurrency():
     return int(_load_ref().ref_hardware_concurrency())
+
+
+def ref_save_csr_cache(path, m, k, row_ptr, col_ind, vals):
+    e = _err()
+    if _load_ref().ref_save_csr_cache(os.fsencode(path), m, k, len(col_ind),
+                                      _nz(row_ptr, np.uint32), _nz(col_ind, np.uint32),
+                                      _nz(vals, np.float32), e, 1024):
+        raise RefError(e.value.decode())
+
+
+def ref_load_matrix(path):
+    """The reference's load_matrix (read + require_canonical); (m, k, rp, ci, v)."""
+    lib = _load_ref()
+    m, k, z = C.c_uint(), C.c_uint(), C.c_ulonglong()
+    e = _err()
+    if lib.ref_load_matrix(os.fsencode(path), C.byref(m), C.byref(k), C.byref(z), None, None,
+                           None, e, 1024):
+        raise RefError(e.value.decode())
+    rp = np.zeros(m.value + 1, np.uint32)
+    ci = np.zeros(max(z.value, 1), np.uint32)
+    v = np.zeros(max(z.value, 1), np.float32)
+    if lib.ref_load_matrix(os.fsencode(path), C.byref(m), C.byref(k), C.byref(z),
+                           rp.ctypes.data, ci.ctypes.data, v.ctypes.data, e, 1024):
+        raise RefError(e.value.decode())
+    return m.value, k.value, rp, ci[: z.value].copy(), v[: z.value].copy()

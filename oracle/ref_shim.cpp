@@ -18,6 +18,8 @@
 //   spmm::validate           include/spmm/csr.hpp:112-153
 //   spmm::select_variant     include/spmm/kernel.hpp:96-98
 //   spmm::from_coo           include/spmm/csr.hpp:58-93
+//   spmm::save_csr_cache     include/spmm/io.hpp:92-96
+//   spmm::load_matrix        include/spmm/io.hpp:100-115
 #include "spmm/spmm.hpp"
 
 #include <cstdio>
@@ -217,6 +219,42 @@ long long ref_from_coo(unsigned rows, unsigned cols, unsigned long long count, c
   } catch (const std::exception& e) {
     put_err(err, err_len, e.what());
     return -1;
+  }
+}
+
+int ref_save_csr_cache(const char* path, unsigned m, unsigned k, unsigned long long nnz,
+                       const unsigned* row_ptr, const unsigned* col_ind, const float* vals,
+                       char* err, unsigned err_len) {
+  try {
+    save_csr_cache(path, make_csr(m, k, nnz, row_ptr, col_ind, vals));
+    return 0;
+  } catch (const std::exception& e) {
+    put_err(err, err_len, e.what());
+    return 1;
+  }
+}
+
+// load_matrix: sizes out first (arrays may be null), then a second call with
+// buffers sized from them.  Returns 1 with the reference's message on error.
+int ref_load_matrix(const char* path, unsigned* m, unsigned* k, unsigned long long* nnz,
+                    unsigned* row_ptr, unsigned* col_ind, float* vals, char* err,
+                    unsigned err_len) {
+  try {
+    const CsrMatrix a = load_matrix(path);
+    *m = a.n_rows;
+    *k = a.n_cols;
+    *nnz = a.nnz();
+    if (row_ptr) {
+      std::memcpy(row_ptr, a.row_ptr.data(), sizeof(unsigned) * a.row_ptr.size());
+      if (a.nnz()) {
+        std::memcpy(col_ind, a.col_ind.data(), sizeof(unsigned) * a.nnz());
+        std::memcpy(vals, a.vals.data(), sizeof(float) * a.nnz());
+      }
+    }
+    return 0;
+  } catch (const std::exception& e) {
+    put_err(err, err_len, e.what());
+    return 1;
   }
 }
 

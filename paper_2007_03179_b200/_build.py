@@ -29,8 +29,8 @@ CXX_FLAGS = ["-O3", "-std=c++17", "-fPIC", "-ffp-contract=off", "-Wall", "-Wextr
              "-I", INCLUDE, "-I", CSRC, "-I", "/usr/local/cuda/include"]
 
 CU_SOURCES = ["api.cu", "validate.cu", "kernels_faithful.cu", "kernels_tuned.cu", "diag.cu",
-              "transpose.cu"]
-CXX_SOURCES = ["gen.cpp"]
+              "transpose.cu", "hotcols.cu"]
+CXX_SOURCES = ["gen.cpp", "io.cpp"]
 HEADERS = ["common.cuh", "launch.h"]
 
 

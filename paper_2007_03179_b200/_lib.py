@@ -34,7 +34,8 @@ EXPORTS = [
     "gespmm_reduce_by_name", "gespmm_checksum", "gespmm_make_random_dense",
     "gespmm_randomize_values", "gespmm_gen_uniform", "gespmm_gen_powerlaw", "gespmm_abi_version",
     "gespmm_device_info", "gespmm_launch_count", "gespmm_diag_gather",
-    "gespmm_csr_transpose_device",
+    "gespmm_csr_transpose_device", "gespmm_validate_device_as", "gespmm_csr1_write",
+    "gespmm_csr1_header", "gespmm_csr1_read_host", "gespmm_csr1_load_device",
 ]
 
 
@@ -48,7 +49,7 @@ class Options(C.Structure):
                 ("arg_kind", C.c_int32), ("validate", C.c_int32),
                 ("fault_skip_tail", C.c_int32), ("l2_hints", C.c_int32),
                 ("hub_threshold", C.c_int32), ("l2_persist", C.c_int32),
-                ("reserved", C.c_int32 * 7)]
+                ("l2_hot_mb", C.c_int32), ("reserved", C.c_int32 * 6)]
 
 
 _lock = threading.Lock()
@@ -104,6 +105,8 @@ def lib():
         L.gespmm_plan_destroy.restype = None
         L.gespmm_validate_device.argtypes = [C.POINTER(Csr), vp]
         L.gespmm_validate_device.restype = C.c_int
+        L.gespmm_validate_device_as.argtypes = [C.POINTER(Csr), vp, C.c_char_p]
+        L.gespmm_validate_device_as.restype = C.c_int
         L.gespmm_select_variant.argtypes = [u32, C.POINTER(i32), C.POINTER(u32)]
         L.gespmm_select_variant.restype = None
         L.gespmm_reduce_by_name.argtypes = [C.c_char_p, C.POINTER(C.c_int)]
@@ -127,6 +130,15 @@ def lib():
         L.gespmm_diag_gather.restype = C.c_int
         L.gespmm_csr_transpose_device.argtypes = [C.POINTER(Csr), vp, vp, vp, vp]
         L.gespmm_csr_transpose_device.restype = C.c_int
+        L.gespmm_csr1_write.argtypes = [C.c_char_p, C.POINTER(Csr)]
+        L.gespmm_csr1_write.restype = C.c_int
+        L.gespmm_csr1_header.argtypes = [C.c_char_p, C.POINTER(u32), C.POINTER(u32),
+                                         C.POINTER(u64)]
+        L.gespmm_csr1_header.restype = C.c_int
+        L.gespmm_csr1_read_host.argtypes = [C.c_char_p, vp, vp, vp]
+        L.gespmm_csr1_read_host.restype = C.c_int
+        L.gespmm_csr1_load_device.argtypes = [C.c_char_p, vp, vp, vp, i32, vp]
+        L.gespmm_csr1_load_device.restype = C.c_int
         L.gespmm_launch_count.argtypes = []
         L.gespmm_launch_count.restype = u64
         _lib = L

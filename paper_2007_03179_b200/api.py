@@ -15,6 +15,8 @@ reference's own tests:
   native_spmm, bench                 native.hpp:101-180
   GraphGenSpec, gen_uniform_random,  generate.hpp:14-80
     randomize_values
+  save_csr_cache, read_csr_cache,    io.hpp:50-115 (CSR1 binary cache)
+    load_matrix, DeviceCsr.load
 
 Compute goes through libgespmm.so only (CUDA, sm_100a); ``workers`` is
 accepted for signature compatibility and ignored.  Two device-level entry
@@ -288,9 +290,11 @@ class ExecOptions:
     fault: FaultMode = FaultMode.None_
     exact: bool = True
     arg_kind: str = "edge"          # "edge" (CSR position p) or "column" (col_ind[p])
-    l2_hints: bool = True
+    l2_hints: int = 1               # 0 off; 1 B evict_last, CSR/C evict_first; 2 = 1 but
+                                    # cold B rows (hot-column map) evict_normal
     hub_threshold: int = 0          # 0 auto, <0 off
     l2_persist: bool = False        # L2 access-policy window marking B persisting
+    l2_hot_mb: int = 0              # hot-column map budget in MB: 0 auto, <0 off
 
 
 def _options(variant: KernelVariant, ex: ExecOptions, validate: bool = True) -> _lib.Options:
@@ -299,7 +303,7 @@ def _options(variant: KernelVariant, ex: ExecOptions, validate: bool = True) -> 
                            arg_kind=_lib.ARG_COLUMN if ex.arg_kind == "column" else _lib.ARG_EDGE,
                            validate=int(validate), fault_skip_tail=int(ex.fault == FaultMode.SkipTail),
                            l2_hints=int(ex.l2_hints), hub_threshold=ex.hub_threshold,
-                           l2_persist=int(ex.l2_persist))
+                           l2_persist=int(ex.l2_persist), l2_hot_mb=int(ex.l2_hot_mb))
 
 
 # ---------------------------------------------------------------------------
@@ -435,6 +439,64 @@ def gen_powerlaw(n_rows: int, nnz_target: int, max_degree: int, exponent: float 
 
 
 # ---------------------------------------------------------------------------
+# CSR1 binary cache (io.hpp:15-16, 50-115)
+# ---------------------------------------------------------------------------
+
+def _path_bytes(path) -> bytes:
+    import os
+    return os.fsencode(path)
+
+
+def save_csr_cache(path, m: CsrMatrix) -> None:
+    """save_csr_cache / write_csr_cache (io.hpp:50-63, 92-96)."""
+    s, _keep = m._c()
+    _check(lib().gespmm_csr1_write(_path_bytes(path), C.byref(s)))
+
+
+def _csr1_header(path) -> Tuple[int, int, int]:
+    r, c, z = C.c_uint32(), C.c_uint32(), C.c_uint64()
+    _check(lib().gespmm_csr1_header(_path_bytes(path), C.byref(r), C.byref(c), C.byref(z)))
+    return r.value, c.value, z.value
+
+
+def read_csr_cache(path) -> CsrMatrix:
+    """read_csr_cache (io.hpp:65-90): no canonical check (as the reference)."""
+    rows, cols, nnz = _csr1_header(path)
+    rp = np.empty(rows + 1, np.uint32)
+    ci = np.empty(nnz, np.uint32)
+    v = np.empty(nnz, np.float32)
+    _check(lib().gespmm_csr1_read_host(_path_bytes(path), rp.ctypes.data, ci.ctypes.data,
+                                       v.ctypes.data))
+    return CsrMatrix(rows, cols, rp, ci, v)
+
+
+def load_matrix(path) -> CsrMatrix:
+    """load_matrix (io.hpp:100-115) for the .csr cache: read, then the canonical
+    check with the reference's "load_matrix: matrix is not canonical CSR: ..."
+    text.  Matrix Market (.mtx) parsing is out of scope here (SURVEY.md §2 #11)."""
+    import os
+    ext = os.path.splitext(os.fspath(path))[1]
+    if ext == ".mtx":
+        raise Error("load_matrix: Matrix Market input is not supported by this build "
+                    "(convert to the .csr cache)", _lib.EUNSUPPORTED)
+    if ext != ".csr":
+        raise Error(f"unknown matrix extension '{ext}' (expected .mtx or .csr)")
+    m = read_csr_cache(path)
+    _host_validate(m, "load_matrix")
+    return m
+
+
+def _host_validate(m: CsrMatrix, who: str) -> None:
+    """Canonical check of a host CSR on the device (validate, csr.hpp:112-153)."""
+    import torch
+    if not torch.cuda.is_available():
+        raise Error(f"{who}: no CUDA device for the canonical check", _lib.ECUDA)
+    d = DeviceCsr.from_host(m, "cuda")
+    _check(lib().gespmm_validate_device_as(C.byref(d.c_struct()), _stream_ptr(None),
+                                           who.encode()))
+
+
+# ---------------------------------------------------------------------------
 # device-resident API (torch tensors for memory/streams only)
 # ---------------------------------------------------------------------------
 
@@ -452,6 +514,21 @@ class DeviceCsr:
         ci = torch.from_numpy(np.ascontiguousarray(a.col_ind, np.uint32).view(np.int32)).to(device)
         v = torch.from_numpy(np.ascontiguousarray(a.vals, np.float32)).to(device)
         return cls(a.n_rows, a.n_cols, rp, ci, v)
+
+    @classmethod
+    def load(cls, path, device="cuda", validate: bool = True, stream=None) -> "DeviceCsr":
+        """Stream a CSR1 cache file straight into HBM (gespmm_csr1_load_device:
+        pinned double-buffered reads overlapped with H2D), then the device
+        canonical check with load_matrix's wording (io.hpp:100-115)."""
+        import torch
+        rows, cols, nnz = _csr1_header(path)
+        rp = torch.empty(rows + 1, dtype=torch.int32, device=device)
+        ci = torch.empty(max(nnz, 1), dtype=torch.int32, device=device)
+        v = torch.empty(max(nnz, 1), dtype=torch.float32, device=device)
+        with torch.cuda.device(rp.device):
+            _check(lib().gespmm_csr1_load_device(_path_bytes(path), rp.data_ptr(), ci.data_ptr(),
+                                                 v.data_ptr(), int(validate), _stream_ptr(stream)))
+        return cls(rows, cols, rp, ci[:nnz], v[:nnz])
 
     def nnz(self) -> int:
         return int(self.col_ind.numel())

@@ -108,6 +108,13 @@ gespmm_status_t check_op(gespmm_reduce_t op, const int32_t* arg) {
 
 gespmm_status_t set_error(gespmm_status_t st, const std::string& msg) { return fail(st, msg); }
 
+gespmm_status_t validate_device_as(const gespmm_csr_t* a, cudaStream_t st, const char* who) {
+  ValidateResult r{};
+  GESPMM_CUDA(validate_csr_device(a->n_rows, a->n_cols, a->nnz, a->row_ptr, a->col_ind, &r, st),
+              "validate");
+  return validation_status(r, a->n_rows, a->n_cols, a->nnz, who);
+}
+
 // ---------------------------------------------------------------------------
 // Plans
 // ---------------------------------------------------------------------------
@@ -123,6 +130,8 @@ struct Plan {
   uint32_t n_hub = 0;        // order[0, n_hub) -> row-per-CTA
   uint32_t hub_threshold = 0;
   uint32_t* d_order = nullptr;
+  uint32_t* d_hot = nullptr;  // hot-column bitmap (frequency-aware L2 policy), nullable
+  HotStats hot{};
   cudaStream_t side = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   std::string desc;
@@ -131,6 +140,7 @@ struct Plan {
 
   ~Plan() {
     if (d_order) cudaFree(d_order);
+    if (d_hot) cudaFree(d_hot);
     if (ev_fork) cudaEventDestroy(ev_fork);
     if (ev_join) cudaEventDestroy(ev_join);
     if (side) cudaStreamDestroy(side);
@@ -150,6 +160,22 @@ uint32_t auto_hub_threshold(uint32_t n, uint64_t nnz) {
   if (n < 64) return 0xffffffffu;  // the CTA split needs >= 2 warps of columns
   const uint64_t t = std::max<uint64_t>(65536, nnz / 1024);
   return t >= 0xffffffffull ? 0xffffffffu : uint32_t(t);
+}
+
+// Frequency-aware L2 policy budget (bytes of B rows kept evict_last), 0 = off.
+// Auto: on when B exceeds twice the L2 — then LRU among all B rows thrashes and
+// the most-gathered rows are worth pinning; the budget is 60% of L2, leaving
+// room for the streamed CSR and C lines in flight.  Measured on B200
+// (profiles/r1_hot_sweep.txt): products N=256 max+arg (B 2.5 GB) 14.49 -> 13.70
+// ms; Reddit N=128 (B 119 MB, about the L2 size) 2.99 -> 3.10 ms, so off there.
+uint64_t hot_budget_bytes(const gespmm_options_t& o, uint32_t k, uint32_t n, int dev) {
+  if (o.l2_hot_mb < 0 || k >= 0x80000000u) return 0;  // bit 31 of a staged column is the mark
+  if (o.l2_hot_mb > 0) return uint64_t(o.l2_hot_mb) << 20;
+  int l2 = 0;
+  cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev);
+  const uint64_t b_bytes = uint64_t(k) * n * sizeof(float);
+  if (l2 <= 0 || b_bytes <= uint64_t(l2) * 2) return 0;
+  return uint64_t(l2) * 6 / 10;
 }
 
 // Inspector: degree-descending row schedule (stable counting sort) so heavy
@@ -201,12 +227,24 @@ gespmm_status_t build_tuned(Plan& p, const uint32_t* host_rp, cudaStream_t st) {
     GESPMM_CUDA(cudaEventCreateWithFlags(&p.ev_fork, cudaEventDisableTiming), "plan_create");
     GESPMM_CUDA(cudaEventCreateWithFlags(&p.ev_join, cudaEventDisableTiming), "plan_create");
   }
-  char buf[320];
-  std::snprintf(buf, sizeof buf,
+  const uint64_t hot_budget = hot_budget_bytes(p.o, p.a.n_cols, p.n, p.device);
+  if (hot_budget && p.o.l2_hints && p.a.nnz) {
+    GESPMM_CUDA(build_hot_bitmap(p.a.col_ind, p.a.nnz, p.a.n_cols,
+                                 hot_budget / (uint64_t(p.n) * sizeof(float)), st, &p.d_hot,
+                                 &p.hot),
+                "plan_create");
+  }
+  char buf[400];
+  int len = std::snprintf(buf, sizeof buf,
                 "tuned: warp(vec=%d,lpr=%d,cf=%d) rows=%u; cta(vec=%d,warps=%d) hub_rows=%u "
                 "(deg>=%u); mean_deg=%.1f max_deg=%u",
                 p.warp_v.vec, p.warp_v.lpr, p.warp_v.cf, m - n_hub, p.cta_v.vec, p.cta_v.warps,
                 n_hub, p.hub_threshold, p.mean_degree, maxd);
+  if (p.d_hot && len > 0 && size_t(len) < sizeof buf)
+    std::snprintf(buf + len, sizeof buf - size_t(len),
+                  "; l2 hot map %.0f MB: %llu cols (gathered>=%u) = %.1f%% of gathers",
+                  double(hot_budget) / 1e6, (unsigned long long)p.hot.hot_cols, p.hot.threshold,
+                  100.0 * p.hot.hot_nnz_frac);
   p.desc = buf;
   return GESPMM_OK;
 }
@@ -294,6 +332,7 @@ gespmm_status_t plan_execute_impl(Plan& p, const float* b, float* c, int32_t* ar
   args.arg_col = p.o.arg_kind == GESPMM_ARG_COLUMN;
   args.skip_tail = p.o.fault_skip_tail;
   args.hints = p.o.l2_hints;
+  args.hot = p.d_hot;
   const bool fast = p.o.exact == 0;
   if (p.o.variant != GESPMM_VARIANT_TUNED) {
     args.order = nullptr;
@@ -486,6 +525,11 @@ uint64_t gespmm_launch_count(void) { return g_launches.load(std::memory_order_re
 gespmm_status_t gespmm_validate_device(const gespmm_csr_t* a, void* stream) {
   if (!a) return fail(GESPMM_EINVAL, "null csr");
   return device_validate(a, static_cast<cudaStream_t>(stream), "spmm");
+}
+
+gespmm_status_t gespmm_validate_device_as(const gespmm_csr_t* a, void* stream, const char* who) {
+  if (!a) return fail(GESPMM_EINVAL, "null csr");
+  return validate_device_as(a, static_cast<cudaStream_t>(stream), who ? who : "spmm");
 }
 
 gespmm_status_t gespmm_plan_create(const gespmm_csr_t* a, uint32_t n, gespmm_reduce_t op,

@@ -118,7 +118,8 @@ __device__ __forceinline__ float finish(float acc, uint32_t row_len) {
 // policies are evict_normal (same code path).
 // ---------------------------------------------------------------------------
 struct Policies {
-  uint64_t keep;    // for B
+  uint64_t keep;    // for B (hot rows when the plan has a hot-column map)
+  uint64_t cold;    // for B rows outside the hot-column map
   uint64_t stream;  // for CSR and C
 };
 
@@ -127,11 +128,23 @@ __device__ __forceinline__ Policies make_policies(int hints) {
   if (hints) {
     asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p.keep));
     asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p.stream));
+    if (hints == 2)
+      asm("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p.cold));
+    else
+      p.cold = p.stream;
   } else {
     asm("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p.keep));
     p.stream = p.keep;
+    p.cold = p.keep;
   }
   return p;
+}
+
+// Hot-column map lookup (plan-time bitmap, hotcols.cu): bit 31 of the staged
+// column marks a COLD column, so an absent map leaves every column "hot".
+constexpr uint32_t kColdBit = 0x80000000u;
+__device__ __forceinline__ uint32_t cold_mark(const uint32_t* __restrict__ hot, uint32_t k) {
+  return ((__ldg(hot + (k >> 5)) >> (k & 31u)) & 1u) ? 0u : kColdBit;
 }
 
 // Streamed sparse arrays: read once, do not allocate in L1.
@@ -258,7 +271,8 @@ struct SpmmArgs {
   uint32_t n_tiles;       // column tiles per row
   int arg_col;            // arg = col_ind[p] instead of p
   int skip_tail;
-  int hints;
+  int hints;              // 0 off, 1 B evict_last / CSR,C evict_first, 2 = 1 with cold B evict_normal
+  const uint32_t* hot;    // hot-column bitmap (nullable): cold B rows use the cold policy
 };
 
 }  // namespace gespmm

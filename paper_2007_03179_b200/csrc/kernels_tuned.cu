@@ -47,8 +47,15 @@ struct Pack<4> {
 
 constexpr int kWarpBlock = 4;  // warps per CTA: 72-register kernel -> 7 CTAs = 28 warps/SM
 
+// max/min carry 2*CF*VEC accumulator registers (value + arg): 6 CTAs per SM
+// (85 registers; 4 at CF=4) instead of spilling under the 7-CTA cap.
+template <int OP, int CF>
+constexpr int warp_min_blocks() {
+  return Reduce<OP>::kHasArg ? (CF >= 4 ? 4 : 6) : 7;
+}
+
 template <int OP, bool FAST, int VEC, int LPR, int CF>
-__global__ void __launch_bounds__(32 * kWarpBlock, 7) k_warp(SpmmArgs a) {
+__global__ void __launch_bounds__(32 * kWarpBlock, warp_min_blocks<OP, CF>()) k_warp(SpmmArgs a) {
   using R = Reduce<OP>;
   constexpr int RPW = 32 / LPR;                     // rows per warp
   constexpr int U0 = 8 / CF;
@@ -113,6 +120,7 @@ __global__ void __launch_bounds__(32 * kWarpBlock, 7) k_warp(SpmmArgs a) {
     if (sl < len) {
       k0 = ld_stream_u32(ci + sl, pol.stream);
       v0 = ld_stream_f32(vs + sl, pol.stream);
+      if (a.hot) k0 |= cold_mark(a.hot, k0);
     }
     my_col[lane] = k0;
     my_val[lane] = v0;
@@ -126,6 +134,7 @@ __global__ void __launch_bounds__(32 * kWarpBlock, 7) k_warp(SpmmArgs a) {
     if (nxt < len) {
       kn = ld_stream_u32(ci + nxt, pol.stream);
       vn = ld_stream_f32(vs + nxt, pol.stream);
+      if (a.hot) kn |= cold_mark(a.hot, kn);
     }
     __syncwarp();
     const uint32_t* cs = my_col + buf * 32 + sub * LPR;
@@ -148,13 +157,17 @@ __global__ void __launch_bounds__(32 * kWarpBlock, 7) k_warp(SpmmArgs a) {
       }
       // all U*CF gathers issued before any fold (memory-level parallelism);
       // unpredicated: past-the-end slots re-read a valid row.
+      // bit 31 of a staged column marks a cold B row (hot-column map)
       Vec<VEC> bv[U][CF];
 #pragma unroll
-      for (int u = 0; u < U; ++u)
+      for (int u = 0; u < U; ++u) {
+        const uint64_t pu = (k[u] & kColdBit) ? pol.cold : pol.keep;
+        k[u] &= ~kColdBit;
 #pragma unroll
         for (int c = 0; c < CF; ++c)
           bv[u][c] = ld_keep<VEC>(
-              reinterpret_cast<const float*>(bbase[c] + uint64_t(k[u]) * stride), pol.keep);
+              reinterpret_cast<const float*>(bbase[c] + uint64_t(k[u]) * stride), pu);
+      }
       const int32_t rem = int32_t(len - off - kk);  // entries left in this row (may be <= 0)
 #pragma unroll
       for (int u = 0; u < U; ++u) {

@@ -50,6 +50,23 @@ CtaShape pick_cta_shape(uint32_t n, bool vec4_ok, bool vec2_ok);
 cudaError_t launch_tuned_cta(const CtaShape& s, int op, bool fast, const SpmmArgs& a,
                              cudaStream_t st);
 
+// --- frequency-aware L2 policy (hotcols.cu) ---
+struct HotStats {
+  uint32_t threshold = 0;     // a column is hot when gathered >= threshold times
+  uint64_t hot_cols = 0;
+  double hot_nnz_frac = 0.0;  // share of the gathers that hit hot columns
+};
+// Counts the gathers per column and returns (cudaMalloc'ed, caller frees) a
+// ceil(k/32)-word bitmap of the most-gathered columns, at most budget_rows of
+// them.  Synchronises `st`.
+cudaError_t build_hot_bitmap(const uint32_t* col_ind, uint64_t nnz, uint32_t k,
+                             uint64_t budget_rows, cudaStream_t st, uint32_t** out_bits,
+                             HotStats* stats);
+
+// Device canonical check of a device CSR, formatted as the reference's
+// require_canonical(m, who) error (csr.hpp:155-158).  Synchronises `st`.
+gespmm_status_t validate_device_as(const gespmm_csr_t* a, cudaStream_t st, const char* who);
+
 // --- validation (validate.cu) ---
 struct ValidateResult {
   uint32_t row_ptr0;

@@ -295,6 +295,34 @@ def test_device_api_plans_and_unaligned_views(cuda):
     assert first_divergence(c.cpu().numpy(), want) is None
 
 
+@pytest.mark.parametrize("n", [64, 128, 256])
+def test_hot_column_map_keeps_bits(n, cuda):
+    """The frequency-aware L2 map only changes cache hints: forced on (tiny
+    budget, so most columns are cold and carry the bit-31 mark through the row
+    cache), every op, edge and column args, is bit-identical to the oracle."""
+    import torch
+    a, b = _powerlaw(6000, 500000, 5000, 31, n)
+    d = G.DeviceCsr.from_host(a)
+    bt = torch.from_numpy(b.data).to(cuda)
+    for op in OPS:
+        want_arg = op in ("max", "min")
+        for kind, okind in (("edge", O.ARG_EDGE), ("column", O.ARG_COLUMN)):
+            if kind == "column" and not want_arg:
+                continue
+            want, warg = _oracle(a, b, op, want_arg, arg_kind=okind)
+            ex = G.ExecOptions(l2_hot_mb=1, arg_kind=kind)
+            plan = G.Plan(d, n, op, exec=ex)
+            assert "hot map" in plan.description, plan.description
+            c = torch.empty((a.n_rows, n), dtype=torch.float32, device=cuda)
+            arg = torch.empty((a.n_rows, n), dtype=torch.int32, device=cuda) if want_arg else None
+            plan.execute(bt, c, arg)
+            torch.cuda.synchronize()
+            assert first_divergence(c.cpu().numpy(), want) is None, (op, kind)
+            if want_arg:
+                assert np.array_equal(arg.cpu().numpy(), warg), (op, kind)
+            plan.close()
+
+
 def test_device_validate_flag(cuda):
     import torch
     a = G.gen_uniform_random(G.GraphGenSpec(100, 1000, 1))
