@@ -332,7 +332,8 @@ def run_ours(args, cfg):
     arg = torch.empty((shard.n_rows, n), dtype=torch.int32, device=dev) if want_arg else None
     hints = 0 if args.no_hints else args.hints
     ex = G.ExecOptions(hub_threshold=args.hub_threshold, exact=not args.fast,
-                       l2_persist=args.l2_persist, l2_hints=hints, l2_hot_mb=args.l2_hot_mb)
+                       l2_persist=args.l2_persist, l2_hints=hints, l2_hot_mb=args.l2_hot_mb,
+                       tuned_cf=args.tuned_cf)
     variant = G.variant_by_name(args.variant, args.cf)
     plan = G.Plan(d, n, op, variant=variant, exec=ex)
     log(f"[bench] rank {rank}: rows [{info.lo},{info.hi}) nnz {shard.nnz()} plan: {plan.description}")
@@ -406,7 +407,7 @@ def run_ours(args, cfg):
         o = _lib.default_options(variant=int(variant.kind), cf=args.cf,
                                  hub_threshold=args.hub_threshold, exact=int(not args.fast),
                                  l2_persist=int(args.l2_persist), l2_hints=hints,
-                                 l2_hot_mb=args.l2_hot_mb)
+                                 l2_hot_mb=args.l2_hot_mb, tuned_cf=args.tuned_cf)
         L = _lib.lib()
 
         def host_call():
@@ -567,6 +568,7 @@ def main():
     p.add_argument("--no-hints", action="store_true", help="evict_normal instead of L2 hints")
     p.add_argument("--hints", type=int, default=1,
                    help="L2 hint mode (1: cold B rows evict_first, 2: evict_normal)")
+    p.add_argument("--tuned-cf", type=int, default=0, help="tuned warp kernel merge factor")
     p.add_argument("--l2-hot-mb", type=int, default=0,
                    help="hot-column map budget in MB (0 auto, <0 off)")
     p.add_argument("--no-flush", action="store_true", help="skip the L2 flush between steps")

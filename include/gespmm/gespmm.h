@@ -94,7 +94,9 @@ typedef struct {
                          fit this many MB are loaded evict_last (the rest evict_first).
                          0 = auto (on when B exceeds twice the L2), <0 = off.  Hints only:
                          results are unaffected. */
-  int32_t reserved[6];
+  int32_t tuned_cf;   /* TUNED plans: CWM merge factor (column sub-tiles per lane) of the
+                         full-warp row kernel, 1, 2 or 4; 0 = auto from N */
+  int32_t reserved[5];
 } gespmm_options_t;
 
 void gespmm_options_default(gespmm_options_t* opts);

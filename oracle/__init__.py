@@ -101,6 +101,9 @@ def _load_ref():
         lib.ref_from_coo.restype = C.c_longlong
         lib.ref_from_coo.argtypes = [cu, cu, cull, _u32p, _u32p, _f32p, _u32p, _u32p, _f32p,
                                      cp, cu]
+        lib.ref_sim_metrics.restype = C.c_int
+        lib.ref_sim_metrics.argtypes = [cu, cu, cull, _u32p, _u32p, _f32p, _f32p, cu, cp,
+                                        C.c_int, cu, C.POINTER(cull), cp, cu]
         lib.ref_save_csr_cache.restype = C.c_int
         lib.ref_save_csr_cache.argtypes = [cp, cu, cu, cull, _u32p, _u32p, _f32p, cp, cu]
         lib.ref_load_matrix.restype = C.c_int
@@ -318,3 +321,23 @@ def ref_load_matrix(path):
                            rp.ctypes.data, ci.ctypes.data, v.ctypes.data, e, 1024):
         raise RefError(e.value.decode())
     return m.value, k.value, rp, ci[: z.value].copy(), v[: z.value].copy()
+
+
+SIM_FIELDS = ("gld_transactions", "gst_transactions", "requested_load_bytes",
+              "transferred_load_bytes", "requested_store_bytes", "transferred_store_bytes",
+              "ld_row_ptr", "ld_col_ind", "ld_val", "ld_b", "ld_c", "shared_loads",
+              "shared_stores")
+
+
+def ref_sim_metrics(m, k, row_ptr, col_ind, vals, b, op="sum", variant="crc", cf=2):
+    """The reference SIMT simulator's counters (simt.hpp:117-162) for one run."""
+    kind = {"naive": 0, "crc": 1, "crc-cwm": 2}[variant]
+    b = np.ascontiguousarray(b, np.float32)
+    out = (C.c_ulonglong * 13)()
+    e = _err()
+    if _load_ref().ref_sim_metrics(m, k, len(col_ind), _nz(row_ptr, np.uint32),
+                                   _nz(col_ind, np.uint32), _nz(vals, np.float32),
+                                   _nz(b.reshape(-1), np.float32), b.shape[1], op.encode(), kind,
+                                   cf, out, e, 1024):
+        raise RefError(e.value.decode())
+    return dict(zip(SIM_FIELDS, (int(x) for x in out)))

@@ -18,6 +18,7 @@
 //   spmm::validate           include/spmm/csr.hpp:112-153
 //   spmm::select_variant     include/spmm/kernel.hpp:96-98
 //   spmm::from_coo           include/spmm/csr.hpp:58-93
+//   spmm::run_kernel         include/spmm/simt.hpp:382-432 (SIMT simulator metrics)
 //   spmm::save_csr_cache     include/spmm/io.hpp:92-96
 //   spmm::load_matrix        include/spmm/io.hpp:100-115
 #include "spmm/spmm.hpp"
@@ -219,6 +220,40 @@ long long ref_from_coo(unsigned rows, unsigned cols, unsigned long long count, c
   } catch (const std::exception& e) {
     put_err(err, err_len, e.what());
     return -1;
+  }
+}
+
+// The reference's SIMT simulator (32-byte segment coalescer): out[0..5] =
+// gld_transactions, gst_transactions, requested_load_bytes,
+// transferred_load_bytes, requested_store_bytes, transferred_store_bytes;
+// out[6..10] = load transactions per array (RowPtr, ColInd, Val, B, C);
+// out[11..12] = shared loads / stores.
+int ref_sim_metrics(unsigned m, unsigned k, unsigned long long nnz, const unsigned* row_ptr,
+                    const unsigned* col_ind, const float* vals, const float* b, unsigned n,
+                    const char* op_name, int kind, unsigned cf, unsigned long long* out,
+                    char* err, unsigned err_len) {
+  try {
+    const CsrMatrix a = make_csr(m, k, nnz, row_ptr, col_ind, vals);
+    const DenseMatrix bd = make_dense(k, n, b);
+    KernelConfig cfg;
+    cfg.variant = variant_of(kind, cf);
+    SimOptions so;
+    so.parallel = true;
+    const SimResult r = run_kernel(a, bd, cfg, reduce_op_by_name(op_name), so);
+    const SimMetrics& s = r.metrics;
+    out[0] = s.gld_transactions;
+    out[1] = s.gst_transactions;
+    out[2] = s.requested_load_bytes;
+    out[3] = s.transferred_load_bytes;
+    out[4] = s.requested_store_bytes;
+    out[5] = s.transferred_store_bytes;
+    for (int i = 0; i < kArrayCount; ++i) out[6 + i] = s.load_by_array[i].transactions;
+    out[11] = s.shared_loads;
+    out[12] = s.shared_stores;
+    return 0;
+  } catch (const std::exception& e) {
+    put_err(err, err_len, e.what());
+    return 1;
   }
 }
 

@@ -49,7 +49,8 @@ class Options(C.Structure):
                 ("arg_kind", C.c_int32), ("validate", C.c_int32),
                 ("fault_skip_tail", C.c_int32), ("l2_hints", C.c_int32),
                 ("hub_threshold", C.c_int32), ("l2_persist", C.c_int32),
-                ("l2_hot_mb", C.c_int32), ("reserved", C.c_int32 * 6)]
+                ("l2_hot_mb", C.c_int32), ("tuned_cf", C.c_int32),
+                ("reserved", C.c_int32 * 5)]
 
 
 _lock = threading.Lock()

@@ -295,6 +295,7 @@ class ExecOptions:
     hub_threshold: int = 0          # 0 auto, <0 off
     l2_persist: bool = False        # L2 access-policy window marking B persisting
     l2_hot_mb: int = 0              # hot-column map budget in MB: 0 auto, <0 off
+    tuned_cf: int = 0               # tuned warp kernel merge factor (1/2/4), 0 auto
 
 
 def _options(variant: KernelVariant, ex: ExecOptions, validate: bool = True) -> _lib.Options:
@@ -303,7 +304,8 @@ def _options(variant: KernelVariant, ex: ExecOptions, validate: bool = True) -> 
                            arg_kind=_lib.ARG_COLUMN if ex.arg_kind == "column" else _lib.ARG_EDGE,
                            validate=int(validate), fault_skip_tail=int(ex.fault == FaultMode.SkipTail),
                            l2_hints=int(ex.l2_hints), hub_threshold=ex.hub_threshold,
-                           l2_persist=int(ex.l2_persist), l2_hot_mb=int(ex.l2_hot_mb))
+                           l2_persist=int(ex.l2_persist), l2_hot_mb=int(ex.l2_hot_mb),
+                           tuned_cf=int(ex.tuned_cf))
 
 
 # ---------------------------------------------------------------------------

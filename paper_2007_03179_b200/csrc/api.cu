@@ -90,6 +90,8 @@ gespmm_status_t check_opts(const gespmm_options_t& o) {
                                    " (naive, crc, crc-cwm, tuned)");
   if (o.variant == GESPMM_VARIANT_CRC_CWM && o.cf != 2 && o.cf != 4 && o.cf != 8)
     return fail(GESPMM_EINVAL, "coarsening factor must be 2, 4 or 8");
+  if (o.tuned_cf != 0 && o.tuned_cf != 1 && o.tuned_cf != 2 && o.tuned_cf != 4)
+    return fail(GESPMM_EINVAL, "tuned_cf must be 0 (auto), 1, 2 or 4");
   if (o.arg_kind != GESPMM_ARG_EDGE && o.arg_kind != GESPMM_ARG_COLUMN)
     return fail(GESPMM_EINVAL, "arg_kind must be edge (0) or column (1)");
   return GESPMM_OK;
@@ -211,6 +213,13 @@ gespmm_status_t build_tuned(Plan& p, const uint32_t* host_rp, cudaStream_t st) {
   const bool n4 = p.n % 4 == 0, n2 = p.n % 2 == 0;
   p.warp_v = pick_warp_shape(p.n, n4, !n4 && n2);
   p.warp_s = pick_warp_shape(p.n, false, false);
+  if (p.o.tuned_cf > 0) {  // explicit CWM merge factor for the warp kernel (tuning)
+    for (WarpShape* w : {&p.warp_v, &p.warp_s}) {
+      WarpShape t = *w;
+      t.cf = p.o.tuned_cf;
+      if (t.lpr == 32 && tuned_shape_supported(t)) *w = t;
+    }
+  }
   p.cta_v = pick_cta_shape(p.n, n4, n2);
   p.cta_s = pick_cta_shape(p.n, false, false);
 

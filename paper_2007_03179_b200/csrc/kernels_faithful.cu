@@ -34,19 +34,28 @@ __global__ void __launch_bounds__(256) k_naive(SpmmArgs a) {
   int32_t who = -1;
   // Batches of kBatch nonzeros: the B loads of a batch are issued before any
   // fold (the same memory-level parallelism every variant gets, so the
-  // ablation compares the algorithms, not the compiler's scheduling).
-  const float* bcol = a.b + (active ? col : 0u);
+  // ablation compares the algorithms, not the compiler's scheduling).  Every
+  // load is predicated exactly like the reference's masks (past-the-end slots
+  // and columns >= N issue nothing), so the kernel's L1 sector counts equal
+  // the reference simulator's transaction counts (tools/sector_parity.py).
+  const float* bcol = a.b + col;
   for (uint32_t p = start; p < end; p += kBatch) {
     uint32_t k[kBatch];
     float v[kBatch], bv[kBatch];
 #pragma unroll
     for (int u = 0; u < kBatch; ++u) {
-      const uint32_t q = min(p + u, end - 1);  // past-the-end slots re-read the last entry
-      k[u] = __ldg(a.col_ind + q);             // warp-uniform (broadcast) loads
-      v[u] = __ldg(a.vals + q);
+      k[u] = 0u;
+      v[u] = 0.0f;
+      if (p + u < end) {
+        k[u] = __ldg(a.col_ind + p + u);  // warp-uniform (broadcast) loads
+        v[u] = __ldg(a.vals + p + u);
+      }
     }
 #pragma unroll
-    for (int u = 0; u < kBatch; ++u) bv[u] = ld_keep<1>(bcol + uint64_t(k[u]) * a.n, pol.keep).x[0];
+    for (int u = 0; u < kBatch; ++u) {
+      bv[u] = 0.0f;
+      if (active && p + u < end) bv[u] = ld_keep<1>(bcol + uint64_t(k[u]) * a.n, pol.keep).x[0];
+    }
 #pragma unroll
     for (int u = 0; u < kBatch; ++u)
       if (active && p + u < end)
@@ -104,7 +113,8 @@ __global__ void __launch_bounds__(256) k_crc(SpmmArgs a) {
 #pragma unroll
         for (int c = 0; c < CF; ++c) {
           const uint32_t col = col_base + c * 32u + lane;
-          bv[u][c] = ld_keep<1>(brow + (col < a.n ? col : 0u), pol.keep).x[0];
+          bv[u][c] = 0.0f;
+          if (kk + u < tile_n && col < a.n) bv[u][c] = ld_keep<1>(brow + col, pol.keep).x[0];
         }
       }
 #pragma unroll

@@ -1,0 +1,41 @@
+"""Observability parity: the reference's SIMT simulator
+counts 32-byte transactions per warp access (simt.hpp:60-104); B200's L1
+counts 32-byte sectors per request.  For the paper's Algorithms 1-3
+(kernels_faithful.cu) the two must agree exactly on the same inputs — measured
+here with ncu on small cases (full table: profiles/r1_sector_parity.md)."""
+import os
+import shutil
+import subprocess
+import sys
+
+import pytest
+
+import oracle as O
+from conftest import ROOT
+
+pytestmark = pytest.mark.gpu
+
+sys.path.insert(0, os.path.join(ROOT, "tools"))
+
+
+@pytest.mark.skipif(not O.ref_available(), reason="oracle/_ref not built")
+def test_l1_sectors_equal_reference_simulator_transactions(tmp_path, cuda):
+    import sector_parity as S
+    ncu = shutil.which("ncu") or "/usr/local/cuda/bin/ncu"
+    if not os.path.exists(ncu):
+        pytest.skip("ncu not available")
+    out = tmp_path / "sectors.csv"
+    env = dict(os.environ, GESPMM_SECTOR_CASES="small")
+    r = subprocess.run([ncu, "--metrics", S.METRICS, "--clock-control", "none",
+                        "-k", "regex:k_naive|k_crc", "--csv", "--log-file", str(out),
+                        sys.executable, os.path.join(ROOT, "tools", "sector_parity.py"), "run"],
+                       env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    os.environ["GESPMM_SECTOR_CASES"] = "small"
+    try:
+        table = S.report(str(out), str(tmp_path / "parity"))
+    finally:
+        del os.environ["GESPMM_SECTOR_CASES"]
+    assert len(table) == len(S.cases()) * len(S.VARIANTS)
+    for row in table:
+        assert row["ld_match"] and row["st_match"], row
