@@ -242,6 +242,23 @@ def dist_env():
     return world, rank, local
 
 
+def init_dist(world, local):
+    """One process per GPU: pick the device, and for world > 1 join the NCCL
+    group.  GESPMM_DIST_BACKEND=gloo (with ranks sharing a device, local %
+    device_count) exercises the multi-rank path on a single-GPU box."""
+    import torch
+    dev = torch.device("cuda", local % max(1, torch.cuda.device_count()))
+    torch.cuda.set_device(dev)
+    if world > 1:
+        import torch.distributed as dist
+        backend = os.environ.get("GESPMM_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
+    return dev
+
+
 def run_reference(args, cfg):
     world, rank, _ = dist_env()
     if rank != 0:
@@ -304,11 +321,7 @@ def run_ours(args, cfg):
     world, rank, local = dist_env()
     if not torch.cuda.is_available():
         raise SystemExit("bench.py: no CUDA device")
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    if world > 1:
-        import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
+    dev = init_dist(world, local)
 
     a = make_inputs(cfg)
     n, op, want_arg = cfg["n"], cfg["op"], bool(cfg.get("arg"))
@@ -498,11 +511,7 @@ def run_gcn(args):
     import paper_2007_03179_b200 as G
 
     world, rank, local = dist_env()
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    if world > 1:
-        import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
+    dev = init_dist(world, local)
     cfg = CONFIGS["reddit"]
     a = gcn.normalize_adjacency(make_inputs(cfg))  # D^-1/2 (A + I) D^-1/2
     gcfg = gcn.GCNConfig(in_features=602, hidden=256, classes=41)

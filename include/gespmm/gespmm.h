@@ -235,6 +235,13 @@ gespmm_status_t gespmm_diag_gather(const uint32_t* idx, uint64_t count, const fl
 /* Kernel launches issued by this library since load (all entry points). */
 uint64_t gespmm_launch_count(void);
 
+/* Diagnostics: as gespmm_diag_gather (n = 128) but rows idx < hub_rows (<= 400)
+ * come from a shared-memory copy of B's first rows (persistent 1024-thread
+ * CTAs, sink = blocks*1024 floats). */
+gespmm_status_t gespmm_diag_gather_hub(const uint32_t* idx, uint64_t count, const float* b,
+                                       uint32_t hub_rows, float* sink, int32_t blocks,
+                                       void* stream);
+
 #ifdef __cplusplus
 }  /* extern "C" */
 #endif

@@ -36,6 +36,7 @@ EXPORTS = [
     "gespmm_device_info", "gespmm_launch_count", "gespmm_diag_gather",
     "gespmm_csr_transpose_device", "gespmm_validate_device_as", "gespmm_csr1_write",
     "gespmm_csr1_header", "gespmm_csr1_read_host", "gespmm_csr1_load_device",
+    "gespmm_diag_gather_hub",
 ]
 
 
@@ -129,6 +130,8 @@ def lib():
         L.gespmm_device_info.restype = C.c_int
         L.gespmm_diag_gather.argtypes = [vp, u64, vp, u32, vp, i32, i32, vp]
         L.gespmm_diag_gather.restype = C.c_int
+        L.gespmm_diag_gather_hub.argtypes = [vp, u64, vp, u32, vp, i32, vp]
+        L.gespmm_diag_gather_hub.restype = C.c_int
         L.gespmm_csr_transpose_device.argtypes = [C.POINTER(Csr), vp, vp, vp, vp]
         L.gespmm_csr_transpose_device.restype = C.c_int
         L.gespmm_csr1_write.argtypes = [C.c_char_p, C.POINTER(Csr)]

@@ -85,3 +85,42 @@ def test_two_rank_gloo_spmm_equals_single_process(tmp_path, op):
         got = np.load(tmp_path / f"rank{r}.npy")
         assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
         assert np.array_equal(np.load(tmp_path / f"b{r}.npy"), b.data)  # broadcast reached rank 1
+
+
+def _cuda_worker(rank, world, port, op, result_dir):
+    """Two ranks sharing cuda:0 over gloo: the library's CUDA kernels as the
+    per-shard compute, B broadcast and C all-gathered as CUDA tensors."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(dev)
+    a = G.gen_powerlaw(6000, 300000, 3000, 1.0, 21)
+    G.randomize_values(a, 22)
+    if rank == 0:
+        b = torch.from_numpy(G.make_random_dense(6000, 128, 23).data.copy()).to(dev)
+    else:
+        b = torch.zeros(6000, 128, device=dev)
+
+    def compute(shard, bt):
+        c, arg = G.spmm(G.DeviceCsr.from_host(shard, dev), bt, op, want_arg=op == "max")
+        torch.cuda.synchronize()
+        return c
+
+    full, info = D.distributed_spmm(a, b, rank, world, compute)
+    np.save(os.path.join(result_dir, f"cuda_rank{rank}.npy"), full.cpu().numpy())
+    dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("op", ["sum", "max"])
+def test_two_rank_cuda_shards_equal_oracle(tmp_path, op):
+    world = 2
+    mp.spawn(_cuda_worker, args=(world, _free_port(), op, str(tmp_path)), nprocs=world,
+             join=True)
+    a = G.gen_powerlaw(6000, 300000, 3000, 1.0, 21)
+    G.randomize_values(a, 22)
+    b = G.make_random_dense(6000, 128, 23)
+    want, _ = O.spmm(a.n_rows, a.n_cols, a.row_ptr, a.col_ind, a.vals, b.data, op)
+    for r in range(world):
+        got = np.load(tmp_path / f"cuda_rank{r}.npy")
+        assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
