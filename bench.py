@@ -346,7 +346,7 @@ def run_ours(args, cfg):
     hints = 0 if args.no_hints else args.hints
     ex = G.ExecOptions(hub_threshold=args.hub_threshold, exact=not args.fast,
                        l2_persist=args.l2_persist, l2_hints=hints, l2_hot_mb=args.l2_hot_mb,
-                       tuned_cf=args.tuned_cf)
+                       tuned_cf=args.tuned_cf, col_slices=args.col_slices)
     variant = G.variant_by_name(args.variant, args.cf)
     plan = G.Plan(d, n, op, variant=variant, exec=ex)
     log(f"[bench] rank {rank}: rows [{info.lo},{info.hi}) nnz {shard.nnz()} plan: {plan.description}")
@@ -420,7 +420,8 @@ def run_ours(args, cfg):
         o = _lib.default_options(variant=int(variant.kind), cf=args.cf,
                                  hub_threshold=args.hub_threshold, exact=int(not args.fast),
                                  l2_persist=int(args.l2_persist), l2_hints=hints,
-                                 l2_hot_mb=args.l2_hot_mb, tuned_cf=args.tuned_cf)
+                                 l2_hot_mb=args.l2_hot_mb, tuned_cf=args.tuned_cf,
+                                 col_slices=args.col_slices)
         L = _lib.lib()
 
         def host_call():
@@ -577,6 +578,8 @@ def main():
     p.add_argument("--no-hints", action="store_true", help="evict_normal instead of L2 hints")
     p.add_argument("--hints", type=int, default=1,
                    help="L2 hint mode (1: cold B rows evict_first, 2: evict_normal)")
+    p.add_argument("--col-slices", type=int, default=0,
+                   help="slice-major column traversal: 0 auto, 1 off, S slices")
     p.add_argument("--tuned-cf", type=int, default=0, help="tuned warp kernel merge factor")
     p.add_argument("--l2-hot-mb", type=int, default=0,
                    help="hot-column map budget in MB (0 auto, <0 off)")

@@ -96,7 +96,13 @@ typedef struct {
                          results are unaffected. */
   int32_t tuned_cf;   /* TUNED plans: CWM merge factor (column sub-tiles per lane) of the
                          full-warp row kernel, 1, 2 or 4; 0 = auto from N */
-  int32_t reserved[5];
+  int32_t col_slices; /* TUNED plans: traverse the N columns as S slices, slice-major (every
+                         row of slice 0, then slice 1, ...), so the live B working set is
+                         B/S and stays in L2 when B does not.  Each output element is still
+                         folded by one thread in CSR order: results are unchanged.
+                         0 = auto (currently off: measured slower on B200), 1 = off,
+                         S >= 2 explicit */
+  int32_t reserved[4];
 } gespmm_options_t;
 
 void gespmm_options_default(gespmm_options_t* opts);
@@ -241,6 +247,12 @@ uint64_t gespmm_launch_count(void);
 gespmm_status_t gespmm_diag_gather_hub(const uint32_t* idx, uint64_t count, const float* b,
                                        uint32_t hub_rows, float* sink, int32_t blocks,
                                        void* stream);
+/* Diagnostic: the gather ceiling under different B-row load paths (N = 128):
+ * 0 LDG.128 L1-allocating, 1 LDG.128 L1::no_allocate, 2 cp.async.cg 16 B per
+ * lane into shared memory, 3 cp.async.bulk 512-B rows into shared memory
+ * (mbarrier complete_tx).  sink: blocks*256 floats. */
+gespmm_status_t gespmm_diag_gather_mode(const uint32_t* idx, uint64_t count, const float* b,
+                                        float* sink, int32_t blocks, int32_t mode, void* stream);
 
 #ifdef __cplusplus
 }  /* extern "C" */

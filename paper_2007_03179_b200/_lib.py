@@ -36,7 +36,7 @@ EXPORTS = [
     "gespmm_device_info", "gespmm_launch_count", "gespmm_diag_gather",
     "gespmm_csr_transpose_device", "gespmm_validate_device_as", "gespmm_csr1_write",
     "gespmm_csr1_header", "gespmm_csr1_read_host", "gespmm_csr1_load_device",
-    "gespmm_diag_gather_hub",
+    "gespmm_diag_gather_hub", "gespmm_diag_gather_mode",
 ]
 
 
@@ -51,7 +51,7 @@ class Options(C.Structure):
                 ("fault_skip_tail", C.c_int32), ("l2_hints", C.c_int32),
                 ("hub_threshold", C.c_int32), ("l2_persist", C.c_int32),
                 ("l2_hot_mb", C.c_int32), ("tuned_cf", C.c_int32),
-                ("reserved", C.c_int32 * 5)]
+                ("col_slices", C.c_int32), ("reserved", C.c_int32 * 4)]
 
 
 _lock = threading.Lock()
@@ -132,6 +132,8 @@ def lib():
         L.gespmm_diag_gather.restype = C.c_int
         L.gespmm_diag_gather_hub.argtypes = [vp, u64, vp, u32, vp, i32, vp]
         L.gespmm_diag_gather_hub.restype = C.c_int
+        L.gespmm_diag_gather_mode.argtypes = [vp, u64, vp, vp, i32, i32, vp]
+        L.gespmm_diag_gather_mode.restype = C.c_int
         L.gespmm_csr_transpose_device.argtypes = [C.POINTER(Csr), vp, vp, vp, vp]
         L.gespmm_csr_transpose_device.restype = C.c_int
         L.gespmm_csr1_write.argtypes = [C.c_char_p, C.POINTER(Csr)]

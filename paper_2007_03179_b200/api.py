@@ -296,6 +296,7 @@ class ExecOptions:
     l2_persist: bool = False        # L2 access-policy window marking B persisting
     l2_hot_mb: int = 0              # hot-column map budget in MB: 0 auto, <0 off
     tuned_cf: int = 0               # tuned warp kernel merge factor (1/2/4), 0 auto
+    col_slices: int = 0             # slice-major column traversal: 0 auto, 1 off, S slices
 
 
 def _options(variant: KernelVariant, ex: ExecOptions, validate: bool = True) -> _lib.Options:
@@ -305,7 +306,7 @@ def _options(variant: KernelVariant, ex: ExecOptions, validate: bool = True) -> 
                            validate=int(validate), fault_skip_tail=int(ex.fault == FaultMode.SkipTail),
                            l2_hints=int(ex.l2_hints), hub_threshold=ex.hub_threshold,
                            l2_persist=int(ex.l2_persist), l2_hot_mb=int(ex.l2_hot_mb),
-                           tuned_cf=int(ex.tuned_cf))
+                           tuned_cf=int(ex.tuned_cf), col_slices=int(ex.col_slices))
 
 
 # ---------------------------------------------------------------------------

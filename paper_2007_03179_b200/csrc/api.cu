@@ -120,6 +120,17 @@ gespmm_status_t validate_device_as(const gespmm_csr_t* a, cudaStream_t st, const
 // ---------------------------------------------------------------------------
 // Plans
 // ---------------------------------------------------------------------------
+
+// Tuned-kernel shapes for one (n, options): the column slicing and, per slice
+// width, the vectorised shapes with their scalar-lane fallbacks.
+struct TunedShapes {
+  uint32_t n = 0;
+  uint32_t slices = 1;   // column slices, traversed slice-major
+  uint32_t slice_w = 0;  // columns per slice (the last one may be narrower)
+  WarpShape warp_v, warp_s;
+  CtaShape cta_v, cta_s;
+};
+
 struct Plan {
   gespmm_csr_t a{};
   uint32_t n = 0;
@@ -127,8 +138,7 @@ struct Plan {
   gespmm_options_t o{};
   int device = 0;
   // tuned
-  WarpShape warp_v, warp_s;  // vectorised shape and scalar-lane fallback
-  CtaShape cta_v, cta_s;
+  TunedShapes sh;            // kernel shapes + column slicing
   uint32_t n_hub = 0;        // order[0, n_hub) -> row-per-CTA
   uint32_t hub_threshold = 0;
   uint32_t* d_order = nullptr;
@@ -180,11 +190,100 @@ uint64_t hot_budget_bytes(const gespmm_options_t& o, uint32_t k, uint32_t n, int
   return uint64_t(l2) * 6 / 10;
 }
 
+// Column slices (slice-major traversal).  The kernels fold each output
+// element in one thread in CSR order whatever the slice, so slicing only
+// changes which columns of B are live at a time: B/S instead of B.  Measured
+// on B200 (profiles/r1_col_slices.txt) it never pays: products N=256 max+arg
+// 13.5 ms at S=1 -> 15.9 / 18.2 / 30.0 ms at S=2/4/8 (the CSR stream and the
+// per-row work repeat per slice and narrower gathers cost more per byte than
+// the extra L2 hits save); Reddit N=128 3.0 -> 4.1 ms at S=2.  Auto = off;
+// explicit S stays available.
+uint32_t pick_slices(const gespmm_options_t& o, uint32_t /*k*/, uint32_t n, int /*dev*/) {
+  if (o.col_slices >= 1) return std::max<uint32_t>(1, std::min<uint32_t>(uint32_t(o.col_slices), n));
+  return 1;
+}
+
+TunedShapes make_shapes(const gespmm_options_t& o, uint32_t k, uint32_t n, int dev) {
+  TunedShapes t;
+  t.n = n;
+  t.slices = pick_slices(o, k, n, dev);
+  uint32_t w = (n + t.slices - 1) / t.slices;
+  if (n % 4 == 0) w = (w + 3) & ~3u;  // slice offsets keep float4 alignment
+  t.slice_w = std::max<uint32_t>(1, std::min(w, n));
+  t.slices = (n + t.slice_w - 1) / t.slice_w;
+  const uint32_t sw = t.slice_w;
+  const bool n4 = n % 4 == 0, n2 = n % 2 == 0;
+  t.warp_v = pick_warp_shape(sw, n4, !n4 && n2);
+  t.warp_s = pick_warp_shape(sw, false, false);
+  if (o.tuned_cf > 0) {  // explicit CWM merge factor for the warp kernel (tuning)
+    for (WarpShape* ws : {&t.warp_v, &t.warp_s}) {
+      WarpShape u = *ws;
+      u.cf = o.tuned_cf;
+      if (u.lpr == 32 && tuned_shape_supported(u)) *ws = u;
+    }
+  }
+  t.cta_v = pick_cta_shape(sw, n4, n2);
+  t.cta_s = pick_cta_shape(sw, false, false);
+  return t;
+}
+
+// Launches the tuned kernels over the rows `order[0, n_hub + n_rest)` (hub
+// rows first, row-per-CTA) for every column slice, slice-major.  `a` carries
+// the full-width B/C/arg pointers with ld = row stride.  With `side` the hub
+// kernel overlaps the warp kernel of the same slice on that stream.
+gespmm_status_t launch_tuned_rows(const TunedShapes& t, int op, bool fast, const SpmmArgs& a,
+                                  const uint32_t* order, uint32_t n_hub, uint32_t n_rest,
+                                  cudaStream_t st, cudaStream_t side, cudaEvent_t fork,
+                                  cudaEvent_t join, const cudaAccessPolicyWindow* winp) {
+  const bool v_ok = aligned(a.b, 16) && aligned(a.c, 16) && (!a.arg || aligned(a.arg, 16));
+  const bool v2_ok = aligned(a.b, 8) && aligned(a.c, 8) && (!a.arg || aligned(a.arg, 8));
+  const bool n4 = t.n % 4 == 0, n2 = t.n % 2 == 0;
+  for (uint32_t j = 0; j < t.slices; ++j) {
+    const uint32_t off = j * t.slice_w;
+    const uint32_t w = std::min(t.slice_w, t.n - off);
+    const bool narrow = w != t.slice_w;  // ragged last slice
+    const WarpShape wv = narrow ? pick_warp_shape(w, n4, !n4 && n2) : t.warp_v;
+    const WarpShape wsc = narrow ? pick_warp_shape(w, false, false) : t.warp_s;
+    const CtaShape cv = narrow ? pick_cta_shape(w, n4, n2) : t.cta_v;
+    const CtaShape csc = narrow ? pick_cta_shape(w, false, false) : t.cta_s;
+    const WarpShape& ws = v_ok ? wv : wsc;
+    const CtaShape& cs = v_ok ? cv : csc;
+    const WarpShape& wsel = (ws.vec == 2 && !v2_ok) ? wsc : ws;
+    SpmmArgs sa = a;
+    sa.b = a.b + off;
+    sa.c = a.c + off;
+    sa.arg = a.arg ? a.arg + off : nullptr;
+    sa.n = w;
+    if (n_hub) {
+      SpmmArgs h = sa;
+      h.order = order;
+      h.n_sched = n_hub;
+      const uint32_t tw = uint32_t(cs.vec * cs.warps * 32);
+      h.n_tiles = (w + tw - 1) / tw;
+      cudaStream_t hs = side ? side : st;
+      if (side) {
+        GESPMM_CUDA(cudaEventRecord(fork, st), "spmm");
+        GESPMM_CUDA(cudaStreamWaitEvent(side, fork, 0), "spmm");
+      }
+      GESPMM_CUDA(launch_tuned_cta(cs, op, fast, h, hs), "spmm");
+      if (side) GESPMM_CUDA(cudaEventRecord(join, side), "spmm");
+    }
+    sa.order = order + n_hub;
+    sa.n_sched = n_rest;
+    sa.n_tiles = (w + wsel.tile_width() - 1) / wsel.tile_width();
+    if (n_rest) GESPMM_CUDA(launch_tuned_warp(wsel, op, fast, sa, st, winp), "spmm");
+    if (n_hub && side) GESPMM_CUDA(cudaStreamWaitEvent(st, join, 0), "spmm");
+  }
+  return GESPMM_OK;
+}
+
 // Inspector: degree-descending row schedule (stable counting sort) so heavy
 // rows start first (LPT) and sub-warps pair rows of similar length; rows with
 // degree >= threshold are peeled off for the row-per-CTA kernel.
 gespmm_status_t build_tuned(Plan& p, const uint32_t* host_rp, cudaStream_t st) {
   const uint32_t m = p.a.n_rows;
+  p.sh = make_shapes(p.o, p.a.n_cols, p.n, p.device);
+  const uint32_t sw = p.sh.slice_w;
   std::vector<uint32_t> deg(m);
   uint32_t maxd = 0;
   for (uint32_t r = 0; r < m; ++r) {
@@ -205,23 +304,11 @@ gespmm_status_t build_tuned(Plan& p, const uint32_t* host_rp, cudaStream_t st) {
   for (uint32_t r = 0; r < m; ++r) order[count[maxd - deg[r]]++] = r;
 
   const int32_t ht = p.o.hub_threshold;
-  p.hub_threshold = ht > 0 ? uint32_t(ht) : (ht < 0 ? 0xffffffffu : auto_hub_threshold(p.n, host_rp[m]));
+  p.hub_threshold = ht > 0 ? uint32_t(ht) : (ht < 0 ? 0xffffffffu : auto_hub_threshold(sw, host_rp[m]));
   uint32_t n_hub = 0;
   while (n_hub < m && deg[order[n_hub]] >= p.hub_threshold) ++n_hub;
   p.n_hub = n_hub;
 
-  const bool n4 = p.n % 4 == 0, n2 = p.n % 2 == 0;
-  p.warp_v = pick_warp_shape(p.n, n4, !n4 && n2);
-  p.warp_s = pick_warp_shape(p.n, false, false);
-  if (p.o.tuned_cf > 0) {  // explicit CWM merge factor for the warp kernel (tuning)
-    for (WarpShape* w : {&p.warp_v, &p.warp_s}) {
-      WarpShape t = *w;
-      t.cf = p.o.tuned_cf;
-      if (t.lpr == 32 && tuned_shape_supported(t)) *w = t;
-    }
-  }
-  p.cta_v = pick_cta_shape(p.n, n4, n2);
-  p.cta_s = pick_cta_shape(p.n, false, false);
 
   if (m) {
     GESPMM_CUDA(cudaMalloc(reinterpret_cast<void**>(&p.d_order), sizeof(uint32_t) * m),
@@ -239,7 +326,7 @@ gespmm_status_t build_tuned(Plan& p, const uint32_t* host_rp, cudaStream_t st) {
   const uint64_t hot_budget = hot_budget_bytes(p.o, p.a.n_cols, p.n, p.device);
   if (hot_budget && p.o.l2_hints && p.a.nnz) {
     GESPMM_CUDA(build_hot_bitmap(p.a.col_ind, p.a.nnz, p.a.n_cols,
-                                 hot_budget / (uint64_t(p.n) * sizeof(float)), st, &p.d_hot,
+                                 hot_budget / (uint64_t(sw) * sizeof(float)), st, &p.d_hot,
                                  &p.hot),
                 "plan_create");
   }
@@ -247,13 +334,17 @@ gespmm_status_t build_tuned(Plan& p, const uint32_t* host_rp, cudaStream_t st) {
   int len = std::snprintf(buf, sizeof buf,
                 "tuned: warp(vec=%d,lpr=%d,cf=%d) rows=%u; cta(vec=%d,warps=%d) hub_rows=%u "
                 "(deg>=%u); mean_deg=%.1f max_deg=%u",
-                p.warp_v.vec, p.warp_v.lpr, p.warp_v.cf, m - n_hub, p.cta_v.vec, p.cta_v.warps,
+                p.sh.warp_v.vec, p.sh.warp_v.lpr, p.sh.warp_v.cf, m - n_hub, p.sh.cta_v.vec,
+                p.sh.cta_v.warps,
                 n_hub, p.hub_threshold, p.mean_degree, maxd);
   if (p.d_hot && len > 0 && size_t(len) < sizeof buf)
     std::snprintf(buf + len, sizeof buf - size_t(len),
                   "; l2 hot map %.0f MB: %llu cols (gathered>=%u) = %.1f%% of gathers",
                   double(hot_budget) / 1e6, (unsigned long long)p.hot.hot_cols, p.hot.threshold,
                   100.0 * p.hot.hot_nnz_frac);
+  len = int(std::strlen(buf));
+  if (p.sh.slices > 1 && size_t(len) < sizeof buf)
+    std::snprintf(buf + len, sizeof buf - size_t(len), "; %u column slices of %u", p.sh.slices, sw);
   p.desc = buf;
   return GESPMM_OK;
 }
@@ -346,29 +437,12 @@ gespmm_status_t plan_execute_impl(Plan& p, const float* b, float* c, int32_t* ar
   if (p.o.variant != GESPMM_VARIANT_TUNED) {
     args.order = nullptr;
     args.n_sched = p.a.n_rows;
+    args.ld = p.n;
     args.n_tiles = faithful_tiles(p.o.variant, p.o.cf, p.n);
     GESPMM_CUDA(launch_faithful(p.o.variant, p.o.cf, p.op, fast, args, st), "spmm");
     return GESPMM_OK;
   }
-  const bool v_ok = aligned(b, 16) && aligned(c, 16) && (!arg || aligned(arg, 16));
-  const WarpShape& ws = v_ok ? p.warp_v : p.warp_s;
-  const CtaShape& cs = v_ok ? p.cta_v : p.cta_s;
-  const bool v2_ok = aligned(b, 8) && aligned(c, 8) && (!arg || aligned(arg, 8));
-  const WarpShape& wsel = (ws.vec == 2 && !v2_ok) ? p.warp_s : ws;
-  if (p.n_hub) {
-    SpmmArgs h = args;
-    h.order = p.d_order;
-    h.n_sched = p.n_hub;
-    const uint32_t tw = uint32_t(cs.vec * cs.warps * 32);
-    h.n_tiles = (p.n + tw - 1) / tw;
-    GESPMM_CUDA(cudaEventRecord(p.ev_fork, st), "spmm");
-    GESPMM_CUDA(cudaStreamWaitEvent(p.side, p.ev_fork, 0), "spmm");
-    GESPMM_CUDA(launch_tuned_cta(cs, p.op, fast, h, p.side), "spmm");
-    GESPMM_CUDA(cudaEventRecord(p.ev_join, p.side), "spmm");
-  }
-  args.order = p.d_order + p.n_hub;
-  args.n_sched = p.a.n_rows - p.n_hub;
-  args.n_tiles = (p.n + wsel.tile_width() - 1) / wsel.tile_width();
+  args.ld = p.n;
   cudaAccessPolicyWindow win{};
   const cudaAccessPolicyWindow* winp = nullptr;
   if (p.o.l2_persist) {
@@ -383,9 +457,8 @@ gespmm_status_t plan_execute_impl(Plan& p, const float* b, float* c, int32_t* ar
       winp = &win;
     }
   }
-  if (args.n_sched) GESPMM_CUDA(launch_tuned_warp(wsel, p.op, fast, args, st, winp), "spmm");
-  if (p.n_hub) GESPMM_CUDA(cudaStreamWaitEvent(st, p.ev_join, 0), "spmm");
-  return GESPMM_OK;
+  return launch_tuned_rows(p.sh, p.op, fast, args, p.d_order, p.n_hub, p.a.n_rows - p.n_hub, st,
+                           p.side, p.ev_fork, p.ev_join, winp);
 }
 
 // Small LRU of plans for the plan-less device entry point: keyed by the CSR
@@ -686,11 +759,14 @@ gespmm_status_t gespmm_spmm_host(const gespmm_csr_t* a, const float* b, uint32_t
   //      rows at or above the hub threshold first, for the row-per-CTA kernel
   const bool tuned = o.variant == GESPMM_VARIANT_TUNED;
   uint32_t hub_count[kMaxChunks] = {};
-  WarpShape wv{}, wsc{};
-  CtaShape cv{}, csc{};
+  TunedShapes shapes;
   if (tuned) {
+    int dev = 0;
+    GESPMM_CUDA(cudaGetDevice(&dev), "spmm");
+    shapes = make_shapes(o, a->n_cols, n, dev);
     const int32_t ht = o.hub_threshold;
-    const uint32_t hub_t = ht > 0 ? uint32_t(ht) : (ht < 0 ? 0xffffffffu : auto_hub_threshold(n, nnz));
+    const uint32_t hub_t =
+        ht > 0 ? uint32_t(ht) : (ht < 0 ? 0xffffffffu : auto_hub_threshold(shapes.slice_w, nnz));
     std::vector<uint32_t> order(m);
     uint32_t maxd = 0;
     for (uint64_t r = 0; r < m; ++r) maxd = std::max(maxd, a->row_ptr[r + 1] - a->row_ptr[r]);
@@ -715,11 +791,6 @@ gespmm_status_t gespmm_spmm_host(const gespmm_csr_t* a, const float* b, uint32_t
                                 cudaMemcpyHostToDevice, ws->in), "spmm");
     // order[] lives in a host vector: wait for that copy before it goes away
     GESPMM_CUDA(cudaStreamSynchronize(ws->in), "spmm");
-    const bool n4 = n % 4 == 0, n2 = n % 2 == 0;
-    wv = pick_warp_shape(n, n4, !n4 && n2);
-    wsc = pick_warp_shape(n, false, false);
-    cv = pick_cta_shape(n, n4, n2);
-    csc = pick_cta_shape(n, false, false);
   }
   tr.mark("row_ptr+B enqueued, schedule built");
   GESPMM_CUDA(cudaEventRecord(ws->ev_b, ws->in), "spmm");
@@ -749,6 +820,7 @@ gespmm_status_t gespmm_spmm_host(const gespmm_csr_t* a, const float* b, uint32_t
     args.c = d_c + uint64_t(lo) * n;
     args.arg = d_arg ? d_arg + uint64_t(lo) * n : nullptr;
     args.n = n;
+    args.ld = n;
     args.arg_col = o.arg_kind == GESPMM_ARG_COLUMN;
     args.skip_tail = o.fault_skip_tail;
     args.hints = o.l2_hints;
@@ -759,24 +831,10 @@ gespmm_status_t gespmm_spmm_host(const gespmm_csr_t* a, const float* b, uint32_t
         args.n_tiles = faithful_tiles(o.variant, o.cf, n);
         GESPMM_CUDA(launch_faithful(o.variant, o.cf, op, fast, args, ws->stream), "spmm");
       } else {
-        const bool v_ok = aligned(args.c, 16) && (!args.arg || aligned(args.arg, 16));
-        const WarpShape& w = v_ok ? wv : wsc;
-        const CtaShape& cs = v_ok ? cv : csc;
-        const bool v2 = aligned(args.c, 8) && (!args.arg || aligned(args.arg, 8));
-        const WarpShape& wsel = (w.vec == 2 && !v2) ? wsc : w;
         const uint32_t nh = hub_count[ch];
-        if (nh) {
-          SpmmArgs h = args;
-          h.order = d_order + lo;
-          h.n_sched = nh;
-          const uint32_t tw = uint32_t(cs.vec * cs.warps * 32);
-          h.n_tiles = (n + tw - 1) / tw;
-          GESPMM_CUDA(launch_tuned_cta(cs, op, fast, h, ws->stream), "spmm");
-        }
-        args.order = d_order + lo + nh;
-        args.n_sched = hi - lo - nh;
-        args.n_tiles = (n + wsel.tile_width() - 1) / wsel.tile_width();
-        if (args.n_sched) GESPMM_CUDA(launch_tuned_warp(wsel, op, fast, args, ws->stream), "spmm");
+        s = launch_tuned_rows(shapes, op, fast, args, d_order + lo, nh, hi - lo - nh, ws->stream,
+                              nullptr, nullptr, nullptr, nullptr);
+        if (s != GESPMM_OK) return s;
       }
     }
     GESPMM_CUDA(cudaEventRecord(ws->ev_done[ch], ws->stream), "spmm");

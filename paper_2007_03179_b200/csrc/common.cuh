@@ -267,7 +267,8 @@ struct SpmmArgs {
   int32_t* arg;
   const uint32_t* order;  // row schedule (nullable -> identity)
   uint32_t n_sched;       // rows in the schedule
-  uint32_t n;             // dense width N
+  uint32_t n;             // dense width N (of this launch's column slice)
+  uint32_t ld;            // row stride of B, C and arg in elements (>= n)
   uint32_t n_tiles;       // column tiles per row
   int arg_col;            // arg = col_ind[p] instead of p
   int skip_tail;

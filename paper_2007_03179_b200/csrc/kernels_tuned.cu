@@ -107,7 +107,7 @@ __global__ void __launch_bounds__(32 * kWarpBlock, warp_min_blocks<OP, CF>()) k_
       who[c][e] = -1;
     }
   }
-  const uint32_t stride = a.n * 4u;  // bytes per B row (B < 4 GiB per row index * stride)
+  const uint32_t stride = a.ld * 4u;  // bytes per B row (B < 4 GiB per row index * stride)
   const uint32_t* ci = a.col_ind + start;
   const float* vs = a.vals + start;
   uint32_t* my_col = &s_col[wib][0][0];
@@ -191,7 +191,7 @@ __global__ void __launch_bounds__(32 * kWarpBlock, warp_min_blocks<OP, CF>()) k_
     float out[VEC];
 #pragma unroll
     for (int e = 0; e < VEC; ++e) out[e] = finish<OP>(acc[c][e], row_len);
-    const uint64_t o = uint64_t(row) * a.n + col0 + c * SUB;
+    const uint64_t o = uint64_t(row) * a.ld + col0 + c * SUB;
     st_stream<VEC>(a.c + o, out, pol.stream);
     if (R::kHasArg && a.arg) st_stream_i32<VEC>(a.arg + o, who[c], pol.stream);
   }
@@ -263,7 +263,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_cta(SpmmArgs a) {
       for (int u = 0; u < U; ++u) {
 #pragma unroll
         for (int e = 0; e < VEC; ++e) bv[u].x[e] = 0.0f;
-        if (colok && kk + u < n_cur) bv[u] = ld_keep<VEC>(bcol + uint64_t(kv[u].x) * a.n, pol.keep);
+        if (colok && kk + u < n_cur) bv[u] = ld_keep<VEC>(bcol + uint64_t(kv[u].x) * a.ld, pol.keep);
       }
 #pragma unroll
       for (int u = 0; u < U; ++u) {
@@ -284,7 +284,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_cta(SpmmArgs a) {
     float out[VEC];
 #pragma unroll
     for (int e = 0; e < VEC; ++e) out[e] = finish<OP>(acc[e], full_end - start);
-    const uint64_t o = uint64_t(row) * a.n + col0;
+    const uint64_t o = uint64_t(row) * a.ld + col0;
     st_stream<VEC>(a.c + o, out, pol.stream);
     if (R::kHasArg && a.arg) st_stream_i32<VEC>(a.arg + o, who, pol.stream);
   }

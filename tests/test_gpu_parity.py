@@ -390,3 +390,22 @@ def test_products_scale_max_arg_sampled_rows(cuda):
     # oracle positions are within the sub-CSR; map back to global CSR positions
     mapped = np.where(warg >= 0, idx[np.maximum(warg, 0)], -1)
     assert np.array_equal(got_arg, mapped)
+
+
+@pytest.mark.parametrize("slices", [2, 3, 8])
+@pytest.mark.parametrize("n", [64, 100, 256])
+def test_column_slices_keep_bits(slices, n, cuda):
+    """Slice-major traversal (col_slices) only reorders which columns of B are
+    live; every op with edge args stays bit-identical, incl. ragged last slices
+    and the hub kernel (threshold forced low)."""
+    a, b = _powerlaw(3000, 120000, 2500, 11 + n, n)
+    for op in OPS:
+        want_arg = op in ("max", "min")
+        want, warg = _oracle(a, b, op, want_arg)
+        for ht in (0, 300):
+            ex = G.ExecOptions(col_slices=slices, hub_threshold=ht)
+            c, arg = G.native_spmm_arg(a, b, G.KernelVariant.tuned(), G.reduce_op_by_name(op),
+                                       exec=ex, want_arg=want_arg)
+            assert first_divergence(c.data, want) is None, (op, ht)
+            if want_arg:
+                assert np.array_equal(arg, warg), (op, ht)

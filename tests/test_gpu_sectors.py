@@ -34,8 +34,9 @@ def test_l1_sectors_equal_reference_simulator_transactions(tmp_path, cuda):
     os.environ["GESPMM_SECTOR_CASES"] = "small"
     try:
         table = S.report(str(out), str(tmp_path / "parity"))
+        expected = len(S.cases()) * len(S.VARIANTS)
     finally:
         del os.environ["GESPMM_SECTOR_CASES"]
-    assert len(table) == len(S.cases()) * len(S.VARIANTS)
+    assert len(table) == expected
     for row in table:
         assert row["ld_match"] and row["st_match"], row
