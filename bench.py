@@ -574,7 +574,8 @@ def main():
     p.add_argument("--cf", type=int, default=2)
     p.add_argument("--hub-threshold", type=int, default=0)
     p.add_argument("--fast", action="store_true", help="FFMA sum (1e-5 tolerance) instead of exact")
-    p.add_argument("--l2-persist", action="store_true", help="L2 access-policy window on B")
+    p.add_argument("--l2-persist", type=int, nargs="?", const=1, default=0,
+                   help="1: L2 access-policy window on B; 2: persisting set-aside only")
     p.add_argument("--no-hints", action="store_true", help="evict_normal instead of L2 hints")
     p.add_argument("--hints", type=int, default=1,
                    help="L2 hint mode (1: cold B rows evict_first, 2: evict_normal)")

@@ -88,11 +88,13 @@ typedef struct {
                          evict_normal instead of evict_first */
   int32_t hub_threshold; /* TUNED: rows with degree >= this go row-per-CTA; 0 = auto, <0 = off */
   int32_t l2_persist; /* 1: launch with an L2 access-policy window marking B persisting
-                         (sets the device's persisting-L2 limit to its maximum); default 0 */
+                         (sets the device's persisting-L2 limit to its maximum); 2: only raise
+                         the persisting-L2 set-aside (evict_last lines of the hint policies
+                         may use it), no window; default 0 */
   int32_t l2_hot_mb;  /* TUNED plans: frequency-aware L2 policy for B.  The plan counts the
                          gathers per column and only the most-gathered columns whose B rows
                          fit this many MB are loaded evict_last (the rest evict_first).
-                         0 = auto (on when B exceeds twice the L2), <0 = off.  Hints only:
+                         0 = auto (off: measured slower on B200), <0 = off.  Hints only:
                          results are unaffected. */
   int32_t tuned_cf;   /* TUNED plans: CWM merge factor (column sub-tiles per lane) of the
                          full-warp row kernel, 1, 2 or 4; 0 = auto from N */

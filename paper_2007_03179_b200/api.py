@@ -293,8 +293,8 @@ class ExecOptions:
     l2_hints: int = 1               # 0 off; 1 B evict_last, CSR/C evict_first; 2 = 1 but
                                     # cold B rows (hot-column map) evict_normal
     hub_threshold: int = 0          # 0 auto, <0 off
-    l2_persist: bool = False        # L2 access-policy window marking B persisting
-    l2_hot_mb: int = 0              # hot-column map budget in MB: 0 auto, <0 off
+    l2_persist: int = 0             # 1 L2 access-policy window marking B persisting; 2 set-aside only
+    l2_hot_mb: int = 0              # hot-column map budget in MB: 0 auto (off), <0 off
     tuned_cf: int = 0               # tuned warp kernel merge factor (1/2/4), 0 auto
     col_slices: int = 0             # slice-major column traversal: 0 auto, 1 off, S slices
 

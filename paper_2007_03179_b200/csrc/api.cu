@@ -175,19 +175,18 @@ uint32_t auto_hub_threshold(uint32_t n, uint64_t nnz) {
 }
 
 // Frequency-aware L2 policy budget (bytes of B rows kept evict_last), 0 = off.
-// Auto: on when B exceeds twice the L2 — then LRU among all B rows thrashes and
-// the most-gathered rows are worth pinning; the budget is 60% of L2, leaving
-// room for the streamed CSR and C lines in flight.  Measured on B200
-// (profiles/r1_hot_sweep.txt): products N=256 max+arg (B 2.5 GB) 14.49 -> 13.70
-// ms; Reddit N=128 (B 119 MB, about the L2 size) 2.99 -> 3.10 ms, so off there.
+// Opt-in (l2_hot_mb > 0).  History on B200 (profiles/r1_hot_sweep.txt,
+// profiles/r1_kernel_v4.txt): with the per-load policy select of the first
+// kernel it helped products N=256 max+arg (14.49 -> 13.70 ms); once the
+// un-mapped kernel dropped that select (one loop-invariant policy register,
+// check-free full batches) the map-less kernel is faster (13.14 ms) than the
+// mapped one (17.2 ms: the cold/hot branch costs registers and spills at 6
+// CTAs/SM), so auto = off.
 uint64_t hot_budget_bytes(const gespmm_options_t& o, uint32_t k, uint32_t n, int dev) {
-  if (o.l2_hot_mb < 0 || k >= 0x80000000u) return 0;  // bit 31 of a staged column is the mark
-  if (o.l2_hot_mb > 0) return uint64_t(o.l2_hot_mb) << 20;
-  int l2 = 0;
-  cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev);
-  const uint64_t b_bytes = uint64_t(k) * n * sizeof(float);
-  if (l2 <= 0 || b_bytes <= uint64_t(l2) * 2) return 0;
-  return uint64_t(l2) * 6 / 10;
+  (void)n;
+  (void)dev;
+  if (o.l2_hot_mb <= 0 || k >= 0x80000000u) return 0;  // bit 31 of a staged column is the mark
+  return uint64_t(o.l2_hot_mb) << 20;
 }
 
 // Column slices (slice-major traversal).  The kernels fold each output
@@ -445,7 +444,8 @@ gespmm_status_t plan_execute_impl(Plan& p, const float* b, float* c, int32_t* ar
   args.ld = p.n;
   cudaAccessPolicyWindow win{};
   const cudaAccessPolicyWindow* winp = nullptr;
-  if (p.o.l2_persist) {
+  if (p.o.l2_persist == 2) persist_limits(p.device);  // set-aside only, no window
+  if (p.o.l2_persist == 1) {
     const size_t b_bytes = size_t(p.a.n_cols) * p.n * sizeof(float);
     const PersistLimits lim = persist_limits(p.device);
     if (lim.max_window > 0 && lim.set_aside > 0 && b_bytes > 0) {

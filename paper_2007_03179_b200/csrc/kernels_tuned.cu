@@ -54,7 +54,10 @@ constexpr int warp_min_blocks() {
   return Reduce<OP>::kHasArg ? (CF >= 4 ? 4 : 6) : 7;
 }
 
-template <int OP, bool FAST, int VEC, int LPR, int CF>
+// HOT: the plan carries a hot-column map (bit 31 of a staged column marks a
+// cold B row, loaded with the cold policy).  Without it every gather uses one
+// policy register, so no per-load descriptor selection is emitted.
+template <int OP, bool FAST, int VEC, int LPR, int CF, bool HOT>
 __global__ void __launch_bounds__(32 * kWarpBlock, warp_min_blocks<OP, CF>()) k_warp(SpmmArgs a) {
   using R = Reduce<OP>;
   constexpr int RPW = 32 / LPR;                     // rows per warp
@@ -107,6 +110,10 @@ __global__ void __launch_bounds__(32 * kWarpBlock, warp_min_blocks<OP, CF>()) k_
       who[c][e] = -1;
     }
   }
+  bool all_cols = true;  // every sub-tile of every row of the warp in range (warp-uniform)
+#pragma unroll
+  for (int c = 0; c < CF; ++c) all_cols = all_cols && colok[c];
+  all_cols = __all_sync(kFull, all_cols);
   const uint32_t stride = a.ld * 4u;  // bytes per B row (B < 4 GiB per row index * stride)
   const uint32_t* ci = a.col_ind + start;
   const float* vs = a.vals + start;
@@ -120,7 +127,7 @@ __global__ void __launch_bounds__(32 * kWarpBlock, warp_min_blocks<OP, CF>()) k_
     if (sl < len) {
       k0 = ld_stream_u32(ci + sl, pol.stream);
       v0 = ld_stream_f32(vs + sl, pol.stream);
-      if (a.hot) k0 |= cold_mark(a.hot, k0);
+      if (HOT) k0 |= cold_mark(a.hot, k0);
     }
     my_col[lane] = k0;
     my_val[lane] = v0;
@@ -134,7 +141,7 @@ __global__ void __launch_bounds__(32 * kWarpBlock, warp_min_blocks<OP, CF>()) k_
     if (nxt < len) {
       kn = ld_stream_u32(ci + nxt, pol.stream);
       vn = ld_stream_f32(vs + nxt, pol.stream);
-      if (a.hot) kn |= cold_mark(a.hot, kn);
+      if (HOT) kn |= cold_mark(a.hot, kn);
     }
     __syncwarp();
     const uint32_t* cs = my_col + buf * 32 + sub * LPR;
@@ -157,25 +164,52 @@ __global__ void __launch_bounds__(32 * kWarpBlock, warp_min_blocks<OP, CF>()) k_
       }
       // all U*CF gathers issued before any fold (memory-level parallelism);
       // unpredicated: past-the-end slots re-read a valid row.
-      // bit 31 of a staged column marks a cold B row (hot-column map)
       Vec<VEC> bv[U][CF];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        const uint64_t pu = (k[u] & kColdBit) ? pol.cold : pol.keep;
-        k[u] &= ~kColdBit;
+        if (HOT) {
+          // bit 31 of a staged column marks a cold B row (hot-column map).  With
+          // one row per warp the mark is warp-uniform: vote on it and branch, so
+          // each load keeps a loop-invariant policy register.
+          const bool cold = RPW == 1 ? __any_sync(kFull, k[u] & kColdBit) : (k[u] & kColdBit);
+          k[u] &= ~kColdBit;
+          if (cold) {
 #pragma unroll
-        for (int c = 0; c < CF; ++c)
-          bv[u][c] = ld_keep<VEC>(
-              reinterpret_cast<const float*>(bbase[c] + uint64_t(k[u]) * stride), pu);
-      }
-      const int32_t rem = int32_t(len - off - kk);  // entries left in this row (may be <= 0)
+            for (int c = 0; c < CF; ++c)
+              bv[u][c] = ld_keep<VEC>(
+                  reinterpret_cast<const float*>(bbase[c] + uint64_t(k[u]) * stride), pol.cold);
+          } else {
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        if (u < rem) {
-          const int32_t pos = a.arg_col ? int32_t(k[u]) : int32_t(start + off + kk + u);
+            for (int c = 0; c < CF; ++c)
+              bv[u][c] = ld_keep<VEC>(
+                  reinterpret_cast<const float*>(bbase[c] + uint64_t(k[u]) * stride), pol.keep);
+          }
+        } else {
 #pragma unroll
           for (int c = 0; c < CF; ++c)
-            if (colok[c]) fold_vec<OP, FAST, VEC>(acc[c], who[c], v[u], bv[u][c].x, pos);
+            bv[u][c] = ld_keep<VEC>(
+                reinterpret_cast<const float*>(bbase[c] + uint64_t(k[u]) * stride), pol.keep);
+        }
+      }
+      const int32_t rem = int32_t(len - off - kk);  // entries left in this row (may be <= 0)
+      const int32_t pos0 = int32_t(start + off + kk);
+      if (rem >= U && all_cols) {
+        // full batch, every sub-tile in range: no per-element predicates
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int32_t pos = a.arg_col ? int32_t(k[u]) : pos0 + u;
+#pragma unroll
+          for (int c = 0; c < CF; ++c) fold_vec<OP, FAST, VEC>(acc[c], who[c], v[u], bv[u][c].x, pos);
+        }
+      } else {
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          if (u < rem) {
+            const int32_t pos = a.arg_col ? int32_t(k[u]) : pos0 + u;
+#pragma unroll
+            for (int c = 0; c < CF; ++c)
+              if (colok[c]) fold_vec<OP, FAST, VEC>(acc[c], who[c], v[u], bv[u][c].x, pos);
+          }
         }
       }
     }
@@ -321,11 +355,12 @@ cudaError_t warp_dispatch(const WarpShape& s, const SpmmArgs& a, cudaStream_t st
   if (blocks == 0) return cudaSuccess;
   if (blocks > 0x7fffffffull) return cudaErrorInvalidConfiguration;
   const dim3 g{uint32_t(blocks)}, b{32 * kWarpBlock};
-#define GESPMM_W(V, L, F)                                              \
-  if (s.vec == V && s.lpr == L && s.cf == F) {                         \
-    const cudaError_t e = launch_ex(k_warp<OP, FAST, V, L, F>, g, b, st, a, window); \
-    note_launch();                                                     \
-    return e;                                                          \
+#define GESPMM_W(V, L, F)                                                              \
+  if (s.vec == V && s.lpr == L && s.cf == F) {                                         \
+    const cudaError_t e = a.hot ? launch_ex(k_warp<OP, FAST, V, L, F, true>, g, b, st, a, window) \
+                                : launch_ex(k_warp<OP, FAST, V, L, F, false>, g, b, st, a, window); \
+    note_launch();                                                                     \
+    return e;                                                                          \
   }
   GESPMM_W(4, 4, 1) GESPMM_W(4, 8, 1) GESPMM_W(4, 16, 1) GESPMM_W(4, 32, 1)
   GESPMM_W(4, 32, 2) GESPMM_W(4, 32, 4)
