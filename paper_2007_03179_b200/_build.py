@@ -48,7 +48,12 @@ def _run(cmd):
     return r.stderr
 
 
-def build(verbose: bool = False, force: bool = False) -> str:
+def build(verbose: bool = False, force: bool = False, defines=(), build_dir=None,
+          lib=None) -> str:
+    """defines/build_dir/lib: an experimental variant (-D flags) built into its
+    own object dir and library path (tools/variant_build.py)."""
+    BUILD = build_dir or globals()["BUILD"]
+    LIB = lib or globals()["LIB"]
     os.makedirs(BUILD, exist_ok=True)
     hdrs = [os.path.join(CSRC, h) for h in HEADERS] + [os.path.join(INCLUDE, "gespmm", "gespmm.h")]
     jobs, objs = [], []
@@ -58,11 +63,11 @@ def build(verbose: bool = False, force: bool = False) -> str:
         objs.append(obj)
         if force or _stale(obj, [path] + hdrs):
             if src.endswith(".cu"):
-                cmd = [NVCC] + NVCC_FLAGS + ["-c", path, "-o", obj]
+                cmd = [NVCC] + NVCC_FLAGS + [f"-D{d}" for d in defines] + ["-c", path, "-o", obj]
                 if src == "kernels_tuned.cu" and verbose:
                     cmd += ["-Xptxas", "-v"]
             else:
-                cmd = ["g++"] + CXX_FLAGS + ["-c", path, "-o", obj]
+                cmd = ["g++"] + CXX_FLAGS + [f"-D{d}" for d in defines] + ["-c", path, "-o", obj]
             jobs.append(cmd)
     log = []
     if jobs:

@@ -13,7 +13,9 @@ import shutil
 import threading
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libgespmm.so")
+# GESPMM_LIB: an alternative build of the same library (A/B kernel experiments,
+# tools/variant_build.py); the default is the in-tree build.
+LIB_PATH = os.environ.get("GESPMM_LIB") or os.path.join(_HERE, "libgespmm.so")
 
 # gespmm_status_t
 OK, EINVAL, EDIM, ENONCANON, ECUDA, ENOMEM, EUNSUPPORTED = range(7)

@@ -230,10 +230,12 @@ TunedShapes make_shapes(const gespmm_options_t& o, uint32_t k, uint32_t n, int d
 // rows first, row-per-CTA) for every column slice, slice-major.  `a` carries
 // the full-width B/C/arg pointers with ld = row stride.  With `side` the hub
 // kernel overlaps the warp kernel of the same slice on that stream.
-gespmm_status_t launch_tuned_rows(const TunedShapes& t, int op, bool fast, const SpmmArgs& a,
+gespmm_status_t launch_tuned_rows(const TunedShapes& t, int op, bool fast, const SpmmArgs& a0,
                                   const uint32_t* order, uint32_t n_hub, uint32_t n_rest,
                                   cudaStream_t st, cudaStream_t side, cudaEvent_t fork,
                                   cudaEvent_t join, const cudaAccessPolicyWindow* winp) {
+  SpmmArgs a = a0;
+  GESPMM_CUDA(resolve_policies(&a, st), "spmm");
   const bool v_ok = aligned(a.b, 16) && aligned(a.c, 16) && (!a.arg || aligned(a.arg, 16));
   const bool v2_ok = aligned(a.b, 8) && aligned(a.c, 8) && (!a.arg || aligned(a.arg, 8));
   const bool n4 = t.n % 4 == 0, n2 = t.n % 2 == 0;

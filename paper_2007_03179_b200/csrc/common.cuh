@@ -274,6 +274,23 @@ struct SpmmArgs {
   int skip_tail;
   int hints;              // 0 off, 1 B evict_last / CSR,C evict_first, 2 = 1 with cold B evict_normal
   const uint32_t* hot;    // hot-column bitmap (nullable): cold B rows use the cold policy
+  // L2 policies resolved once on the device (resolve_policies) and passed as
+  // launch parameters: they then live in uniform registers, so a per-gather
+  // choice between two of them is a uniform select, not a per-load descriptor
+  // move.  pol_valid = 0 -> the kernel creates them itself (make_policies).
+  uint64_t pol_keep, pol_cold, pol_stream;
+  int pol_valid;
 };
+
+__device__ __forceinline__ Policies args_policies(const SpmmArgs& a) {
+  if (a.pol_valid) {
+    Policies p;
+    p.keep = a.pol_keep;
+    p.cold = a.pol_cold;
+    p.stream = a.pol_stream;
+    return p;
+  }
+  return make_policies(a.hints);
+}
 
 }  // namespace gespmm

@@ -18,6 +18,7 @@
 //   or 8 vector loads per lane) gives the hub the latency hiding a single warp
 //   cannot.
 #include <algorithm>
+#include <mutex>
 
 #include "common.cuh"
 #include "launch.h"
@@ -78,7 +79,7 @@ __global__ void __launch_bounds__(32 * kWarpBlock, warp_min_blocks<OP, CF>()) k_
   const uint64_t unit = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const uint64_t groups = (uint64_t(a.n_sched) + RPW - 1) / RPW;
   if (unit >= groups * a.n_tiles) return;  // warp-uniform exit
-  const Policies pol = make_policies(a.hints);
+  const Policies pol = args_policies(a);
 
   const uint32_t group = uint32_t(unit / a.n_tiles);
   const uint32_t tile = uint32_t(unit % a.n_tiles);
@@ -167,29 +168,19 @@ __global__ void __launch_bounds__(32 * kWarpBlock, warp_min_blocks<OP, CF>()) k_
       Vec<VEC> bv[U][CF];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
+        uint64_t pu = pol.keep;
         if (HOT) {
           // bit 31 of a staged column marks a cold B row (hot-column map).  With
-          // one row per warp the mark is warp-uniform: vote on it and branch, so
-          // each load keeps a loop-invariant policy register.
+          // one row per warp the mark is warp-uniform (vote), and with the
+          // policies in launch parameters the choice is a uniform select.
           const bool cold = RPW == 1 ? __any_sync(kFull, k[u] & kColdBit) : (k[u] & kColdBit);
           k[u] &= ~kColdBit;
-          if (cold) {
-#pragma unroll
-            for (int c = 0; c < CF; ++c)
-              bv[u][c] = ld_keep<VEC>(
-                  reinterpret_cast<const float*>(bbase[c] + uint64_t(k[u]) * stride), pol.cold);
-          } else {
-#pragma unroll
-            for (int c = 0; c < CF; ++c)
-              bv[u][c] = ld_keep<VEC>(
-                  reinterpret_cast<const float*>(bbase[c] + uint64_t(k[u]) * stride), pol.keep);
-          }
-        } else {
-#pragma unroll
-          for (int c = 0; c < CF; ++c)
-            bv[u][c] = ld_keep<VEC>(
-                reinterpret_cast<const float*>(bbase[c] + uint64_t(k[u]) * stride), pol.keep);
+          pu = cold ? pol.cold : pol.keep;
         }
+#pragma unroll
+        for (int c = 0; c < CF; ++c)
+          bv[u][c] = ld_keep<VEC>(
+              reinterpret_cast<const float*>(bbase[c] + uint64_t(k[u]) * stride), pu);
       }
       const int32_t rem = int32_t(len - off - kk);  // entries left in this row (may be <= 0)
       const int32_t pos0 = int32_t(start + off + kk);
@@ -389,7 +380,50 @@ cudaError_t cta_dispatch(const CtaShape& s, const SpmmArgs& a, cudaStream_t st) 
   return cudaErrorInvalidValue;
 }
 
+__global__ void k_policies(int hints, uint64_t* out) {
+  const Policies p = make_policies(hints);
+  out[0] = p.keep;
+  out[1] = p.cold;
+  out[2] = p.stream;
+}
+
 }  // namespace
+
+cudaError_t resolve_policies(SpmmArgs* a, cudaStream_t st) {
+  struct Entry {
+    bool ok = false;
+    uint64_t v[3] = {0, 0, 0};
+  };
+  static std::mutex mu;
+  static Entry cache[64][3];
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  const int h = a->hints < 0 ? 0 : (a->hints > 2 ? 2 : a->hints);
+  if (dev < 0 || dev >= 64) {
+    a->pol_valid = 0;
+    return cudaSuccess;
+  }
+  std::lock_guard<std::mutex> lk(mu);
+  Entry& en = cache[dev][h];
+  if (!en.ok) {
+    uint64_t* d = nullptr;
+    if ((e = cudaMalloc(reinterpret_cast<void**>(&d), sizeof(en.v))) != cudaSuccess) return e;
+    k_policies<<<1, 1, 0, st>>>(h, d);
+    note_launch();
+    e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaMemcpyAsync(en.v, d, sizeof(en.v), cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    cudaFree(d);
+    if (e != cudaSuccess) return e;
+    en.ok = true;
+  }
+  a->pol_keep = en.v[0];
+  a->pol_cold = en.v[1];
+  a->pol_stream = en.v[2];
+  a->pol_valid = 1;
+  return cudaSuccess;
+}
 
 bool tuned_shape_supported(const WarpShape& s) {
   static const int table[][3] = {{4, 4, 1},  {4, 8, 1},  {4, 16, 1}, {4, 32, 1}, {4, 32, 2},

@@ -18,6 +18,11 @@ gespmm_status_t set_error(gespmm_status_t st, const std::string& msg);
 // Counts every kernel launch issued by the library (reported by bench.py).
 void note_launch();
 
+// Creates the L2 cache policies for `hints` on the current device once (a
+// one-thread kernel, cached per device and hint mode) and stores them into
+// a->pol_* (pol_valid = 1).  Synchronous the first time only.
+cudaError_t resolve_policies(SpmmArgs* a, cudaStream_t st);
+
 // --- faithful Algorithms 1-3 (kernels_faithful.cu) ---
 uint32_t faithful_tiles(int variant, uint32_t cf, uint32_t n);
 cudaError_t launch_faithful(int variant, uint32_t cf, int op, bool fast, const SpmmArgs& a,
