@@ -346,7 +346,8 @@ def run_ours(args, cfg):
     hints = 0 if args.no_hints else args.hints
     ex = G.ExecOptions(hub_threshold=args.hub_threshold, exact=not args.fast,
                        l2_persist=args.l2_persist, l2_hints=hints, l2_hot_mb=args.l2_hot_mb,
-                       tuned_cf=args.tuned_cf, col_slices=args.col_slices)
+                       tuned_cf=args.tuned_cf, col_slices=args.col_slices,
+                       rows_per_warp=args.rows_per_warp)
     variant = G.variant_by_name(args.variant, args.cf)
     plan = G.Plan(d, n, op, variant=variant, exec=ex)
     log(f"[bench] rank {rank}: rows [{info.lo},{info.hi}) nnz {shard.nnz()} plan: {plan.description}")
@@ -421,7 +422,7 @@ def run_ours(args, cfg):
                                  hub_threshold=args.hub_threshold, exact=int(not args.fast),
                                  l2_persist=int(args.l2_persist), l2_hints=hints,
                                  l2_hot_mb=args.l2_hot_mb, tuned_cf=args.tuned_cf,
-                                 col_slices=args.col_slices)
+                                 col_slices=args.col_slices, rows_per_warp=args.rows_per_warp)
         L = _lib.lib()
 
         def host_call():
@@ -582,6 +583,8 @@ def main():
     p.add_argument("--col-slices", type=int, default=0,
                    help="slice-major column traversal: 0 auto, 1 off, S slices")
     p.add_argument("--tuned-cf", type=int, default=0, help="tuned warp kernel merge factor")
+    p.add_argument("--rows-per-warp", type=int, default=0,
+                   help="rows sharing a warp (float4 lanes, N <= 256): 0 auto")
     p.add_argument("--l2-hot-mb", type=int, default=0,
                    help="hot-column map budget in MB (0 auto, <0 off)")
     p.add_argument("--no-flush", action="store_true", help="skip the L2 flush between steps")

@@ -104,7 +104,9 @@ typedef struct {
                          folded by one thread in CSR order: results are unchanged.
                          0 = auto (currently off: measured slower on B200), 1 = off,
                          S >= 2 explicit */
-  int32_t reserved[4];
+  int32_t rows_per_warp; /* TUNED plans: rows sharing a warp when N <= 256 (float4 lanes): 0 =
+                         auto (4 for low-degree matrices, else as N dictates), 1, 2, 4 or 8 */
+  int32_t reserved[3];
 } gespmm_options_t;
 
 void gespmm_options_default(gespmm_options_t* opts);

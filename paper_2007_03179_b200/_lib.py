@@ -53,7 +53,8 @@ class Options(C.Structure):
                 ("fault_skip_tail", C.c_int32), ("l2_hints", C.c_int32),
                 ("hub_threshold", C.c_int32), ("l2_persist", C.c_int32),
                 ("l2_hot_mb", C.c_int32), ("tuned_cf", C.c_int32),
-                ("col_slices", C.c_int32), ("reserved", C.c_int32 * 4)]
+                ("col_slices", C.c_int32), ("rows_per_warp", C.c_int32),
+                ("reserved", C.c_int32 * 3)]
 
 
 _lock = threading.Lock()

@@ -94,6 +94,9 @@ gespmm_status_t check_opts(const gespmm_options_t& o) {
     return fail(GESPMM_EINVAL, "tuned_cf must be 0 (auto), 1, 2 or 4");
   if (o.arg_kind != GESPMM_ARG_EDGE && o.arg_kind != GESPMM_ARG_COLUMN)
     return fail(GESPMM_EINVAL, "arg_kind must be edge (0) or column (1)");
+  if (o.rows_per_warp != 0 && o.rows_per_warp != 1 && o.rows_per_warp != 2 &&
+      o.rows_per_warp != 4 && o.rows_per_warp != 8)
+    return fail(GESPMM_EINVAL, "rows_per_warp must be 0 (auto), 1, 2, 4 or 8");
   return GESPMM_OK;
 }
 
@@ -127,6 +130,7 @@ struct TunedShapes {
   uint32_t n = 0;
   uint32_t slices = 1;   // column slices, traversed slice-major
   uint32_t slice_w = 0;  // columns per slice (the last one may be narrower)
+  int rpw = 1;           // rows per warp requested for float4 lanes
   WarpShape warp_v, warp_s;
   CtaShape cta_v, cta_s;
 };
@@ -202,7 +206,8 @@ uint32_t pick_slices(const gespmm_options_t& o, uint32_t /*k*/, uint32_t n, int 
   return 1;
 }
 
-TunedShapes make_shapes(const gespmm_options_t& o, uint32_t k, uint32_t n, int dev) {
+TunedShapes make_shapes(const gespmm_options_t& o, uint32_t k, uint32_t n, int dev,
+                        double mean_degree) {
   TunedShapes t;
   t.n = n;
   t.slices = pick_slices(o, k, n, dev);
@@ -212,7 +217,8 @@ TunedShapes make_shapes(const gespmm_options_t& o, uint32_t k, uint32_t n, int d
   t.slices = (n + t.slice_w - 1) / t.slice_w;
   const uint32_t sw = t.slice_w;
   const bool n4 = n % 4 == 0, n2 = n % 2 == 0;
-  t.warp_v = pick_warp_shape(sw, n4, !n4 && n2);
+  t.rpw = o.rows_per_warp > 0 ? o.rows_per_warp : (mean_degree <= 16.0 ? 4 : 1);
+  t.warp_v = pick_warp_shape(sw, n4, !n4 && n2, t.rpw);
   t.warp_s = pick_warp_shape(sw, false, false);
   if (o.tuned_cf > 0) {  // explicit CWM merge factor for the warp kernel (tuning)
     for (WarpShape* ws : {&t.warp_v, &t.warp_s}) {
@@ -243,8 +249,8 @@ gespmm_status_t launch_tuned_rows(const TunedShapes& t, int op, bool fast, const
     const uint32_t off = j * t.slice_w;
     const uint32_t w = std::min(t.slice_w, t.n - off);
     const bool narrow = w != t.slice_w;  // ragged last slice
-    const WarpShape wv = narrow ? pick_warp_shape(w, n4, !n4 && n2) : t.warp_v;
-    const WarpShape wsc = narrow ? pick_warp_shape(w, false, false) : t.warp_s;
+    WarpShape wv = narrow ? pick_warp_shape(w, n4, !n4 && n2, t.rpw) : t.warp_v;
+    WarpShape wsc = narrow ? pick_warp_shape(w, false, false) : t.warp_s;
     const CtaShape cv = narrow ? pick_cta_shape(w, n4, n2) : t.cta_v;
     const CtaShape csc = narrow ? pick_cta_shape(w, false, false) : t.cta_s;
     const WarpShape& ws = v_ok ? wv : wsc;
@@ -283,8 +289,6 @@ gespmm_status_t launch_tuned_rows(const TunedShapes& t, int op, bool fast, const
 // degree >= threshold are peeled off for the row-per-CTA kernel.
 gespmm_status_t build_tuned(Plan& p, const uint32_t* host_rp, cudaStream_t st) {
   const uint32_t m = p.a.n_rows;
-  p.sh = make_shapes(p.o, p.a.n_cols, p.n, p.device);
-  const uint32_t sw = p.sh.slice_w;
   std::vector<uint32_t> deg(m);
   uint32_t maxd = 0;
   for (uint32_t r = 0; r < m; ++r) {
@@ -293,6 +297,8 @@ gespmm_status_t build_tuned(Plan& p, const uint32_t* host_rp, cudaStream_t st) {
   }
   p.max_degree = maxd;
   p.mean_degree = m ? double(host_rp[m]) / m : 0.0;
+  p.sh = make_shapes(p.o, p.a.n_cols, p.n, p.device, p.mean_degree);
+  const uint32_t sw = p.sh.slice_w;
   std::vector<uint32_t> count(size_t(maxd) + 2, 0);
   for (uint32_t r = 0; r < m; ++r) ++count[maxd - deg[r]];
   uint64_t acc = 0;
@@ -310,8 +316,10 @@ gespmm_status_t build_tuned(Plan& p, const uint32_t* host_rp, cudaStream_t st) {
   while (n_hub < m && deg[order[n_hub]] >= p.hub_threshold) ++n_hub;
   p.n_hub = n_hub;
 
-
-  if (m) {
+  // Rows of at most two staged chunks gain nothing from the LPT schedule:
+  // the identity order saves the schedule load in front of every row.
+  const bool identity = n_hub == 0 && maxd <= 64;
+  if (m && !identity) {
     GESPMM_CUDA(cudaMalloc(reinterpret_cast<void**>(&p.d_order), sizeof(uint32_t) * m),
                 "plan_create");
     GESPMM_CUDA(cudaMemcpyAsync(p.d_order, order.data(), sizeof(uint32_t) * m,
@@ -343,6 +351,10 @@ gespmm_status_t build_tuned(Plan& p, const uint32_t* host_rp, cudaStream_t st) {
                   "; l2 hot map %.0f MB: %llu cols (gathered>=%u) = %.1f%% of gathers",
                   double(hot_budget) / 1e6, (unsigned long long)p.hot.hot_cols, p.hot.threshold,
                   100.0 * p.hot.hot_nnz_frac);
+  len = int(std::strlen(buf));
+  if (size_t(len) < sizeof buf)
+    std::snprintf(buf + len, sizeof buf - size_t(len), "; %s",
+                  identity ? "identity order" : "degree-sorted (LPT) order");
   len = int(std::strlen(buf));
   if (p.sh.slices > 1 && size_t(len) < sizeof buf)
     std::snprintf(buf + len, sizeof buf - size_t(len), "; %u column slices of %u", p.sh.slices, sw);
@@ -765,7 +777,7 @@ gespmm_status_t gespmm_spmm_host(const gespmm_csr_t* a, const float* b, uint32_t
   if (tuned) {
     int dev = 0;
     GESPMM_CUDA(cudaGetDevice(&dev), "spmm");
-    shapes = make_shapes(o, a->n_cols, n, dev);
+    shapes = make_shapes(o, a->n_cols, n, dev, m ? double(nnz) / double(m) : 0.0);
     const int32_t ht = o.hub_threshold;
     const uint32_t hub_t =
         ht > 0 ? uint32_t(ht) : (ht < 0 ? 0xffffffffu : auto_hub_threshold(shapes.slice_w, nnz));

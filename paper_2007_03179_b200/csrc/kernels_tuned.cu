@@ -19,6 +19,8 @@
 //   cannot.
 #include <algorithm>
 #include <mutex>
+#include <utility>
+#include <vector>
 
 #include "common.cuh"
 #include "launch.h"
@@ -52,47 +54,73 @@ constexpr int kWarpBlock = 4;  // warps per CTA: 72-register kernel -> 7 CTAs = 
 // (85 registers; 4 at CF=4) instead of spilling under the 7-CTA cap.
 template <int OP, int CF>
 constexpr int warp_min_blocks() {
-  return Reduce<OP>::kHasArg ? (CF >= 4 ? 4 : 6) : 7;
+  return Reduce<OP>::kHasArg ? (CF >= 4 ? 4 : 6) : (CF >= 4 ? 6 : 7);
 }
 
+template <int LPR, int CF>
+struct WarpGeom {
+  static constexpr int RPW = 32 / LPR;                     // rows per warp
+  static constexpr int U0 = 8 / CF;
+  static constexpr int U = U0 < LPR ? U0 : LPR;            // gather batch; LPR % U == 0
+  static constexpr int W = U < 4 ? U : 4;                  // LDS width (entries per read)
+  static_assert(LPR % U == 0 && U % W == 0, "batch geometry");
+};
+
+// Row metadata of one (sub)warp unit for this lane: the row, its CSR range,
+// and this lane's entry of the row's first staged chunk.
+struct UnitMeta {
+  uint32_t row, start, full_end;
+  uint32_t k0;
+  float v0;
+  bool row_ok;
+};
+
+template <int LPR>
+__device__ __forceinline__ void unit_rows(const SpmmArgs& a, uint32_t group, UnitMeta& m) {
+  const uint32_t sidx = group * (32 / LPR) + (threadIdx.x & 31) / LPR;
+  m.row_ok = sidx < a.n_sched;
+  m.row = m.row_ok ? (a.order ? a.order[sidx] : sidx) : 0u;
+  m.start = m.full_end = 0;
+  if (m.row_ok) {
+    m.start = a.row_ptr[m.row];
+    m.full_end = a.row_ptr[m.row + 1];
+  }
+}
+
+// Issues this lane's chunk-0 (col, val) loads; slots past the row end hold
+// column 0 (a valid row).
+template <int LPR, bool HOT>
+__device__ __forceinline__ void unit_chunk0(const SpmmArgs& a, const Policies& pol, UnitMeta& m) {
+  const uint32_t sl = (threadIdx.x & 31) % LPR;
+  const uint32_t len = faulted_end(m.start, m.full_end, a.skip_tail) - m.start;
+  m.k0 = 0;
+  m.v0 = 0.0f;
+  if (sl < len) {
+    m.k0 = ld_stream_u32(a.col_ind + m.start + sl, pol.stream);
+    m.v0 = ld_stream_f32(a.vals + m.start + sl, pol.stream);
+    if (HOT) m.k0 |= cold_mark(a.hot, m.k0);
+  }
+}
+
+// One (row group, column tile) unit: Coalesced Row Caching of the row's
+// sparse segment through the per-warp double-buffered shared tile, CF column
+// sub-tiles per lane (warp merging), U gathers in flight, ordered fold.
 // HOT: the plan carries a hot-column map (bit 31 of a staged column marks a
 // cold B row, loaded with the cold policy).  Without it every gather uses one
 // policy register, so no per-load descriptor selection is emitted.
 template <int OP, bool FAST, int VEC, int LPR, int CF, bool HOT>
-__global__ void __launch_bounds__(32 * kWarpBlock, warp_min_blocks<OP, CF>()) k_warp(SpmmArgs a) {
+__device__ __forceinline__ void warp_unit(const SpmmArgs& a, const Policies& pol, uint32_t tile,
+                                          const UnitMeta& m, uint32_t* my_col, float* my_val) {
   using R = Reduce<OP>;
-  constexpr int RPW = 32 / LPR;                     // rows per warp
-  constexpr int U0 = 8 / CF;
-  constexpr int U = U0 < LPR ? U0 : LPR;            // gather batch; LPR % U == 0
-  constexpr int W = U < 4 ? U : 4;                  // LDS width (entries per read)
+  using G = WarpGeom<LPR, CF>;
+  constexpr int RPW = G::RPW, U = G::U, W = G::W;
   constexpr uint32_t SUB = uint32_t(VEC * LPR);     // columns per sub-tile
   constexpr uint32_t TW = SUB * CF;                 // columns per tile
-  static_assert(LPR % U == 0 && U % W == 0, "batch geometry");
-  // Staged sparse tile, double-buffered per warp: phase 1 writes one (col, val)
-  // per lane, phase 2 reads them back with broadcast LDS of W entries — 2/W
-  // shared-pipe wavefronts per nonzero instead of two shuffles.
-  __shared__ __align__(16) uint32_t s_col[kWarpBlock][2][32];
-  __shared__ __align__(16) float s_val[kWarpBlock][2][32];
-
   const uint32_t lane = threadIdx.x & 31;
-  const uint32_t wib = threadIdx.x >> 5;
-  const uint64_t unit = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  const uint64_t groups = (uint64_t(a.n_sched) + RPW - 1) / RPW;
-  if (unit >= groups * a.n_tiles) return;  // warp-uniform exit
-  const Policies pol = args_policies(a);
-
-  const uint32_t group = uint32_t(unit / a.n_tiles);
-  const uint32_t tile = uint32_t(unit % a.n_tiles);
   const uint32_t sub = lane / LPR;
   const uint32_t sl = lane % LPR;
-  const uint32_t sidx = group * RPW + sub;
-  const bool row_ok = sidx < a.n_sched;
-  const uint32_t row = row_ok ? (a.order ? a.order[sidx] : sidx) : 0u;
-  uint32_t start = 0, full_end = 0;
-  if (row_ok) {
-    start = a.row_ptr[row];
-    full_end = a.row_ptr[row + 1];
-  }
+  const bool row_ok = m.row_ok;
+  const uint32_t row = m.row, start = m.start, full_end = m.full_end;
   const uint32_t len = faulted_end(start, full_end, a.skip_tail) - start;
   const uint32_t maxlen = RPW == 1 ? len : __reduce_max_sync(kFull, len);
 
@@ -118,21 +146,10 @@ __global__ void __launch_bounds__(32 * kWarpBlock, warp_min_blocks<OP, CF>()) k_
   const uint32_t stride = a.ld * 4u;  // bytes per B row (B < 4 GiB per row index * stride)
   const uint32_t* ci = a.col_ind + start;
   const float* vs = a.vals + start;
-  uint32_t* my_col = &s_col[wib][0][0];
-  float* my_val = &s_val[wib][0][0];
 
-  // phase 1 of chunk 0; slots past the row end hold column 0 (a valid row)
-  {
-    uint32_t k0 = 0;
-    float v0 = 0.0f;
-    if (sl < len) {
-      k0 = ld_stream_u32(ci + sl, pol.stream);
-      v0 = ld_stream_f32(vs + sl, pol.stream);
-      if (HOT) k0 |= cold_mark(a.hot, k0);
-    }
-    my_col[lane] = k0;
-    my_val[lane] = v0;
-  }
+  __syncwarp();  // the previous unit's reads of the tile are done
+  my_col[lane] = m.k0;  // phase 1 of chunk 0
+  my_val[lane] = m.v0;
   uint32_t buf = 0;
   for (uint32_t off = 0; off < maxlen; off += LPR) {
     // issue the next chunk's sparse loads before consuming this one
@@ -220,6 +237,36 @@ __global__ void __launch_bounds__(32 * kWarpBlock, warp_min_blocks<OP, CF>()) k_
     st_stream<VEC>(a.c + o, out, pol.stream);
     if (R::kHasArg && a.arg) st_stream_i32<VEC>(a.arg + o, who[c], pol.stream);
   }
+}
+
+template <int OP, bool FAST, int VEC, int LPR, int CF, bool HOT>
+__global__ void __launch_bounds__(32 * kWarpBlock, warp_min_blocks<OP, CF>()) k_warp(SpmmArgs a) {
+  // Staged sparse tile, double-buffered per warp: phase 1 writes one (col, val)
+  // per lane, phase 2 reads them back with broadcast LDS of W entries — 2/W
+  // shared-pipe wavefronts per nonzero instead of two shuffles.
+  __shared__ __align__(16) uint32_t s_col[kWarpBlock][2][32];
+  __shared__ __align__(16) float s_val[kWarpBlock][2][32];
+  const uint32_t wib = threadIdx.x >> 5;
+  const uint64_t unit = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t groups = (uint64_t(a.n_sched) + WarpGeom<LPR, CF>::RPW - 1) / WarpGeom<LPR, CF>::RPW;
+  if (unit >= groups * a.n_tiles) return;  // warp-uniform exit
+  const Policies pol = args_policies(a);
+  // (group, tile) without a 64-bit division in the common cases
+  uint32_t group, tile;
+  if (a.n_tiles == 1) {
+    group = uint32_t(unit);
+    tile = 0;
+  } else if (unit <= 0xffffffffull) {
+    group = uint32_t(unit) / a.n_tiles;
+    tile = uint32_t(unit) - group * a.n_tiles;
+  } else {
+    group = uint32_t(unit / a.n_tiles);
+    tile = uint32_t(unit % a.n_tiles);
+  }
+  UnitMeta m;
+  unit_rows<LPR>(a, group, m);
+  unit_chunk0<LPR, HOT>(a, pol, m);
+  warp_unit<OP, FAST, VEC, LPR, CF, HOT>(a, pol, tile, m, &s_col[wib][0][0], &s_val[wib][0][0]);
 }
 
 template <int OP, bool FAST, int VEC, int WARPS>
@@ -345,16 +392,20 @@ cudaError_t warp_dispatch(const WarpShape& s, const SpmmArgs& a, cudaStream_t st
   const uint64_t blocks = (warps + kWarpBlock - 1) / kWarpBlock;
   if (blocks == 0) return cudaSuccess;
   if (blocks > 0x7fffffffull) return cudaErrorInvalidConfiguration;
-  const dim3 g{uint32_t(blocks)}, b{32 * kWarpBlock};
-#define GESPMM_W(V, L, F)                                                              \
-  if (s.vec == V && s.lpr == L && s.cf == F) {                                         \
-    const cudaError_t e = a.hot ? launch_ex(k_warp<OP, FAST, V, L, F, true>, g, b, st, a, window) \
-                                : launch_ex(k_warp<OP, FAST, V, L, F, false>, g, b, st, a, window); \
-    note_launch();                                                                     \
-    return e;                                                                          \
+  const dim3 b{32 * kWarpBlock};
+#define GESPMM_W(V, L, F)                                                                    \
+  if (s.vec == V && s.lpr == L && s.cf == F) {                                               \
+    constexpr bool kHotShape = L == 32; /* hot-column map on full-warp rows only */          \
+    const dim3 g{uint32_t(blocks)};                                                          \
+    const cudaError_t e =                                                                    \
+        (kHotShape && a.hot) ? launch_ex(k_warp<OP, FAST, V, L, F, kHotShape>, g, b, st, a, window) \
+                             : launch_ex(k_warp<OP, FAST, V, L, F, false>, g, b, st, a, window); \
+    note_launch();                                                                           \
+    return e;                                                                                \
   }
   GESPMM_W(4, 4, 1) GESPMM_W(4, 8, 1) GESPMM_W(4, 16, 1) GESPMM_W(4, 32, 1)
   GESPMM_W(4, 32, 2) GESPMM_W(4, 32, 4)
+  GESPMM_W(4, 4, 2) GESPMM_W(4, 8, 2) GESPMM_W(4, 8, 4) GESPMM_W(4, 16, 2) GESPMM_W(4, 16, 4)
   GESPMM_W(2, 32, 1) GESPMM_W(2, 32, 2) GESPMM_W(2, 32, 4)
   GESPMM_W(1, 1, 1) GESPMM_W(1, 2, 1) GESPMM_W(1, 4, 1) GESPMM_W(1, 8, 1)
   GESPMM_W(1, 16, 1) GESPMM_W(1, 32, 1) GESPMM_W(1, 32, 2) GESPMM_W(1, 32, 4)
@@ -427,7 +478,8 @@ cudaError_t resolve_policies(SpmmArgs* a, cudaStream_t st) {
 
 bool tuned_shape_supported(const WarpShape& s) {
   static const int table[][3] = {{4, 4, 1},  {4, 8, 1},  {4, 16, 1}, {4, 32, 1}, {4, 32, 2},
-                                 {4, 32, 4}, {2, 32, 1}, {2, 32, 2}, {2, 32, 4}, {1, 1, 1},
+                                 {4, 32, 4}, {4, 4, 2},  {4, 8, 2},  {4, 8, 4},  {4, 16, 2},
+                                 {4, 16, 4}, {2, 32, 1}, {2, 32, 2}, {2, 32, 4}, {1, 1, 1},
                                  {1, 2, 1},  {1, 4, 1},  {1, 8, 1},  {1, 16, 1}, {1, 32, 1},
                                  {1, 32, 2}, {1, 32, 4}};
   for (const auto& t : table)
@@ -438,11 +490,26 @@ bool tuned_shape_supported(const WarpShape& s) {
 // N -> (VEC, LPR, CF): the smallest sub-warp whose VEC-wide lanes cover N
 // (several short rows per warp when N < 128), then the CWM merge factor so a
 // warp covers up to 4 sub-tiles of one row before the row is re-staged.
-WarpShape pick_warp_shape(uint32_t n, bool vec4_ok, bool vec2_ok) {
+// rows_per_warp > 1 (low-degree matrices, where the per-row prologue and
+// epilogue outweigh the few gathers of a row): float4 lanes only, LPR shrunk
+// so that several rows share a warp, each lane covering up to 4 sub-tiles.
+WarpShape pick_warp_shape(uint32_t n, bool vec4_ok, bool vec2_ok, int rows_per_warp) {
   WarpShape s;
   s.vec = vec4_ok ? 4 : (vec2_ok ? 2 : 1);
   if (n < 16 || (s.vec == 2 && n < 64)) s.vec = 1;  // narrow rows: scalar lanes waste less
   const uint32_t lanes = (n + uint32_t(s.vec) - 1) / uint32_t(s.vec);
+  if (rows_per_warp > 1 && s.vec == 4 && lanes >= 8 && lanes <= 64) {
+    uint32_t lpr = 32u / uint32_t(rows_per_warp);
+    lpr = std::max<uint32_t>(4, std::min<uint32_t>(16, lpr));
+    while (lanes > lpr * 4u) lpr *= 2;  // CF <= 4
+    uint32_t cf = (lanes + lpr - 1) / lpr;
+    cf = cf >= 4 ? 4 : (cf >= 2 ? 2 : 1);
+    WarpShape t;
+    t.vec = 4;
+    t.lpr = int(lpr);
+    t.cf = int(cf);
+    if (lpr < 32 && tuned_shape_supported(t)) return t;
+  }
   if (lanes >= 32) {
     s.lpr = 32;
     const uint32_t sub = 32u * uint32_t(s.vec);

@@ -46,7 +46,7 @@ struct CtaShape {
 };
 
 bool tuned_shape_supported(const WarpShape& s);
-WarpShape pick_warp_shape(uint32_t n, bool vec4_ok, bool vec2_ok);
+WarpShape pick_warp_shape(uint32_t n, bool vec4_ok, bool vec2_ok, int rows_per_warp = 1);
 // `window` (nullable): L2 access-policy window attached to the launch.
 cudaError_t launch_tuned_warp(const WarpShape& s, int op, bool fast, const SpmmArgs& a,
                               cudaStream_t st, const cudaAccessPolicyWindow* window = nullptr);

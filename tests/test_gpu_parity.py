@@ -409,3 +409,24 @@ def test_column_slices_keep_bits(slices, n, cuda):
             assert first_divergence(c.data, want) is None, (op, ht)
             if want_arg:
                 assert np.array_equal(arg, warg), (op, ht)
+
+
+@pytest.mark.parametrize("rpw", [2, 4, 8])
+@pytest.mark.parametrize("n", [32, 64, 100, 128, 200, 256])
+def test_rows_per_warp_shapes_keep_bits(rpw, n, cuda):
+    """Multi-row warp shapes for low-degree matrices ((4,4,2) ... (4,16,4)): every
+    op with args, bit-identical, incl. ragged N and power-law rows spanning many
+    chunks (degree-sorted schedule) and low-degree rows (identity schedule)."""
+    pl = _powerlaw(3000, 60000, 2000, 17 + n, n)
+    un = G.gen_uniform_random(G.GraphGenSpec(5000, 20000, 7))
+    G.randomize_values(un, 8)
+    for a, b in (pl, (un, G.make_random_dense(5000, n, 9))):
+        for op in OPS:
+            want_arg = op in ("max", "min")
+            want, warg = _oracle(a, b, op, want_arg)
+            ex = G.ExecOptions(rows_per_warp=rpw)
+            c, arg = G.native_spmm_arg(a, b, G.KernelVariant.tuned(), G.reduce_op_by_name(op),
+                                       exec=ex, want_arg=want_arg)
+            assert first_divergence(c.data, want) is None, (op, a.n_rows)
+            if want_arg:
+                assert np.array_equal(arg, warg), (op, a.n_rows)
