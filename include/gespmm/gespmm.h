@@ -153,6 +153,52 @@ const char* gespmm_plan_describe(gespmm_plan_t plan);
 int32_t gespmm_plan_launches(gespmm_plan_t plan);
 void gespmm_plan_destroy(gespmm_plan_t plan);
 
+/* ---- multi-GPU: fused all-gather epilogue over peer memory ---------------- */
+/* Row-sharded stacked layers: each rank computes the rows
+ * of its nnz-balanced shard and every rank needs all rows for the next layer.
+ * Instead of a kernel followed by ncclAllGather, the SpMM's epilogue stores
+ * each finished output row into every rank's full-height buffer directly —
+ * peer-mapped device pointers (CUDA IPC / symmetric memory: NVLink P2P stores
+ * through NVSwitch) and/or one NVLS multicast address (multimem.st, the
+ * switch replicates the store) — so the exchange overlaps the gathers row by
+ * row.  A cross-rank barrier (gespmm_peer_barrier) orders the next layer's
+ * reads after every rank's stores.  Results are the plan's, bit for bit. */
+#define GESPMM_MAX_GATHER_DSTS 8
+
+/* Executes a TUNED plan with replicated outputs.  c_dsts[0] is the local C (as
+ * gespmm_plan_execute's c); c_dsts[1..n_dsts) are replicas on other ranks,
+ * each pointing at the element where THIS shard's row 0 lands (the caller adds
+ * the shard's row offset * n).  arg_dsts: same for arg (NULL, or entries may
+ * be NULL).  c_multicast / arg_multicast: multicast addresses of the same
+ * landing element (NULL: unused); with a multicast address the replicas list
+ * may hold only the local C.  1 <= n_dsts <= GESPMM_MAX_GATHER_DSTS.
+ * Asynchronous; no ordering with other ranks (see gespmm_peer_barrier). */
+gespmm_status_t gespmm_plan_execute_gather(gespmm_plan_t plan, const float* b,
+                                           float* const* c_dsts, int32_t* const* arg_dsts,
+                                           int32_t n_dsts, float* c_multicast,
+                                           int32_t* arg_multicast, void* stream);
+
+/* Cross-rank barrier on `stream` over peer-mapped signal words: signals[p] is
+ * rank p's array of `world` u32 words as mapped in this process (signals[rank]
+ * is the local one).  Rank r stores `epoch` to signals[p][r] for every p with
+ * release semantics at system scope (after a system-scope fence, so every
+ * store this rank made before it — the gather epilogue included — is visible
+ * first), then waits until signals[r][p] == epoch for every p with acquire
+ * loads.  epoch must differ from the previous barrier's (a counter).  A wait
+ * longer than timeout_ms (0 = 60000) abandons the barrier and sets *error
+ * (device int32, nullable) to 1 instead of hanging the device. */
+gespmm_status_t gespmm_peer_barrier(uint32_t* const* signals, int32_t rank, int32_t world,
+                                    uint32_t epoch, uint32_t timeout_ms, int32_t* error,
+                                    void* stream);
+
+/* Peer-shareable device buffers (cudaMalloc base pointers, so a CUDA IPC handle
+ * maps exactly the buffer) and their IPC handles (64 opaque bytes). */
+gespmm_status_t gespmm_peer_alloc(uint64_t bytes, void** out);
+gespmm_status_t gespmm_peer_free(void* ptr);
+gespmm_status_t gespmm_ipc_get_handle(void* ptr, unsigned char out[64]);
+gespmm_status_t gespmm_ipc_open_handle(const unsigned char handle[64], void** out);
+gespmm_status_t gespmm_ipc_close(void* ptr);
+
 /* ---- format helpers ------------------------------------------------------ */
 
 /* A^T of a device CSR, as canonical CSR on the device: t_row_ptr[n_cols+1],

@@ -38,8 +38,11 @@ EXPORTS = [
     "gespmm_device_info", "gespmm_launch_count", "gespmm_diag_gather",
     "gespmm_csr_transpose_device", "gespmm_validate_device_as", "gespmm_csr1_write",
     "gespmm_csr1_header", "gespmm_csr1_read_host", "gespmm_csr1_load_device",
-    "gespmm_diag_gather_hub", "gespmm_diag_gather_mode",
+    "gespmm_diag_gather_hub", "gespmm_diag_gather_mode", "gespmm_plan_execute_gather",
+    "gespmm_peer_barrier", "gespmm_peer_alloc", "gespmm_peer_free", "gespmm_ipc_get_handle",
+    "gespmm_ipc_open_handle", "gespmm_ipc_close",
 ]
+MAX_GATHER_DSTS = 8
 
 
 class Csr(C.Structure):
@@ -148,6 +151,20 @@ def lib():
         L.gespmm_csr1_read_host.restype = C.c_int
         L.gespmm_csr1_load_device.argtypes = [C.c_char_p, vp, vp, vp, i32, vp]
         L.gespmm_csr1_load_device.restype = C.c_int
+        L.gespmm_plan_execute_gather.argtypes = [vp, vp, vp, vp, i32, vp, vp, vp]
+        L.gespmm_plan_execute_gather.restype = C.c_int
+        L.gespmm_peer_barrier.argtypes = [vp, i32, i32, u32, u32, vp, vp]
+        L.gespmm_peer_barrier.restype = C.c_int
+        L.gespmm_peer_alloc.argtypes = [u64, C.POINTER(vp)]
+        L.gespmm_peer_alloc.restype = C.c_int
+        L.gespmm_peer_free.argtypes = [vp]
+        L.gespmm_peer_free.restype = C.c_int
+        L.gespmm_ipc_get_handle.argtypes = [vp, C.c_char_p]
+        L.gespmm_ipc_get_handle.restype = C.c_int
+        L.gespmm_ipc_open_handle.argtypes = [C.c_char_p, C.POINTER(vp)]
+        L.gespmm_ipc_open_handle.restype = C.c_int
+        L.gespmm_ipc_close.argtypes = [vp]
+        L.gespmm_ipc_close.restype = C.c_int
         L.gespmm_launch_count.argtypes = []
         L.gespmm_launch_count.restype = u64
         _lib = L

@@ -623,6 +623,22 @@ class Plan:
                                          _stream_ptr(stream)))
         return c
 
+    def execute_gather(self, b, c_dsts, arg_dsts=None, c_multicast=None, arg_multicast=None,
+                       stream=None):
+        """gespmm_plan_execute_gather: the plan's SpMM with its output rows also
+        stored into replicas (fused all-gather epilogue).  ``c_dsts`` are raw
+        device addresses (ints) of where this shard's row 0 lands, local first;
+        ``arg_dsts`` likewise for max/min arg (or None)."""
+        k = len(c_dsts)
+        cd = (C.c_void_p * k)(*[int(x) for x in c_dsts])
+        ad = None
+        if arg_dsts is not None:
+            ad = (C.c_void_p * k)(*[int(x) if x else None for x in arg_dsts])
+        _check(lib().gespmm_plan_execute_gather(self._h, b.data_ptr(), cd, ad, k,
+                                                int(c_multicast) if c_multicast else None,
+                                                int(arg_multicast) if arg_multicast else None,
+                                                _stream_ptr(stream)))
+
     def close(self):
         if getattr(self, "_h", None):
             lib().gespmm_plan_destroy(self._h)

@@ -172,10 +172,24 @@ namespace {
 // moves 4x more load instructions per byte and competes for the same SMs).
 // A warp sustains ~1/3500 of the chip's gather rate, so a row is a tail risk
 // only beyond ~nnz/1024 nonzeros.
-uint32_t auto_hub_threshold(uint32_t n, uint64_t nnz) {
-  if (n < 64) return 0xffffffffu;  // the CTA split needs >= 2 warps of columns
-  const uint64_t t = std::max<uint64_t>(65536, nnz / 1024);
-  return t >= 0xffffffffull ? 0xffffffffu : uint32_t(t);
+// Hub rows: a row of degree d on one warp costs ~d * L * CF / 8 (one L2 round
+// trip L ~ 0.7 us per batch of 8/CF gathers), while a launch over `nnz`
+// nonzeros is gather-bound at ~nnz * 4N / 19 TB/s.  Rows whose single-warp
+// time would exceed 1/1.5 of the launch go to the ring-fed row-per-CTA kernel
+// (k_hub: a 21,657-nonzero row in ~0.3 ms instead of ~1.7 ms).  So the
+// threshold scales with the work per launch: none on the whole Reddit shape
+// (23.6k > max degree), ~11.8k on a 1/2 row shard, ~2.9k on a 1/8 shard or
+// one block of the pipelined host entry.  Measured with
+// tools/shard_emulation.py (profiles/r1_shard_emulation.md): factor 1.5 keeps
+// the 1-GPU step unchanged and halves the 8-shard step (1.51 -> 0.79 ms).
+uint32_t auto_hub_threshold(uint32_t n, uint64_t nnz, int cf) {
+  if (n < 64) return 0xffffffffu;  // narrow rows: one warp already covers the row cheaply
+  const double t_launch = double(nnz) * 4.0 * double(n) / 19e12;
+  const double t_nnz = 0.7e-6 * double(cf < 1 ? 1 : cf) / 8.0;
+  double f = 1.5;  // GESPMM_HUB_FACTOR: tuning experiments (tools/shard_emulation.py)
+  if (const char* e = std::getenv("GESPMM_HUB_FACTOR")) f = std::max(0.05, std::atof(e));
+  const double t = std::max(2048.0, t_launch / (f * t_nnz));
+  return t >= 4294967295.0 ? 0xffffffffu : uint32_t(t);
 }
 
 // Frequency-aware L2 policy budget (bytes of B rows kept evict_last), 0 = off.
@@ -260,19 +274,32 @@ gespmm_status_t launch_tuned_rows(const TunedShapes& t, int op, bool fast, const
     sa.b = a.b + off;
     sa.c = a.c + off;
     sa.arg = a.arg ? a.arg + off : nullptr;
+    for (int q = 0; q < a.n_peer; ++q) {
+      sa.c_peer[q] = a.c_peer[q] + off;
+      sa.arg_peer[q] = a.arg_peer[q] ? a.arg_peer[q] + off : nullptr;
+    }
+    sa.c_mc = a.c_mc ? a.c_mc + off : nullptr;
+    sa.arg_mc = a.arg_mc ? a.arg_mc + off : nullptr;
     sa.n = w;
     if (n_hub) {
       SpmmArgs h = sa;
       h.order = order;
       h.n_sched = n_hub;
-      const uint32_t tw = uint32_t(cs.vec * cs.warps * 32);
+      // TMA-ring hub kernel when bulk copies can address the B slices (16-byte
+      // units: N % 4 == 0, ld % 4 == 0, 16-byte aligned B/C/arg at this offset)
+      const bool tma = w % 4 == 0 && a.ld % 4 == 0 && aligned(sa.b, 16) && aligned(sa.c, 16) &&
+                       (!sa.arg || aligned(sa.arg, 16));
+      const uint32_t tw = tma ? hub_tile_width(w, n_hub) : uint32_t(cs.vec * cs.warps * 32);
       h.n_tiles = (w + tw - 1) / tw;
       cudaStream_t hs = side ? side : st;
       if (side) {
         GESPMM_CUDA(cudaEventRecord(fork, st), "spmm");
         GESPMM_CUDA(cudaStreamWaitEvent(side, fork, 0), "spmm");
       }
-      GESPMM_CUDA(launch_tuned_cta(cs, op, fast, h, hs), "spmm");
+      if (tma)
+        GESPMM_CUDA(launch_tuned_hub(op, fast, h, hs), "spmm");
+      else
+        GESPMM_CUDA(launch_tuned_cta(cs, op, fast, h, hs), "spmm");
       if (side) GESPMM_CUDA(cudaEventRecord(join, side), "spmm");
     }
     sa.order = order + n_hub;
@@ -311,7 +338,8 @@ gespmm_status_t build_tuned(Plan& p, const uint32_t* host_rp, cudaStream_t st) {
   for (uint32_t r = 0; r < m; ++r) order[count[maxd - deg[r]]++] = r;
 
   const int32_t ht = p.o.hub_threshold;
-  p.hub_threshold = ht > 0 ? uint32_t(ht) : (ht < 0 ? 0xffffffffu : auto_hub_threshold(sw, host_rp[m]));
+  p.hub_threshold = ht > 0 ? uint32_t(ht)
+                           : (ht < 0 ? 0xffffffffu : auto_hub_threshold(sw, host_rp[m], p.sh.warp_v.cf));
   uint32_t n_hub = 0;
   while (n_hub < m && deg[order[n_hub]] >= p.hub_threshold) ++n_hub;
   p.n_hub = n_hub;
@@ -328,7 +356,11 @@ gespmm_status_t build_tuned(Plan& p, const uint32_t* host_rp, cudaStream_t st) {
     GESPMM_CUDA(cudaStreamSynchronize(st), "plan_create");
   }
   if (n_hub) {
-    GESPMM_CUDA(cudaStreamCreateWithFlags(&p.side, cudaStreamNonBlocking), "plan_create");
+    // hub rows are the critical path: their CTAs dispatch ahead of the warp
+    // kernel's whenever an SM frees up
+    int lo_prio = 0, hi_prio = 0;
+    cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio);
+    GESPMM_CUDA(cudaStreamCreateWithPriority(&p.side, cudaStreamNonBlocking, hi_prio), "plan_create");
     GESPMM_CUDA(cudaEventCreateWithFlags(&p.ev_fork, cudaEventDisableTiming), "plan_create");
     GESPMM_CUDA(cudaEventCreateWithFlags(&p.ev_join, cudaEventDisableTiming), "plan_create");
   }
@@ -430,7 +462,7 @@ PersistLimits persist_limits(int dev) {
 }
 
 gespmm_status_t plan_execute_impl(Plan& p, const float* b, float* c, int32_t* arg,
-                                  cudaStream_t st) {
+                                  cudaStream_t st, const SpmmArgs* rep = nullptr) {
   gespmm_status_t s = check_op(p.op, arg);
   if (s != GESPMM_OK) return s;
   if (p.a.n_rows == 0) return GESPMM_OK;
@@ -446,6 +478,15 @@ gespmm_status_t plan_execute_impl(Plan& p, const float* b, float* c, int32_t* ar
   args.skip_tail = p.o.fault_skip_tail;
   args.hints = p.o.l2_hints;
   args.hot = p.d_hot;
+  if (rep) {  // fused all-gather epilogue (tuned plans only, checked by the caller)
+    args.n_peer = rep->n_peer;
+    for (int q = 0; q < rep->n_peer; ++q) {
+      args.c_peer[q] = rep->c_peer[q];
+      args.arg_peer[q] = rep->arg_peer[q];
+    }
+    args.c_mc = rep->c_mc;
+    args.arg_mc = rep->arg_mc;
+  }
   const bool fast = p.o.exact == 0;
   if (p.o.variant != GESPMM_VARIANT_TUNED) {
     args.order = nullptr;
@@ -518,9 +559,11 @@ constexpr int kMaxChunks = 16;
 struct Workspace {
   std::mutex mu;
   cudaStream_t stream = nullptr, in = nullptr, out = nullptr;
+  cudaStream_t side = nullptr;  // hub-row kernels next to the warp kernel of a block
   cudaEvent_t ev_b = nullptr, ev_in[kMaxChunks] = {}, ev_done[kMaxChunks] = {};
-  void* buf[7] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
-  size_t cap[7] = {0, 0, 0, 0, 0, 0, 0};
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  void* buf[8] = {};   // row_ptr, col_ind, vals, B, C, arg, order, validation scratch
+  size_t cap[8] = {};
   cudaError_t reserve(int i, size_t bytes) {
     if (bytes <= cap[i]) return cudaSuccess;
     if (buf[i]) cudaFree(buf[i]);
@@ -543,6 +586,11 @@ Workspace* workspace() {
     cudaStreamCreateWithFlags(&w->stream, cudaStreamNonBlocking);
     cudaStreamCreateWithFlags(&w->in, cudaStreamNonBlocking);
     cudaStreamCreateWithFlags(&w->out, cudaStreamNonBlocking);
+    int lo_prio = 0, hi_prio = 0;
+    cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio);
+    cudaStreamCreateWithPriority(&w->side, cudaStreamNonBlocking, hi_prio);
+    cudaEventCreateWithFlags(&w->ev_fork, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&w->ev_join, cudaEventDisableTiming);
     cudaEventCreateWithFlags(&w->ev_b, cudaEventDisableTiming);
     for (int i = 0; i < kMaxChunks; ++i) {
       cudaEventCreateWithFlags(&w->ev_in[i], cudaEventDisableTiming);
@@ -566,6 +614,27 @@ struct Trace {
     if (!on) return;
     const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
     std::fprintf(stderr, "[gespmm] %8.3f ms  %s\n", ms, what);
+  }
+  // device timeline: timing events recorded on the streams, printed by dump()
+  // relative to the first one (after the streams are synchronised)
+  mutable std::vector<std::pair<std::string, cudaEvent_t>> ev;
+  void dev(const std::string& what, cudaStream_t s) const {
+    if (!on) return;
+    cudaEvent_t e = nullptr;
+    if (cudaEventCreate(&e) != cudaSuccess) return;
+    cudaEventRecord(e, s);
+    ev.emplace_back(what, e);
+  }
+  void dump() const {
+    if (!on) return;
+    for (auto& [what, e] : ev) {
+      float ms = 0.0f;
+      cudaEventSynchronize(e);
+      cudaEventElapsedTime(&ms, ev.front().second, e);
+      std::fprintf(stderr, "[gespmm] device %8.3f ms  %s\n", ms, what.c_str());
+    }
+    for (auto& pr : ev) cudaEventDestroy(pr.second);
+    ev.clear();
   }
 };
 
@@ -645,6 +714,41 @@ gespmm_status_t gespmm_plan_execute(gespmm_plan_t plan, const float* b, float* c
   if (!plan) return fail(GESPMM_EINVAL, "null plan");
   return plan_execute_impl(*reinterpret_cast<Plan*>(plan), b, c, arg,
                            static_cast<cudaStream_t>(stream));
+}
+
+gespmm_status_t gespmm_plan_execute_gather(gespmm_plan_t plan, const float* b,
+                                           float* const* c_dsts, int32_t* const* arg_dsts,
+                                           int32_t n_dsts, float* c_multicast,
+                                           int32_t* arg_multicast, void* stream) {
+  if (!plan || !c_dsts) return fail(GESPMM_EINVAL, "null argument");
+  Plan& p = *reinterpret_cast<Plan*>(plan);
+  if (n_dsts < 1 || n_dsts > GESPMM_MAX_GATHER_DSTS)
+    return fail(GESPMM_EINVAL, "gather: n_dsts must be in [1, " +
+                                   std::to_string(GESPMM_MAX_GATHER_DSTS) + "]");
+  if (p.o.variant != GESPMM_VARIANT_TUNED)
+    return fail(GESPMM_EUNSUPPORTED, "gather: the fused all-gather epilogue needs a tuned plan");
+  const bool has_arg = p.op == GESPMM_MAX || p.op == GESPMM_MIN;
+  int32_t* arg0 = (arg_dsts && has_arg) ? arg_dsts[0] : nullptr;
+  SpmmArgs rep{};
+  rep.n_peer = n_dsts - 1;
+  for (int q = 1; q < n_dsts; ++q) {
+    if (!c_dsts[q]) return fail(GESPMM_EINVAL, "gather: null destination");
+    // replicas share the local C's alignment class, so the chosen vector
+    // width is valid for every destination
+    if ((reinterpret_cast<uintptr_t>(c_dsts[q]) ^ reinterpret_cast<uintptr_t>(c_dsts[0])) % 16)
+      return fail(GESPMM_EINVAL, "gather: destinations must share the local C's 16-byte alignment");
+    rep.c_peer[q - 1] = c_dsts[q];
+    rep.arg_peer[q - 1] = (arg_dsts && has_arg) ? arg_dsts[q] : nullptr;
+    if (rep.arg_peer[q - 1] && (!arg0 || (reinterpret_cast<uintptr_t>(rep.arg_peer[q - 1]) ^
+                                          reinterpret_cast<uintptr_t>(arg0)) % 16))
+      return fail(GESPMM_EINVAL, "gather: arg replicas need a local arg with the same 16-byte alignment");
+  }
+  rep.c_mc = c_multicast;
+  rep.arg_mc = has_arg ? arg_multicast : nullptr;
+  if (c_multicast &&
+      (reinterpret_cast<uintptr_t>(c_multicast) ^ reinterpret_cast<uintptr_t>(c_dsts[0])) % 16)
+    return fail(GESPMM_EINVAL, "gather: multicast address must share the local C's 16-byte alignment");
+  return plan_execute_impl(p, b, c_dsts[0], arg0, static_cast<cudaStream_t>(stream), &rep);
 }
 
 const char* gespmm_plan_describe(gespmm_plan_t plan) {
@@ -752,6 +856,7 @@ gespmm_status_t gespmm_spmm_host(const gespmm_csr_t* a, const float* b, uint32_t
   tr.mark("workspace ready");
 
   // ---- copy-in stream: row_ptr, B first (every block needs them)
+  tr.dev("start (copy-in stream)", ws->in);
   GESPMM_CUDA(cudaMemcpyAsync(d_rp, a->row_ptr, sizeof(uint32_t) * (m + 1),
                               cudaMemcpyHostToDevice, ws->in), "spmm");
   if (bsz)
@@ -759,7 +864,11 @@ gespmm_status_t gespmm_spmm_host(const gespmm_csr_t* a, const float* b, uint32_t
                 "spmm");
 
   // ---- row blocks balanced by nnz (binary search on the host row_ptr)
-  const int chunks = nnz >= (uint64_t(8) << 20) ? 8 : 1;
+  int chunks = nnz >= (uint64_t(8) << 20) ? 8 : 1;
+  if (const char* e = std::getenv("GESPMM_CHUNKS")) {  // pipeline depth experiments
+    const int v = std::atoi(e);
+    if (v >= 1 && v <= kMaxChunks && nnz >= uint64_t(v)) chunks = v;
+  }
   uint32_t bound[kMaxChunks + 1];
   bound[0] = 0;
   for (int i = 1; i < chunks; ++i) {
@@ -779,8 +888,11 @@ gespmm_status_t gespmm_spmm_host(const gespmm_csr_t* a, const float* b, uint32_t
     GESPMM_CUDA(cudaGetDevice(&dev), "spmm");
     shapes = make_shapes(o, a->n_cols, n, dev, m ? double(nnz) / double(m) : 0.0);
     const int32_t ht = o.hub_threshold;
+    // every row block is its own launch: the threshold follows the block's work
     const uint32_t hub_t =
-        ht > 0 ? uint32_t(ht) : (ht < 0 ? 0xffffffffu : auto_hub_threshold(shapes.slice_w, nnz));
+        ht > 0 ? uint32_t(ht)
+               : (ht < 0 ? 0xffffffffu
+                         : auto_hub_threshold(shapes.slice_w, nnz / uint64_t(chunks), shapes.warp_v.cf));
     std::vector<uint32_t> order(m);
     uint32_t maxd = 0;
     for (uint64_t r = 0; r < m; ++r) maxd = std::max(maxd, a->row_ptr[r + 1] - a->row_ptr[r]);
@@ -807,10 +919,14 @@ gespmm_status_t gespmm_spmm_host(const gespmm_csr_t* a, const float* b, uint32_t
     GESPMM_CUDA(cudaStreamSynchronize(ws->in), "spmm");
   }
   tr.mark("row_ptr+B enqueued, schedule built");
+  tr.dev("row_ptr + B (+ order) landed", ws->in);
   GESPMM_CUDA(cudaEventRecord(ws->ev_b, ws->in), "spmm");
   GESPMM_CUDA(cudaStreamWaitEvent(ws->stream, ws->ev_b, 0), "spmm");
   ColCheck* cc = nullptr;
-  if (o.validate && nnz) GESPMM_CUDA(colcheck_begin(&cc, ws->stream), "spmm");
+  if (o.validate && nnz) {
+    GESPMM_CUDA(ws->reserve(7, colcheck_workspace_bytes(nnz)), "spmm");
+    GESPMM_CUDA(colcheck_begin(&cc, nnz, ws->buf[7], ws->stream), "spmm");
+  }
 
   const bool fast = o.exact == 0;
   for (int ch = 0; ch < chunks; ++ch) {
@@ -822,10 +938,12 @@ gespmm_status_t gespmm_spmm_host(const gespmm_csr_t* a, const float* b, uint32_t
       GESPMM_CUDA(cudaMemcpyAsync(d_v + ps, a->vals + ps, sizeof(float) * (pe - ps),
                                   cudaMemcpyHostToDevice, ws->in), "spmm");
     }
+    tr.dev("block " + std::to_string(ch) + " CSR landed", ws->in);
     GESPMM_CUDA(cudaEventRecord(ws->ev_in[ch], ws->in), "spmm");
     GESPMM_CUDA(cudaStreamWaitEvent(ws->stream, ws->ev_in[ch], 0), "spmm");
-    if (cc) GESPMM_CUDA(colcheck_rows(cc, d_rp + lo, hi - lo, d_ci, a->n_cols, nnz, ws->stream),
-                        "spmm");
+    if (cc)
+      GESPMM_CUDA(colcheck_rows(cc, d_rp + lo, hi - lo, ps, pe, d_ci, a->n_cols, nnz, ws->stream),
+                  "spmm");
     SpmmArgs args{};
     args.row_ptr = d_rp + lo;  // positions stay global; rows and outputs are block-local
     args.col_ind = d_ci;
@@ -847,10 +965,11 @@ gespmm_status_t gespmm_spmm_host(const gespmm_csr_t* a, const float* b, uint32_t
       } else {
         const uint32_t nh = hub_count[ch];
         s = launch_tuned_rows(shapes, op, fast, args, d_order + lo, nh, hi - lo - nh, ws->stream,
-                              nullptr, nullptr, nullptr, nullptr);
+                              ws->side, ws->ev_fork, ws->ev_join, nullptr);
         if (s != GESPMM_OK) return s;
       }
     }
+    tr.dev("block " + std::to_string(ch) + " computed", ws->stream);
     GESPMM_CUDA(cudaEventRecord(ws->ev_done[ch], ws->stream), "spmm");
     GESPMM_CUDA(cudaStreamWaitEvent(ws->out, ws->ev_done[ch], 0), "spmm");
     const uint64_t rows = hi - lo;
@@ -862,8 +981,10 @@ gespmm_status_t gespmm_spmm_host(const gespmm_csr_t* a, const float* b, uint32_t
         GESPMM_CUDA(cudaMemcpyAsync(arg + uint64_t(lo) * n, d_arg + uint64_t(lo) * n,
                                     sizeof(int32_t) * rows * n, cudaMemcpyDeviceToHost, ws->out),
                     "spmm");
+      tr.dev("block " + std::to_string(ch) + " C copied out", ws->out);
     }
   }
+  tr.dev("all C rows copied out", ws->out);
   tr.mark("all blocks enqueued");
   if (cc) {
     uint64_t key = ~0ull;
@@ -884,6 +1005,7 @@ gespmm_status_t gespmm_spmm_host(const gespmm_csr_t* a, const float* b, uint32_t
   GESPMM_CUDA(cudaStreamSynchronize(ws->stream), "spmm");
   GESPMM_CUDA(cudaStreamSynchronize(ws->out), "spmm");
   tr.mark("done");
+  tr.dump();
   return GESPMM_OK;
 }
 

@@ -258,6 +258,52 @@ __device__ __forceinline__ uint32_t faulted_end(uint32_t start, uint32_t end, in
 }
 
 // Launch parameters shared by every SpMM kernel.
+// ---------------------------------------------------------------------------
+// Fused all-gather epilogue (multi-GPU stacked layers): the
+// output row is also stored to peer-mapped replicas of C on the other ranks
+// (NVLink P2P stores through UVA), or once through an NVLS multicast address
+// (multimem.st: the NVSwitch fans the store out to every member GPU).  Plain
+// stores, no L2 policy: the lines live in the peer's L2, not ours.
+// ---------------------------------------------------------------------------
+constexpr int kMaxPeers = GESPMM_MAX_GATHER_DSTS - 1;
+
+template <int VEC>
+__device__ __forceinline__ void st_peer(float* ptr, const float* v) {
+  if constexpr (VEC == 4) {
+    asm volatile("st.global.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(ptr), "f"(v[0]), "f"(v[1]),
+                 "f"(v[2]), "f"(v[3])
+                 : "memory");
+  } else if constexpr (VEC == 2) {
+    asm volatile("st.global.v2.f32 [%0], {%1, %2};" ::"l"(ptr), "f"(v[0]), "f"(v[1]) : "memory");
+  } else {
+    asm volatile("st.global.f32 [%0], %1;" ::"l"(ptr), "f"(v[0]) : "memory");
+  }
+}
+template <int VEC>
+__device__ __forceinline__ void st_peer_i32(int32_t* ptr, const int32_t* v) {
+  st_peer<VEC>(reinterpret_cast<float*>(ptr), reinterpret_cast<const float*>(v));
+}
+template <int VEC>
+__device__ __forceinline__ void st_multicast(float* ptr, const float* v) {
+  if constexpr (VEC == 4) {
+    asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(ptr),
+                 "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3])
+                 : "memory");
+  } else if constexpr (VEC == 2) {
+    asm volatile("multimem.st.relaxed.sys.global.v2.f32 [%0], {%1, %2};" ::"l"(ptr), "f"(v[0]),
+                 "f"(v[1])
+                 : "memory");
+  } else {
+    asm volatile("multimem.st.relaxed.sys.global.f32 [%0], %1;" ::"l"(ptr), "f"(v[0]) : "memory");
+  }
+}
+// ptxas takes vector multimem.st only for float types: the int32 arg lanes go
+// as their bit patterns (a store never alters them).
+template <int VEC>
+__device__ __forceinline__ void st_multicast_i32(int32_t* ptr, const int32_t* v) {
+  st_multicast<VEC>(reinterpret_cast<float*>(ptr), reinterpret_cast<const float*>(v));
+}
+
 struct SpmmArgs {
   const uint32_t* row_ptr;
   const uint32_t* col_ind;
@@ -280,7 +326,29 @@ struct SpmmArgs {
   // move.  pol_valid = 0 -> the kernel creates them itself (make_policies).
   uint64_t pol_keep, pol_cold, pol_stream;
   int pol_valid;
+  // Fused all-gather epilogue: n_peer replicas of C (and arg) on other ranks,
+  // each addressed like c (same row offsets and ld); c_mc/arg_mc: multicast
+  // addresses of C/arg (nullable).  n_peer = 0 and c_mc = null: local only.
+  int n_peer;
+  float* c_peer[kMaxPeers];
+  int32_t* arg_peer[kMaxPeers];
+  float* c_mc;
+  int32_t* arg_mc;
 };
+
+// Epilogue replicas of one output vector (element offset o from c / arg).
+template <int VEC, bool ARG>
+__device__ __forceinline__ void store_replicas(const SpmmArgs& a, uint64_t o, const float* out,
+                                               const int32_t* who) {
+  for (int p = 0; p < a.n_peer; ++p) {
+    st_peer<VEC>(a.c_peer[p] + o, out);
+    if (ARG && a.arg_peer[p]) st_peer_i32<VEC>(a.arg_peer[p] + o, who);
+  }
+  if (a.c_mc) {
+    st_multicast<VEC>(a.c_mc + o, out);
+    if (ARG && a.arg_mc) st_multicast_i32<VEC>(a.arg_mc + o, who);
+  }
+}
 
 __device__ __forceinline__ Policies args_policies(const SpmmArgs& a) {
   if (a.pol_valid) {

@@ -18,6 +18,7 @@
 //   or 8 vector loads per lane) gives the hub the latency hiding a single warp
 //   cannot.
 #include <algorithm>
+#include <cstdlib>
 #include <mutex>
 #include <utility>
 #include <vector>
@@ -236,6 +237,7 @@ __device__ __forceinline__ void warp_unit(const SpmmArgs& a, const Policies& pol
     const uint64_t o = uint64_t(row) * a.ld + col0 + c * SUB;
     st_stream<VEC>(a.c + o, out, pol.stream);
     if (R::kHasArg && a.arg) st_stream_i32<VEC>(a.arg + o, who[c], pol.stream);
+    if (a.n_peer || a.c_mc) store_replicas<VEC, R::kHasArg>(a, o, out, who[c]);
   }
 }
 
@@ -359,7 +361,226 @@ __global__ void __launch_bounds__(WARPS * 32) k_cta(SpmmArgs a) {
     const uint64_t o = uint64_t(row) * a.ld + col0;
     st_stream<VEC>(a.c + o, out, pol.stream);
     if (R::kHasArg && a.arg) st_stream_i32<VEC>(a.arg + o, who, pol.stream);
+    if (a.n_peer || a.c_mc) store_replicas<VEC, R::kHasArg>(a, o, out, who);
   }
+}
+
+// k_hub — row per CTA for hub rows, fed by a shared-memory ring.  The ring
+//   holds S stages of G nonzeros: for each nonzero the B-row slice of this
+//   column tile (512*VEC bytes) plus its (col, val).  kHubProducers producer
+//   warps fill stages round-robin with cp.async (LDGSTS, 16 B per lane, L1
+//   bypassed), each stage's completion tracked by an mbarrier through
+//   cp.async.mbarrier.arrive; one consumer warp owns the tile's 32*VEC columns
+//   (VEC per lane) and folds the stages in ascending position — the
+//   per-element ordered fold, bit-exact like every other kernel.  Narrow tiles
+//   (VEC = 1: 32 columns) spread one hub row over N/32 SMs.  With ~64 KB of
+//   gathers in flight per CTA a 21k-nonzero row is no longer bound by one
+//   warp's 8-deep load batch (~1.6 ms), which otherwise caps a row shard's
+//   step time from below (row-sharded multi-GPU, the pipelined host entry).
+//   (A first version issued one TMA bulk copy per nonzero from a single
+//   producer warp: 0.87 ms for a 21,657-nonzero row — the per-SM bulk-copy
+//   engine keeps too few 512-B copies in flight; tools/longrow_probe.py.)
+//   Needs N % 4 == 0 and 16-byte aligned B/C (16-byte copy units).
+#ifndef GESPMM_HUB_CONSUMERS
+#define GESPMM_HUB_CONSUMERS 1
+#endif
+#ifndef GESPMM_HUB_PRODUCERS
+#define GESPMM_HUB_PRODUCERS 4
+#endif
+#ifndef GESPMM_HUB_RING_KB
+#define GESPMM_HUB_RING_KB 32
+#endif
+constexpr int kHubConsumers = GESPMM_HUB_CONSUMERS;  // consumer warps (lane owns VEC columns)
+constexpr int kHubProducers = GESPMM_HUB_PRODUCERS;  // producer (LDGSTS) warps
+#ifndef GESPMM_HUB_GROUP
+#define GESPMM_HUB_GROUP 16
+#endif
+constexpr int kHubGroup = GESPMM_HUB_GROUP;  // nonzeros per stage (one full/empty barrier pair)
+constexpr int kHubRingBytes = GESPMM_HUB_RING_KB * 1024;
+
+template <int VEC>
+struct HubGeom {
+  static constexpr int TW = 32 * kHubConsumers * VEC;          // columns per tile
+  static constexpr int ROW_BYTES = TW * 4;                     // bytes per staged B slice
+  static constexpr int CHUNKS = ROW_BYTES / 16;                // 16-byte copies per slice
+  static constexpr int STAGES = kHubRingBytes / (ROW_BYTES * kHubGroup);
+  static_assert(STAGES >= kHubProducers, "every producer warp needs a stage of its own");
+  static_assert((kHubGroup * CHUNKS) % 32 == 0, "a stage is whole warp-wide copy rounds");
+};
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  uint32_t done = 0;
+  while (!done)
+    asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+                 "selp.u32 %0, 1, 0, p;\n\t}"
+                 : "=r"(done)
+                 : "r"(bar), "r"(parity)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, uint64_t pol) {
+  asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(dst), "l"(src),
+               "l"(pol)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async4(uint32_t dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst), "l"(src) : "memory");
+}
+
+template <int VEC>
+__device__ __forceinline__ Vec<VEC> lds_vec(const float* p) {
+  Vec<VEC> r;
+  if constexpr (VEC == 4) {
+    const float4 f = *reinterpret_cast<const float4*>(p);
+    r.x[0] = f.x;
+    r.x[1] = f.y;
+    r.x[2] = f.z;
+    r.x[3] = f.w;
+  } else if constexpr (VEC == 2) {
+    const float2 f = *reinterpret_cast<const float2*>(p);
+    r.x[0] = f.x;
+    r.x[1] = f.y;
+  } else {
+    r.x[0] = p[0];
+  }
+  return r;
+}
+
+template <int OP, bool FAST, int VEC>
+__global__ void __launch_bounds__(32 * (kHubConsumers + kHubProducers))
+k_hub(SpmmArgs a) {
+  using R = Reduce<OP>;
+  using H = HubGeom<VEC>;
+  constexpr int S = H::STAGES, G = kHubGroup;
+  extern __shared__ __align__(128) unsigned char hub_smem[];
+  float* ring = reinterpret_cast<float*>(hub_smem);                       // [S][G][TW]
+  float* s_val = reinterpret_cast<float*>(hub_smem + kHubRingBytes);      // [S*G]
+  uint32_t* s_col = reinterpret_cast<uint32_t*>(s_val + S * G);           // [S*G]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(s_col + S * G);            // full[S], empty[S]
+
+  const uint32_t sidx = blockIdx.x / a.n_tiles;
+  const uint32_t tile = blockIdx.x - sidx * a.n_tiles;
+  if (sidx >= a.n_sched) return;
+  const Policies pol = args_policies(a);
+  const uint32_t row = a.order ? a.order[sidx] : sidx;
+  const uint32_t start = a.row_ptr[row];
+  const uint32_t full_end = a.row_ptr[row + 1];
+  const uint32_t len = faulted_end(start, full_end, a.skip_tail) - start;
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t col0 = tile * uint32_t(H::TW);
+  const uint32_t tw = min(uint32_t(H::TW), a.n - col0);      // valid columns of this tile
+  const uint32_t chunks = tw / 4u;                            // 16-byte copies per slice
+  const uint32_t full0 = smem_addr(bars), empty0 = smem_addr(bars + S);
+  const uint32_t groups = (len + G - 1) / G;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < S; ++i) {
+      // full: one cp.async-completion arrival per producer lane; empty: one
+      // arrival per consumer warp
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 32;" ::"r"(full0 + 8 * i));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(empty0 + 8 * i),
+                   "r"(kHubConsumers));
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  if (warp >= kHubConsumers) {
+    // ---- producer warp pw fills groups q = pw, pw + P, ...; the group's
+    // (col, val) are loaded one group ahead of the copies they address.
+    const uint32_t pw = warp - kHubConsumers;
+    const uint32_t* ci = a.col_ind + start;
+    const float* vs = a.vals + start;
+    const char* bsrc = reinterpret_cast<const char*>(a.b + col0);
+    const uint64_t stride = uint64_t(a.ld) * 4u;
+    uint32_t q = pw;
+    uint32_t kn = 0;
+    if (q < groups && q * G + lane < len && lane < uint32_t(G)) kn = ld_stream_u32(ci + q * G + lane, pol.stream);
+    for (; q < groups; q += kHubProducers) {
+      const uint32_t kcur = kn;
+      const uint32_t qn = q + kHubProducers;
+      kn = 0;
+      if (qn < groups && lane < uint32_t(G) && qn * G + lane < len)
+        kn = ld_stream_u32(ci + qn * G + lane, pol.stream);
+      const uint32_t st = q % S, round = q / S;
+      if (round > 0) mbar_wait(empty0 + 8 * st, (round - 1) & 1u);
+      const uint32_t cnt = min(uint32_t(G), len - q * G);
+      const uint32_t e0 = st * G;
+      if (lane < cnt) {
+        cp_async4(smem_addr(s_val + e0 + lane), vs + q * G + lane);
+        cp_async4(smem_addr(s_col + e0 + lane), ci + q * G + lane);
+      }
+      // the group's G x CHUNKS 16-byte pieces, spread over the lanes: piece c is
+      // entry c / CHUNKS, bytes 16 * (c % CHUNKS) of its B slice
+      const uint32_t slot = smem_addr(ring + size_t(e0) * H::TW);
+#pragma unroll
+      for (int j = 0; j < (G * H::CHUNKS) / 32; ++j) {
+        const uint32_t c = lane + 32u * uint32_t(j);
+        const uint32_t e = c / uint32_t(H::CHUNKS), piece = c % uint32_t(H::CHUNKS);
+        const uint32_t k = __shfl_sync(0xffffffffu, kcur, int(e));
+        if (e < cnt && piece < chunks)
+          cp_async16(slot + c * 16u, bsrc + uint64_t(k) * stride + piece * 16u, pol.keep);
+      }
+      asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(full0 + 8 * st)
+                   : "memory");
+    }
+    return;
+  }
+
+  // ---- consumer warps: thread t owns columns col0 + t*VEC .. +VEC
+  const uint32_t t = threadIdx.x;                    // 0 .. 32*kHubConsumers-1
+  const bool colok = t * uint32_t(VEC) < tw;
+  float acc[VEC];
+  int32_t who[VEC];
+#pragma unroll
+  for (int e = 0; e < VEC; ++e) {
+    acc[e] = R::init();
+    who[e] = -1;
+  }
+  for (uint32_t q = 0; q < groups; ++q) {
+    const uint32_t st = q % S;
+    mbar_wait(full0 + 8 * st, (q / S) & 1u);
+    const uint32_t cnt = min(uint32_t(G), len - q * G);
+    const float* slot = ring + size_t(st) * G * H::TW + t * VEC;
+    if (colok) {
+      if (cnt == uint32_t(G)) {
+#pragma unroll
+        for (int e = 0; e < G; ++e) {
+          const Vec<VEC> bv = lds_vec<VEC>(slot + e * H::TW);
+          const float v = s_val[st * G + e];
+          const int32_t pos = a.arg_col ? int32_t(s_col[st * G + e]) : int32_t(start + q * G + e);
+          fold_vec<OP, FAST, VEC>(acc, who, v, bv.x, pos);
+        }
+      } else {
+        for (uint32_t e = 0; e < cnt; ++e) {
+          const Vec<VEC> bv = lds_vec<VEC>(slot + e * H::TW);
+          const float v = s_val[st * G + e];
+          const int32_t pos = a.arg_col ? int32_t(s_col[st * G + e]) : int32_t(start + q * G + e);
+          fold_vec<OP, FAST, VEC>(acc, who, v, bv.x, pos);
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0)
+      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(empty0 + 8 * st) : "memory");
+  }
+  if (colok) {
+    float out[VEC];
+#pragma unroll
+    for (int e = 0; e < VEC; ++e) out[e] = finish<OP>(acc[e], full_end - start);
+    const uint64_t o = uint64_t(row) * a.ld + col0 + t * VEC;
+    st_stream<VEC>(a.c + o, out, pol.stream);
+    if (R::kHasArg && a.arg) st_stream_i32<VEC>(a.arg + o, who, pol.stream);
+    if (a.n_peer || a.c_mc) store_replicas<VEC, R::kHasArg>(a, o, out, who);
+  }
+}
+
+template <int VEC>
+constexpr size_t hub_smem_bytes() {
+  using H = HubGeom<VEC>;
+  return size_t(kHubRingBytes) + size_t(H::STAGES) * kHubGroup * 8 + size_t(H::STAGES) * 16;
 }
 
 // ---- dispatch tables ------------------------------------------------------
@@ -428,6 +649,26 @@ cudaError_t cta_dispatch(const CtaShape& s, const SpmmArgs& a, cudaStream_t st) 
   GESPMM_C(1, 1) GESPMM_C(1, 2) GESPMM_C(1, 4) GESPMM_C(1, 8)
   GESPMM_C(4, 2) GESPMM_C(4, 4) GESPMM_C(4, 8)
 #undef GESPMM_C
+  return cudaErrorInvalidValue;
+}
+
+template <int OP, bool FAST>
+cudaError_t hub_dispatch(int vec, const SpmmArgs& a, cudaStream_t st) {
+  const uint64_t blocks = uint64_t(a.n_sched) * a.n_tiles;
+  if (blocks == 0) return cudaSuccess;
+  if (blocks > 0x7fffffffull) return cudaErrorInvalidConfiguration;
+#define GESPMM_H(V)                                                                        \
+  if (vec == V) {                                                                          \
+    const size_t sm = hub_smem_bytes<V>();                                                 \
+    const cudaError_t e0 = cudaFuncSetAttribute(                                           \
+        k_hub<OP, FAST, V>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));         \
+    if (e0 != cudaSuccess) return e0;                                                      \
+    k_hub<OP, FAST, V><<<dim3(uint32_t(blocks)), dim3(32 * (kHubConsumers + kHubProducers)), sm, st>>>(a); \
+    note_launch();                                                                         \
+    return cudaGetLastError();                                                             \
+  }
+  GESPMM_H(1) GESPMM_H(2) GESPMM_H(4)
+#undef GESPMM_H
   return cudaErrorInvalidValue;
 }
 
@@ -553,6 +794,35 @@ cudaError_t launch_tuned_warp(const WarpShape& s, int op, bool fast, const SpmmA
     case kMean: return fast ? warp_dispatch<kMean, true>(s, a, st, w) : warp_dispatch<kMean, false>(s, a, st, w);
     case kMax: return warp_dispatch<kMax, false>(s, a, st, w);
     default: return warp_dispatch<kMin, false>(s, a, st, w);
+  }
+}
+
+// Widest lanes (fewest sparse-row re-reads) whose column tiles still put >= 2
+// CTAs on every SM across the hub rows; a handful of hub rows get 32-column
+// tiles, spreading each over N/32 SMs.
+int hub_vec(uint32_t n, uint32_t n_hub) {
+  if (const char* e = std::getenv("GESPMM_HUB_VEC")) {  // tuning experiments
+    const int v = std::atoi(e);
+    if (v == 1 || v == 2 || v == 4) return v;
+  }
+  for (int v : {4, 2}) {
+    const uint64_t tw = 32u * uint64_t(kHubConsumers) * uint64_t(v);
+    const uint64_t tiles = (uint64_t(n) + tw - 1) / tw;
+    if (uint64_t(n_hub) * tiles >= 2ull * 148ull) return v;
+  }
+  return 1;
+}
+uint32_t hub_tile_width(uint32_t n, uint32_t n_hub) {
+  return uint32_t(32 * kHubConsumers * hub_vec(n, n_hub));
+}
+
+cudaError_t launch_tuned_hub(int op, bool fast, const SpmmArgs& a, cudaStream_t st) {
+  const int v = hub_vec(a.n, a.n_sched);
+  switch (op) {
+    case kSum: return fast ? hub_dispatch<kSum, true>(v, a, st) : hub_dispatch<kSum, false>(v, a, st);
+    case kMean: return fast ? hub_dispatch<kMean, true>(v, a, st) : hub_dispatch<kMean, false>(v, a, st);
+    case kMax: return hub_dispatch<kMax, false>(v, a, st);
+    default: return hub_dispatch<kMin, false>(v, a, st);
   }
 }
 

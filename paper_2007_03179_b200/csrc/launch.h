@@ -54,6 +54,10 @@ bool cta_shape_supported(const CtaShape& s);
 CtaShape pick_cta_shape(uint32_t n, bool vec4_ok, bool vec2_ok);
 cudaError_t launch_tuned_cta(const CtaShape& s, int op, bool fast, const SpmmArgs& a,
                              cudaStream_t st);
+// TMA-ring row-per-CTA kernel for hub rows (N % 4 == 0, 16-byte aligned B/C):
+// tile width hub_tile_width(n, n_hub) columns per CTA (a.n_sched = n_hub).
+uint32_t hub_tile_width(uint32_t n, uint32_t n_hub);
+cudaError_t launch_tuned_hub(int op, bool fast, const SpmmArgs& a, cudaStream_t st);
 
 // --- frequency-aware L2 policy (hotcols.cu) ---
 struct HotStats {
@@ -88,9 +92,12 @@ cudaError_t validate_csr_device(uint32_t m, uint32_t k, uint64_t nnz, const uint
 // the block's first row_ptr entry; positions stay global), end (locates the
 // first violation's row, synchronises `st`, frees).
 struct ColCheck;
-cudaError_t colcheck_begin(ColCheck** out, cudaStream_t st);
+size_t colcheck_workspace_bytes(uint64_t nnz);
+cudaError_t colcheck_begin(ColCheck** out, uint64_t nnz, void* ws, cudaStream_t st);
+// rows [0, m_chunk) of row_ptr_chunk own positions [ps, pe)
 cudaError_t colcheck_rows(ColCheck* c, const uint32_t* row_ptr_chunk, uint32_t m_chunk,
-                          const uint32_t* col_ind, uint32_t k, uint64_t usable, cudaStream_t st);
+                          uint64_t ps, uint64_t pe, const uint32_t* col_ind, uint32_t k,
+                          uint64_t usable, cudaStream_t st);
 cudaError_t colcheck_end(ColCheck* c, const uint32_t* row_ptr, const uint32_t* col_ind, uint32_t m,
                          uint64_t* first_bad_key, uint32_t* bad_row, uint32_t* bad_col,
                          cudaStream_t st);

@@ -24,25 +24,56 @@ __global__ void k_check_rowptr(const uint32_t* __restrict__ rp, uint32_t m, Scra
   }
 }
 
-// pass 2 (warp per row): every column in bounds and strictly increasing.
-// Key 2p marks "out of bounds" at p, 2p+1 "not increasing" at p, so the
-// minimum key is the reference's first violation (it checks bounds first).
-__global__ void k_check_cols(const uint32_t* __restrict__ rp, const uint32_t* __restrict__ ci,
-                             uint32_t m, uint32_t k, uint64_t usable, Scratch* s) {
+// pass 2, position-parallel: every column in bounds and strictly increasing
+// within its row.  Key 2p marks "out of bounds" at p, 2p+1 "not increasing"
+// at p, so the minimum key is the reference's first violation (it checks
+// bounds first).  Row starts come from a bitmap over positions (k_mark_starts),
+// so a 20k-entry hub row costs the same as 600 short ones: one coalesced pass
+// over col_ind, the predecessor from the neighbouring lane.
+__global__ void k_mark_starts(const uint32_t* __restrict__ rp, uint32_t m, uint64_t usable,
+                              uint32_t* __restrict__ bits) {
+  for (uint64_t r = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; r < m;
+       r += uint64_t(gridDim.x) * blockDim.x) {
+    const uint64_t p = rp[r];
+    if (p < usable) atomicOr(&bits[p >> 5], 1u << (p & 31));
+  }
+}
+
+__global__ void k_check_positions(const uint32_t* __restrict__ ci, uint64_t ps, uint64_t pe,
+                                  uint32_t k, const uint32_t* __restrict__ bits, Scratch* s) {
   const uint32_t lane = threadIdx.x & 31;
-  const uint64_t warps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
-  for (uint64_t r = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; r < m; r += warps) {
-    const uint64_t start = rp[r];
-    uint64_t end = rp[r + 1];
-    if (end > usable) end = usable;
-    for (uint64_t p = start + lane; p < end; p += 32) {
-      const uint32_t c = ci[p];
-      unsigned long long key = ~0ull;
-      if (c >= k) key = 2ull * p;
-      else if (p > start && c <= ci[p - 1]) key = 2ull * p + 1;
-      if (key != ~0ull) atomicMin(&s->first_bad_key, key);
+  const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+  const uint64_t w0 = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  unsigned long long best = ~0ull;
+  for (uint64_t base = (ps & ~31ull) + w0 * 32; base < pe; base += nwarps * 32) {
+    const uint64_t p = base + lane;
+    const bool in = p >= ps && p < pe;
+    const uint32_t c = in ? ci[p] : 0u;
+    uint32_t prev = __shfl_up_sync(0xffffffffu, c, 1);
+    if (lane == 0 && in && p > 0) prev = ci[p - 1];
+    const bool start = (bits[base >> 5] >> lane) & 1u;
+    if (in) {
+      if (c >= k) best = min(best, 2ull * p);
+      else if (!start && c <= prev) best = min(best, 2ull * p + 1);
     }
   }
+  for (int o = 16; o; o >>= 1) best = min(best, __shfl_xor_sync(0xffffffffu, best, o));
+  if (lane == 0 && best != ~0ull) atomicMin(&s->first_bad_key, best);
+}
+
+// bitmap of row starts + position check over [ps, pe) (positions global)
+cudaError_t launch_colcheck(const uint32_t* rp, uint32_t m, const uint32_t* ci, uint32_t k,
+                            uint64_t ps, uint64_t pe, uint64_t usable, uint32_t* bits, Scratch* s,
+                            cudaStream_t st) {
+  if (pe > usable) pe = usable;
+  if (m == 0 || pe <= ps) return cudaSuccess;
+  const uint64_t mb = (uint64_t(m) + 255) / 256;
+  k_mark_starts<<<uint32_t(mb < 148 * 8 ? mb : 148 * 8), 256, 0, st>>>(rp, m, usable, bits);
+  const uint64_t pb = (pe - ps + 255) / 256 + 1;
+  k_check_positions<<<uint32_t(pb < 148 * 16 ? pb : 148 * 16), 256, 0, st>>>(ci, ps, pe, k, bits, s);
+  note_launch();
+  note_launch();
+  return cudaGetLastError();
 }
 
 // locate the row holding the first bad position (binary search over row_ptr)
@@ -84,14 +115,17 @@ cudaError_t validate_csr_device(uint32_t m, uint32_t k, uint64_t nnz, const uint
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);
   if (e == cudaSuccess && host.first_decrease == 0xffffffffu && m > 0) {
     const uint64_t usable = ends[1] < nnz ? ends[1] : nnz;
-    const uint64_t warps_needed = m;
-    uint64_t blocks = (warps_needed + 7) / 8;
-    if (blocks > 148ull * 16) blocks = 148ull * 16;
-    k_check_cols<<<uint32_t(blocks), 256, 0, st>>>(row_ptr, col_ind, m, k, usable, s);
-    k_locate<<<1, 32, 0, st>>>(row_ptr, col_ind, m, s);
-    note_launch();
-    note_launch();
-    e = cudaGetLastError();
+    uint32_t* bits = nullptr;
+    const size_t bbytes = sizeof(uint32_t) * (usable / 32 + 1);
+    e = cudaMallocAsync(reinterpret_cast<void**>(&bits), bbytes, st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(bits, 0, bbytes, st);
+    if (e == cudaSuccess) e = launch_colcheck(row_ptr, m, col_ind, k, 0, usable, usable, bits, s, st);
+    if (e == cudaSuccess) {
+      k_locate<<<1, 32, 0, st>>>(row_ptr, col_ind, m, s);
+      note_launch();
+    }
+    if (bits) cudaFreeAsync(bits, st);
+    if (e == cudaSuccess) e = cudaGetLastError();
     if (e == cudaSuccess) e = cudaMemcpyAsync(&host, s, sizeof(host), cudaMemcpyDeviceToHost, st);
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
   }
@@ -109,15 +143,22 @@ cudaError_t validate_csr_device(uint32_t m, uint32_t k, uint64_t nnz, const uint
 // col_ind arrives; row_ptr itself is checked on the host) --------------------
 struct ColCheck {
   Scratch* s = nullptr;
+  uint32_t* bits = nullptr;  // row-start bitmap over all nnz positions
 };
 
-cudaError_t colcheck_begin(ColCheck** out, cudaStream_t st) {
+size_t colcheck_workspace_bytes(uint64_t nnz) {
+  return 256 + sizeof(uint32_t) * (nnz / 32 + 1);
+}
+
+// `ws` (colcheck_workspace_bytes(nnz), caller-owned device memory, 256-byte
+// aligned) holds the scratch minima and the bitmap: no allocation per call
+// (stream-ordered allocations released at every sync made host calls stall).
+cudaError_t colcheck_begin(ColCheck** out, uint64_t nnz, void* ws, cudaStream_t st) {
   auto* c = new ColCheck();
-  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&c->s), sizeof(Scratch), st);
-  if (e == cudaSuccess) {
-    static const Scratch init{0xffffffffu, 0u, ~0ull, 0u, 0u};
-    e = cudaMemcpyAsync(c->s, &init, sizeof(init), cudaMemcpyHostToDevice, st);
-  }
+  c->s = static_cast<Scratch*>(ws);
+  c->bits = reinterpret_cast<uint32_t*>(static_cast<char*>(ws) + 256);
+  cudaError_t e = cudaMemsetAsync(c->bits, 0, sizeof(uint32_t) * (nnz / 32 + 1), st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(c->s, 0xff, sizeof(Scratch), st);  // minima start at ~0
   if (e != cudaSuccess) {
     delete c;
     return e;
@@ -127,13 +168,9 @@ cudaError_t colcheck_begin(ColCheck** out, cudaStream_t st) {
 }
 
 cudaError_t colcheck_rows(ColCheck* c, const uint32_t* row_ptr_chunk, uint32_t m_chunk,
-                          const uint32_t* col_ind, uint32_t k, uint64_t usable, cudaStream_t st) {
-  if (m_chunk == 0) return cudaSuccess;
-  uint64_t blocks = (uint64_t(m_chunk) + 7) / 8;
-  if (blocks > 148ull * 16) blocks = 148ull * 16;
-  k_check_cols<<<uint32_t(blocks), 256, 0, st>>>(row_ptr_chunk, col_ind, m_chunk, k, usable, c->s);
-  note_launch();
-  return cudaGetLastError();
+                          uint64_t ps, uint64_t pe, const uint32_t* col_ind, uint32_t k,
+                          uint64_t usable, cudaStream_t st) {
+  return launch_colcheck(row_ptr_chunk, m_chunk, col_ind, k, ps, pe, usable, c->bits, c->s, st);
 }
 
 cudaError_t colcheck_end(ColCheck* c, const uint32_t* row_ptr, const uint32_t* col_ind, uint32_t m,
@@ -148,7 +185,6 @@ cudaError_t colcheck_end(ColCheck* c, const uint32_t* row_ptr, const uint32_t* c
   }
   if (e == cudaSuccess) e = cudaMemcpyAsync(&host, c->s, sizeof(host), cudaMemcpyDeviceToHost, st);
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);
-  cudaFreeAsync(c->s, st);
   delete c;
   *first_bad_key = e == cudaSuccess ? host.first_bad_key : ~0ull;
   *bad_row = host.bad_row;

@@ -18,7 +18,7 @@ with the oracle as the per-shard compute, and runs the CUDA path on the box.
 from __future__ import annotations
 
 import dataclasses
-from typing import Callable, List, Sequence
+from typing import Callable, List, Optional, Sequence
 
 import numpy as np
 
@@ -117,3 +117,196 @@ def shard_balance(row_ptr: Sequence[int], bounds: Sequence[int]) -> float:
     loads = [int(rp[bounds[i + 1]] - rp[bounds[i]]) for i in range(len(bounds) - 1)]
     mean = sum(loads) / len(loads)
     return max(loads) / mean if mean else 1.0
+
+
+# ---------------------------------------------------------------------------
+# Fused all-gather: the SpMM epilogue writes every output row into every
+# rank's full-height buffer over peer memory (gespmm_plan_execute_gather), and
+# one cross-rank barrier (gespmm_peer_barrier) replaces ncclAllGather.
+# ---------------------------------------------------------------------------
+
+class _CudaArray:
+    """__cuda_array_interface__ view of a raw device allocation (no ownership)."""
+
+    def __init__(self, ptr: int, shape, typestr: str):
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr,
+                                         "data": (int(ptr), False), "version": 3,
+                                         "strides": None, "stream": None}
+
+
+def _align(x: int, a: int = 256) -> int:
+    return (x + a - 1) // a * a
+
+
+class PeerRows:
+    """A full-height M x N f32 buffer (+ optional int32 arg buffer) on every
+    rank, mapped into every rank's process, with `world` signal words for the
+    barrier.  Rank r's shard lands at rows [lo_r, hi_r) of EVERY rank's copy.
+
+    Allocation: gespmm_peer_alloc (cudaMalloc base pointers), handles exchanged
+    with ``all_gather_object`` (any backend: gloo on one shared GPU in the
+    tests, NCCL on an NVSwitch box), opened with CUDA IPC (NVLink P2P mappings
+    between GPUs).  ``full`` is a torch view of the local copy; it is valid
+    while this object is open."""
+
+    def __init__(self, m: int, n: int, info: ShardInfo, device, arg: bool = False, group=None):
+        import ctypes as C
+        import torch
+        import torch.distributed as dist
+        from . import _lib
+        if info.world > _lib.MAX_GATHER_DSTS:
+            raise ValueError(f"fused all-gather supports at most {_lib.MAX_GATHER_DSTS} ranks")
+        self.m, self.n, self.info, self.device = int(m), int(n), info, torch.device(device)
+        self._L = _lib.lib()
+        self._data_bytes = _align(4 * self.m * self.n)
+        self._arg_off = self._data_bytes
+        self._sig_off = self._arg_off + (self._data_bytes if arg else 0)
+        total = self._sig_off + _align(4 * info.world)
+        with torch.cuda.device(self.device):
+            p = C.c_void_p()
+            st = self._L.gespmm_peer_alloc(total, C.byref(p))
+            if st != _lib.OK:
+                raise RuntimeError(_lib.last_error())
+            self._base = int(p.value)
+            torch.cuda.synchronize(self.device)
+            # zero the signal words (epoch counting starts at 1)
+            sig = torch.as_tensor(_CudaArray(self._base + self._sig_off, (info.world,), "<u4"),
+                                  device=self.device)
+            sig.zero_()
+            torch.cuda.synchronize(self.device)
+            bases = [self._base] * info.world
+            self._opened = []
+            if info.world > 1:
+                h = C.create_string_buffer(64)
+                st = self._L.gespmm_ipc_get_handle(self._base, h)
+                if st != _lib.OK:
+                    raise RuntimeError(_lib.last_error())
+                handles = [None] * info.world
+                dist.all_gather_object(handles, bytes(h.raw), group=group)
+                for r in range(info.world):
+                    if r == info.rank:
+                        continue
+                    q = C.c_void_p()
+                    st = self._L.gespmm_ipc_open_handle(handles[r], C.byref(q))
+                    if st != _lib.OK:
+                        raise RuntimeError(_lib.last_error())
+                    bases[r] = int(q.value)
+                    self._opened.append(bases[r])
+        self._bases = bases
+        self.has_arg = arg
+        self.epoch = 0
+        self.full = torch.as_tensor(_CudaArray(self._base, (self.m, self.n), "<f4"),
+                                    device=self.device)
+        self.full_arg = (torch.as_tensor(_CudaArray(self._base + self._arg_off, (self.m, self.n),
+                                                    "<i4"), device=self.device)
+                         if arg else None)
+        self._err = torch.zeros(1, dtype=torch.int32, device=self.device)
+        self._sigs = (C.c_void_p * info.world)(*[b + self._sig_off for b in bases])
+
+    def dsts(self, rank: Optional[int] = None):
+        """(c_dsts, arg_dsts): where shard `rank`'s row 0 lands in every copy,
+        this process's own copy first."""
+        r = self.info.rank if rank is None else rank
+        off = 4 * self.info.bounds[r] * self.n
+        order = [self.info.rank] + [p for p in range(self.info.world) if p != self.info.rank]
+        c = [self._bases[p] + off for p in order]
+        a = [self._bases[p] + self._arg_off + off for p in order] if self.has_arg else None
+        return c, a
+
+    def local_rows(self):
+        """This rank's shard rows of the local copy (a view)."""
+        return self.full[self.info.lo:self.info.hi]
+
+    def barrier(self, stream=None, timeout_ms: int = 60000):
+        """Every rank's stores issued before this call (on their streams) are
+        visible to every rank's work enqueued after it (device-side barrier)."""
+        from . import _lib
+        from .api import _stream_ptr
+        self.epoch = (self.epoch + 1) & 0xffffffff or 1
+        st = self._L.gespmm_peer_barrier(self._sigs, self.info.rank, self.info.world, self.epoch,
+                                         timeout_ms, self._err.data_ptr(), _stream_ptr(stream))
+        if st != _lib.OK:
+            raise RuntimeError(_lib.last_error())
+
+    def check(self):
+        """Raises if a barrier timed out (synchronises)."""
+        if int(self._err.item()):
+            raise RuntimeError("peer barrier timed out (a rank did not arrive)")
+
+    def close(self):
+        import torch
+        if getattr(self, "_base", None) is None:
+            return
+        torch.cuda.synchronize(self.device)
+        self.full = self.full_arg = None
+        for q in self._opened:
+            self._L.gespmm_ipc_close(q)
+        self._opened = []
+        self._L.gespmm_peer_free(self._base)
+        self._base = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def fused_propagate(a: CsrMatrix, x0, hops: int, info: ShardInfo, device, op: str = "sum",
+                    group=None, exec=None, keep_buffers: bool = False):
+    """Stacked SpMM layers H_{t+1} = A (x) H_t (SGC/APPNP-style propagation,
+    the "stacked layers" of SURVEY.md §8e.4) on nnz-balanced row shards, with
+    the per-layer all-gather fused into the SpMM epilogue: each rank's kernel
+    stores its rows into every rank's next-layer buffer over NVLink, then one
+    device barrier.  Two PeerRows buffers ping-pong.  x0: the full M x N input
+    (torch, on `device`, identical on every rank — e.g. after broadcast_dense).
+    Returns the full H_hops (a torch tensor owned by the caller)."""
+    import torch
+    from .api import DeviceCsr, ExecOptions, Plan
+    m, n = a.n_rows, int(x0.shape[1])
+    if a.n_rows != a.n_cols:
+        raise ValueError("propagation needs a square A")
+    local = DeviceCsr.from_host(shard_csr(a, info.lo, info.hi), device)
+    plan = Plan(local, n, op, exec=exec or ExecOptions())
+    bufs = [PeerRows(m, n, info, device, group=group), PeerRows(m, n, info, device, group=group)]
+    try:
+        # H_0 only feeds this rank's own kernel; peers first write bufs[0] at hop 1,
+        # after the hop-0 barrier that this rank reaches only after this copy.
+        bufs[0].full.copy_(x0)
+        for t in range(hops):
+            src, dst = bufs[t % 2], bufs[(t + 1) % 2]
+            c_dsts, _ = dst.dsts()
+            if info.hi > info.lo:
+                plan.execute_gather(src.full, c_dsts)
+            dst.barrier()
+        out = bufs[hops % 2].full.clone()
+        torch.cuda.synchronize(device)
+        for bf in bufs:
+            bf.check()
+        return (out, bufs) if keep_buffers else out
+    finally:
+        if not keep_buffers:
+            for bf in bufs:
+                bf.close()
+        plan.close()
+
+
+def nccl_propagate(a: CsrMatrix, x0, hops: int, info: ShardInfo, device, op: str = "sum",
+                   group=None, exec=None):
+    """The same propagation with the unfused exchange: local SpMM, then
+    allgather_rows (padded ncclAllGather).  The baseline fused_propagate replaces."""
+    from .api import DeviceCsr, ExecOptions, Plan
+    import torch
+    n = int(x0.shape[1])
+    local = DeviceCsr.from_host(shard_csr(a, info.lo, info.hi), device)
+    plan = Plan(local, n, op, exec=exec or ExecOptions())
+    h = x0.contiguous()
+    try:
+        for _ in range(hops):
+            y = torch.empty((info.rows, n), dtype=torch.float32, device=device)
+            if info.rows:
+                plan.execute(h, y)
+            h = allgather_rows(y, info, group) if info.world > 1 else y
+        return h
+    finally:
+        plan.close()

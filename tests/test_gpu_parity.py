@@ -108,11 +108,13 @@ def test_tuned_shapes_over_n(n, cuda):
             assert np.array_equal(arg, warg)
 
 
-@pytest.mark.parametrize("n", [32, 64, 96, 128, 200, 256, 512, 520, 1000])
+@pytest.mark.parametrize("n", [30, 32, 64, 96, 128, 130, 200, 256, 512, 520, 1000])
 @pytest.mark.parametrize("op", OPS)
 def test_hub_rows_row_per_cta(n, op, cuda):
-    """Force the row-per-CTA hub kernel (threshold 40) incl. rows spanning many
-    256-wide staging chunks; must stay bit-exact (columns split, not nonzeros)."""
+    """Force the row-per-CTA hub kernels (threshold 40): the TMA-ring k_hub when
+    N % 4 == 0 (rows spanning many ring rounds, ragged column tiles at 200/520/
+    1000), the LDG k_cta otherwise (30, 130); bit-exact (columns split, never
+    nonzeros)."""
     a, b = _powerlaw(3000, 150000, 2999, 7, n)
     ex = G.ExecOptions(hub_threshold=40)
     want_arg = op in ("max", "min")
