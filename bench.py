@@ -459,7 +459,7 @@ def run_ours(args, cfg):
                "step_ms": {"min": round(min(e2e_each), 3),
                            "median": round(statistics.median(e2e_each), 3),
                            "max": round(max(e2e_each), 3)},
-               "path": "gespmm_spmm_host: row_ptr+B H2D, then 8 nnz-balanced row blocks pipelined "
+               "path": "gespmm_spmm_host: row_ptr+B H2D, then 16 nnz-balanced row blocks pipelined "
                        "(CSR H2D | validate+kernel | C D2H on three streams)"}
 
     cpu = None

@@ -145,6 +145,7 @@ struct Plan {
   TunedShapes sh;            // kernel shapes + column slicing
   uint32_t n_hub = 0;        // order[0, n_hub) -> row-per-CTA
   uint32_t hub_threshold = 0;
+  bool hub_pdl = false;      // hub rows carry >= kHubPdlShare of the nonzeros
   uint32_t* d_order = nullptr;
   uint32_t* d_hot = nullptr;  // hot-column bitmap (frequency-aware L2 policy), nullable
   HotStats hot{};
@@ -182,9 +183,15 @@ namespace {
 // one block of the pipelined host entry.  Measured with
 // tools/shard_emulation.py (profiles/r1_shard_emulation.md): factor 1.5 keeps
 // the 1-GPU step unchanged and halves the 8-shard step (1.51 -> 0.79 ms).
-uint32_t auto_hub_threshold(uint32_t n, uint64_t nnz, int cf) {
+uint32_t auto_hub_threshold(uint32_t n, uint64_t nnz, int cf, uint32_t k, int dev) {
   if (n < 64) return 0xffffffffu;  // narrow rows: one warp already covers the row cheaply
-  const double t_launch = double(nnz) * 4.0 * double(n) / 19e12;
+  // gather rate: ~19 TB/s while B (mostly) fits the L2, ~9.5 TB/s once the
+  // gathers miss to HBM (ogbn-products N=256: B = 2.5 GB)
+  int l2 = 0;
+  cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev);
+  const double b_bytes = double(k) * double(n) * 4.0;
+  const double rate = (l2 > 0 && b_bytes > 1.5 * double(l2)) ? 9.5e12 : 19e12;
+  const double t_launch = double(nnz) * 4.0 * double(n) / rate;
   const double t_nnz = 0.7e-6 * double(cf < 1 ? 1 : cf) / 8.0;
   double f = 1.5;  // GESPMM_HUB_FACTOR: tuning experiments (tools/shard_emulation.py)
   if (const char* e = std::getenv("GESPMM_HUB_FACTOR")) f = std::max(0.05, std::atof(e));
@@ -250,10 +257,20 @@ TunedShapes make_shapes(const gespmm_options_t& o, uint32_t k, uint32_t n, int d
 // rows first, row-per-CTA) for every column slice, slice-major.  `a` carries
 // the full-width B/C/arg pointers with ld = row stride.  With `side` the hub
 // kernel overlaps the warp kernel of the same slice on that stream.
+// How the hub kernel shares the GPU with the warp kernel: when the hub rows
+// carry a large share of the nonzeros (a 1/8 row shard of a power-law graph:
+// ~35%), the hub kernel goes first on the same stream and the warp kernel
+// follows as a programmatic dependent launch, so the hub CTAs (the critical
+// path) are resident from the start; with a small share, the hub kernel runs
+// on a high-priority side stream and its CTAs take SM slots as warp CTAs
+// retire, which disturbs the warp kernel less (profiles/r1_shard_emulation.md).
+constexpr double kHubPdlShare = 0.25;
+
 gespmm_status_t launch_tuned_rows(const TunedShapes& t, int op, bool fast, const SpmmArgs& a0,
                                   const uint32_t* order, uint32_t n_hub, uint32_t n_rest,
                                   cudaStream_t st, cudaStream_t side, cudaEvent_t fork,
-                                  cudaEvent_t join, const cudaAccessPolicyWindow* winp) {
+                                  cudaEvent_t join, const cudaAccessPolicyWindow* winp,
+                                  bool hub_pdl) {
   SpmmArgs a = a0;
   GESPMM_CUDA(resolve_policies(&a, st), "spmm");
   const bool v_ok = aligned(a.b, 16) && aligned(a.c, 16) && (!a.arg || aligned(a.arg, 16));
@@ -281,6 +298,7 @@ gespmm_status_t launch_tuned_rows(const TunedShapes& t, int op, bool fast, const
     sa.c_mc = a.c_mc ? a.c_mc + off : nullptr;
     sa.arg_mc = a.arg_mc ? a.arg_mc + off : nullptr;
     sa.n = w;
+    bool hub_then_pdl = false, side_used = false;
     if (n_hub) {
       SpmmArgs h = sa;
       h.order = order;
@@ -291,22 +309,32 @@ gespmm_status_t launch_tuned_rows(const TunedShapes& t, int op, bool fast, const
                        (!sa.arg || aligned(sa.arg, 16));
       const uint32_t tw = tma ? hub_tile_width(w, n_hub) : uint32_t(cs.vec * cs.warps * 32);
       h.n_tiles = (w + tw - 1) / tw;
-      cudaStream_t hs = side ? side : st;
-      if (side) {
-        GESPMM_CUDA(cudaEventRecord(fork, st), "spmm");
-        GESPMM_CUDA(cudaStreamWaitEvent(side, fork, 0), "spmm");
+      if (tma && (hub_pdl || !side)) {
+        // same stream; the warp kernel follows as a programmatic dependent
+        // launch, so the hub CTAs are resident first and both run together
+        GESPMM_CUDA(launch_tuned_hub(op, fast, h, st), "spmm");
+        hub_then_pdl = true;
+      } else {
+        cudaStream_t hs = side ? side : st;
+        if (side) {
+          GESPMM_CUDA(cudaEventRecord(fork, st), "spmm");
+          GESPMM_CUDA(cudaStreamWaitEvent(side, fork, 0), "spmm");
+        }
+        if (tma)
+          GESPMM_CUDA(launch_tuned_hub(op, fast, h, hs), "spmm");
+        else
+          GESPMM_CUDA(launch_tuned_cta(cs, op, fast, h, hs), "spmm");
+        if (side) {
+          GESPMM_CUDA(cudaEventRecord(join, side), "spmm");
+          side_used = true;
+        }
       }
-      if (tma)
-        GESPMM_CUDA(launch_tuned_hub(op, fast, h, hs), "spmm");
-      else
-        GESPMM_CUDA(launch_tuned_cta(cs, op, fast, h, hs), "spmm");
-      if (side) GESPMM_CUDA(cudaEventRecord(join, side), "spmm");
     }
     sa.order = order + n_hub;
     sa.n_sched = n_rest;
     sa.n_tiles = (w + wsel.tile_width() - 1) / wsel.tile_width();
-    if (n_rest) GESPMM_CUDA(launch_tuned_warp(wsel, op, fast, sa, st, winp), "spmm");
-    if (n_hub && side) GESPMM_CUDA(cudaStreamWaitEvent(st, join, 0), "spmm");
+    if (n_rest) GESPMM_CUDA(launch_tuned_warp(wsel, op, fast, sa, st, winp, hub_then_pdl), "spmm");
+    if (side_used) GESPMM_CUDA(cudaStreamWaitEvent(st, join, 0), "spmm");
   }
   return GESPMM_OK;
 }
@@ -339,10 +367,14 @@ gespmm_status_t build_tuned(Plan& p, const uint32_t* host_rp, cudaStream_t st) {
 
   const int32_t ht = p.o.hub_threshold;
   p.hub_threshold = ht > 0 ? uint32_t(ht)
-                           : (ht < 0 ? 0xffffffffu : auto_hub_threshold(sw, host_rp[m], p.sh.warp_v.cf));
+                           : (ht < 0 ? 0xffffffffu
+                                     : auto_hub_threshold(sw, host_rp[m], p.sh.warp_v.cf,
+                                                          p.a.n_cols, p.device));
   uint32_t n_hub = 0;
-  while (n_hub < m && deg[order[n_hub]] >= p.hub_threshold) ++n_hub;
+  uint64_t hub_nnz = 0;
+  while (n_hub < m && deg[order[n_hub]] >= p.hub_threshold) hub_nnz += deg[order[n_hub++]];
   p.n_hub = n_hub;
+  p.hub_pdl = host_rp[m] && double(hub_nnz) >= kHubPdlShare * double(host_rp[m]);
 
   // Rows of at most two staged chunks gain nothing from the LPT schedule:
   // the identity order saves the schedule load in front of every row.
@@ -513,7 +545,7 @@ gespmm_status_t plan_execute_impl(Plan& p, const float* b, float* c, int32_t* ar
     }
   }
   return launch_tuned_rows(p.sh, p.op, fast, args, p.d_order, p.n_hub, p.a.n_rows - p.n_hub, st,
-                           p.side, p.ev_fork, p.ev_join, winp);
+                           p.side, p.ev_fork, p.ev_join, winp, p.hub_pdl);
 }
 
 // Small LRU of plans for the plan-less device entry point: keyed by the CSR
@@ -864,7 +896,9 @@ gespmm_status_t gespmm_spmm_host(const gespmm_csr_t* a, const float* b, uint32_t
                 "spmm");
 
   // ---- row blocks balanced by nnz (binary search on the host row_ptr)
-  int chunks = nnz >= (uint64_t(8) << 20) ? 8 : 1;
+  // pipeline depth: more blocks shrink the un-overlapped tail (last block's
+  // kernel + C copy-out); 16 measured best at Reddit size (20.0 vs 20.6 ms at 8)
+  int chunks = nnz >= (uint64_t(32) << 20) ? 16 : (nnz >= (uint64_t(8) << 20) ? 8 : 1);
   if (const char* e = std::getenv("GESPMM_CHUNKS")) {  // pipeline depth experiments
     const int v = std::atoi(e);
     if (v >= 1 && v <= kMaxChunks && nnz >= uint64_t(v)) chunks = v;
@@ -882,6 +916,7 @@ gespmm_status_t gespmm_spmm_host(const gespmm_csr_t* a, const float* b, uint32_t
   //      rows at or above the hub threshold first, for the row-per-CTA kernel
   const bool tuned = o.variant == GESPMM_VARIANT_TUNED;
   uint32_t hub_count[kMaxChunks] = {};
+  uint64_t hub_nnz[kMaxChunks] = {};
   TunedShapes shapes;
   if (tuned) {
     int dev = 0;
@@ -892,7 +927,8 @@ gespmm_status_t gespmm_spmm_host(const gespmm_csr_t* a, const float* b, uint32_t
     const uint32_t hub_t =
         ht > 0 ? uint32_t(ht)
                : (ht < 0 ? 0xffffffffu
-                         : auto_hub_threshold(shapes.slice_w, nnz / uint64_t(chunks), shapes.warp_v.cf));
+                         : auto_hub_threshold(shapes.slice_w, nnz / uint64_t(chunks),
+                                              shapes.warp_v.cf, a->n_cols, dev));
     std::vector<uint32_t> order(m);
     uint32_t maxd = 0;
     for (uint64_t r = 0; r < m; ++r) maxd = std::max(maxd, a->row_ptr[r + 1] - a->row_ptr[r]);
@@ -910,7 +946,10 @@ gespmm_status_t gespmm_spmm_host(const gespmm_csr_t* a, const float* b, uint32_t
       for (uint32_t r = lo; r < hi; ++r) {
         const uint32_t d = a->row_ptr[r + 1] - a->row_ptr[r];
         order[count[maxd - d]++] = r - lo;  // local id within the block
-        if (d >= hub_t) ++hub_count[ch];
+        if (d >= hub_t) {
+          ++hub_count[ch];
+          hub_nnz[ch] += d;
+        }
       }
     }
     GESPMM_CUDA(cudaMemcpyAsync(d_order, order.data(), sizeof(uint32_t) * m,
@@ -964,8 +1003,9 @@ gespmm_status_t gespmm_spmm_host(const gespmm_csr_t* a, const float* b, uint32_t
         GESPMM_CUDA(launch_faithful(o.variant, o.cf, op, fast, args, ws->stream), "spmm");
       } else {
         const uint32_t nh = hub_count[ch];
+        const bool pdl = double(hub_nnz[ch]) >= kHubPdlShare * double(pe - ps);
         s = launch_tuned_rows(shapes, op, fast, args, d_order + lo, nh, hi - lo - nh, ws->stream,
-                              ws->side, ws->ev_fork, ws->ev_join, nullptr);
+                              ws->side, ws->ev_fork, ws->ev_join, nullptr, pdl);
         if (s != GESPMM_OK) return s;
       }
     }

@@ -334,6 +334,7 @@ struct SpmmArgs {
   int32_t* arg_peer[kMaxPeers];
   float* c_mc;
   int32_t* arg_mc;
+  uint32_t* work;  // hub kernel: unit counter of a persistent launch (zeroed before it), or null
 };
 
 // Epilogue replicas of one output vector (element offset o from c / arg).

@@ -18,6 +18,7 @@
 //   or 8 vector loads per lane) gives the hub the latency hiding a single warp
 //   cannot.
 #include <algorithm>
+#include <atomic>
 #include <cstdlib>
 #include <mutex>
 #include <utility>
@@ -460,20 +461,11 @@ k_hub(SpmmArgs a) {
   uint32_t* s_col = reinterpret_cast<uint32_t*>(s_val + S * G);           // [S*G]
   uint64_t* bars = reinterpret_cast<uint64_t*>(s_col + S * G);            // full[S], empty[S]
 
-  const uint32_t sidx = blockIdx.x / a.n_tiles;
-  const uint32_t tile = blockIdx.x - sidx * a.n_tiles;
-  if (sidx >= a.n_sched) return;
+  __shared__ uint32_t s_unit;
   const Policies pol = args_policies(a);
-  const uint32_t row = a.order ? a.order[sidx] : sidx;
-  const uint32_t start = a.row_ptr[row];
-  const uint32_t full_end = a.row_ptr[row + 1];
-  const uint32_t len = faulted_end(start, full_end, a.skip_tail) - start;
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t col0 = tile * uint32_t(H::TW);
-  const uint32_t tw = min(uint32_t(H::TW), a.n - col0);      // valid columns of this tile
-  const uint32_t chunks = tw / 4u;                            // 16-byte copies per slice
   const uint32_t full0 = smem_addr(bars), empty0 = smem_addr(bars + S);
-  const uint32_t groups = (len + G - 1) / G;
+  const uint32_t n_units = a.n_sched * a.n_tiles;
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < S; ++i) {
@@ -485,95 +477,135 @@ k_hub(SpmmArgs a) {
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  __syncthreads();
 
-  if (warp >= kHubConsumers) {
-    // ---- producer warp pw fills groups q = pw, pw + P, ...; the group's
-    // (col, val) are loaded one group ahead of the copies they address.
-    const uint32_t pw = warp - kHubConsumers;
-    const uint32_t* ci = a.col_ind + start;
-    const float* vs = a.vals + start;
-    const char* bsrc = reinterpret_cast<const char*>(a.b + col0);
-    const uint64_t stride = uint64_t(a.ld) * 4u;
-    uint32_t q = pw;
-    uint32_t kn = 0;
-    if (q < groups && q * G + lane < len && lane < uint32_t(G)) kn = ld_stream_u32(ci + q * G + lane, pol.stream);
-    for (; q < groups; q += kHubProducers) {
-      const uint32_t kcur = kn;
-      const uint32_t qn = q + kHubProducers;
-      kn = 0;
-      if (qn < groups && lane < uint32_t(G) && qn * G + lane < len)
-        kn = ld_stream_u32(ci + qn * G + lane, pol.stream);
-      const uint32_t st = q % S, round = q / S;
-      if (round > 0) mbar_wait(empty0 + 8 * st, (round - 1) & 1u);
-      const uint32_t cnt = min(uint32_t(G), len - q * G);
-      const uint32_t e0 = st * G;
-      if (lane < cnt) {
-        cp_async4(smem_addr(s_val + e0 + lane), vs + q * G + lane);
-        cp_async4(smem_addr(s_col + e0 + lane), ci + q * G + lane);
-      }
-      // the group's G x CHUNKS 16-byte pieces, spread over the lanes: piece c is
-      // entry c / CHUNKS, bytes 16 * (c % CHUNKS) of its B slice
-      const uint32_t slot = smem_addr(ring + size_t(e0) * H::TW);
-#pragma unroll
-      for (int j = 0; j < (G * H::CHUNKS) / 32; ++j) {
-        const uint32_t c = lane + 32u * uint32_t(j);
-        const uint32_t e = c / uint32_t(H::CHUNKS), piece = c % uint32_t(H::CHUNKS);
-        const uint32_t k = __shfl_sync(0xffffffffu, kcur, int(e));
-        if (e < cnt && piece < chunks)
-          cp_async16(slot + c * 16u, bsrc + uint64_t(k) * stride + piece * 16u, pol.keep);
-      }
-      asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(full0 + 8 * st)
-                   : "memory");
-    }
-    return;
-  }
+  // The warp kernel queued behind this one (programmatic dependent launch,
+  // disjoint rows, no data dependence) may start now: these CTAs hold their
+  // SM slots first, the warp kernel fills what is left.
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
-  // ---- consumer warps: thread t owns columns col0 + t*VEC .. +VEC
-  const uint32_t t = threadIdx.x;                    // 0 .. 32*kHubConsumers-1
-  const bool colok = t * uint32_t(VEC) < tw;
-  float acc[VEC];
-  int32_t who[VEC];
-#pragma unroll
-  for (int e = 0; e < VEC; ++e) {
-    acc[e] = R::init();
-    who[e] = -1;
-  }
-  for (uint32_t q = 0; q < groups; ++q) {
-    const uint32_t st = q % S;
-    mbar_wait(full0 + 8 * st, (q / S) & 1u);
-    const uint32_t cnt = min(uint32_t(G), len - q * G);
-    const float* slot = ring + size_t(st) * G * H::TW + t * VEC;
-    if (colok) {
-      if (cnt == uint32_t(G)) {
-#pragma unroll
-        for (int e = 0; e < G; ++e) {
-          const Vec<VEC> bv = lds_vec<VEC>(slot + e * H::TW);
-          const float v = s_val[st * G + e];
-          const int32_t pos = a.arg_col ? int32_t(s_col[st * G + e]) : int32_t(start + q * G + e);
-          fold_vec<OP, FAST, VEC>(acc, who, v, bv.x, pos);
+  // Units (hub row, column tile) in schedule (LPT) order.  Persistent launch
+  // (a.work != null): CTAs pull units from a counter, so a few CTAs per SM
+  // leave room for the warp kernel running alongside; otherwise one unit per
+  // CTA.  Ring stages and barrier phases run on across units (gbase).
+  uint32_t gbase = 0;
+  for (uint32_t iter = 0;; ++iter) {
+    if (threadIdx.x == 0)
+      s_unit = a.work ? atomicAdd(a.work, 1u) : (iter == 0 ? blockIdx.x : 0xffffffffu);
+    __syncthreads();
+    const uint32_t unit = s_unit;
+    if (unit >= n_units) break;
+    const uint32_t sidx = unit / a.n_tiles;
+    const uint32_t tile = unit - sidx * a.n_tiles;
+    const uint32_t row = a.order ? a.order[sidx] : sidx;
+    const uint32_t start = a.row_ptr[row];
+    const uint32_t full_end = a.row_ptr[row + 1];
+    const uint32_t len = faulted_end(start, full_end, a.skip_tail) - start;
+    const uint32_t col0 = tile * uint32_t(H::TW);
+    const uint32_t tw = min(uint32_t(H::TW), a.n - col0);      // valid columns of this tile
+    const uint32_t chunks = tw / 4u;                            // 16-byte copies per slice
+    const uint32_t groups = (len + G - 1) / G;
+
+    if (warp >= kHubConsumers) {
+      // ---- producer warp pw fills groups q = pw, pw + P, ...; the group's
+      // (col, val) are loaded one group ahead of the copies they address.
+      const uint32_t pw = warp - kHubConsumers;
+      const uint32_t* ci = a.col_ind + start;
+      const float* vs = a.vals + start;
+      const char* bsrc = reinterpret_cast<const char*>(a.b + col0);
+      const uint64_t stride = uint64_t(a.ld) * 4u;
+      uint32_t q = pw;
+      uint32_t kn = 0;
+      if (q < groups && q * G + lane < len && lane < uint32_t(G))
+        kn = ld_stream_u32(ci + q * G + lane, pol.stream);
+      for (; q < groups; q += kHubProducers) {
+        const uint32_t kcur = kn;
+        const uint32_t qn = q + kHubProducers;
+        kn = 0;
+        if (qn < groups && lane < uint32_t(G) && qn * G + lane < len)
+          kn = ld_stream_u32(ci + qn * G + lane, pol.stream);
+        const uint32_t ga = gbase + q;
+        const uint32_t st = ga % S, round = ga / S;
+        if (round > 0) mbar_wait(empty0 + 8 * st, (round - 1) & 1u);
+        const uint32_t cnt = min(uint32_t(G), len - q * G);
+        const uint32_t e0 = st * G;
+        if (lane < cnt) {
+          cp_async4(smem_addr(s_val + e0 + lane), vs + q * G + lane);
+          cp_async4(smem_addr(s_col + e0 + lane), ci + q * G + lane);
         }
-      } else {
-        for (uint32_t e = 0; e < cnt; ++e) {
-          const Vec<VEC> bv = lds_vec<VEC>(slot + e * H::TW);
-          const float v = s_val[st * G + e];
-          const int32_t pos = a.arg_col ? int32_t(s_col[st * G + e]) : int32_t(start + q * G + e);
-          fold_vec<OP, FAST, VEC>(acc, who, v, bv.x, pos);
+        // the group's G x CHUNKS 16-byte pieces, spread over the lanes: piece c
+        // is entry c / CHUNKS, bytes 16 * (c % CHUNKS) of its B slice
+        const uint32_t slot = smem_addr(ring + size_t(e0) * H::TW);
+#pragma unroll
+        for (int j = 0; j < (G * H::CHUNKS) / 32; ++j) {
+          const uint32_t c = lane + 32u * uint32_t(j);
+          const uint32_t e = c / uint32_t(H::CHUNKS), piece = c % uint32_t(H::CHUNKS);
+          const uint32_t k = __shfl_sync(0xffffffffu, kcur, int(e));
+          if (e < cnt && piece < chunks)
+            cp_async16(slot + c * 16u, bsrc + uint64_t(k) * stride + piece * 16u, pol.keep);
         }
+        asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(full0 + 8 * st)
+                     : "memory");
+      }
+    } else {
+      // ---- consumer warps: thread t owns columns col0 + t*VEC .. +VEC
+      const uint32_t t = threadIdx.x;                    // 0 .. 32*kHubConsumers-1
+      const bool colok = t * uint32_t(VEC) < tw;
+      float acc[VEC];
+      int32_t who[VEC];
+#pragma unroll
+      for (int e = 0; e < VEC; ++e) {
+        acc[e] = R::init();
+        who[e] = -1;
+      }
+      for (uint32_t q = 0; q < groups; ++q) {
+        const uint32_t ga = gbase + q;
+        const uint32_t st = ga % S;
+        mbar_wait(full0 + 8 * st, (ga / S) & 1u);
+        const uint32_t cnt = min(uint32_t(G), len - q * G);
+        const float* slot = ring + size_t(st) * G * H::TW + t * VEC;
+        if (colok) {
+          if (cnt == uint32_t(G)) {
+            // every shared-memory read of the stage first (G loads in flight),
+            // then the ordered fold
+            Vec<VEC> bv[G];
+            float vv[G];
+#pragma unroll
+            for (int e = 0; e < G; ++e) {
+              bv[e] = lds_vec<VEC>(slot + e * H::TW);
+              vv[e] = s_val[st * G + e];
+            }
+#pragma unroll
+            for (int e = 0; e < G; ++e) {
+              const int32_t pos =
+                  a.arg_col ? int32_t(s_col[st * G + e]) : int32_t(start + q * G + e);
+              fold_vec<OP, FAST, VEC>(acc, who, vv[e], bv[e].x, pos);
+            }
+          } else {
+            for (uint32_t e = 0; e < cnt; ++e) {
+              const Vec<VEC> bv = lds_vec<VEC>(slot + e * H::TW);
+              const float v = s_val[st * G + e];
+              const int32_t pos =
+                  a.arg_col ? int32_t(s_col[st * G + e]) : int32_t(start + q * G + e);
+              fold_vec<OP, FAST, VEC>(acc, who, v, bv.x, pos);
+            }
+          }
+        }
+        __syncwarp();
+        if (lane == 0)
+          asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(empty0 + 8 * st) : "memory");
+      }
+      if (colok) {
+        float out[VEC];
+#pragma unroll
+        for (int e = 0; e < VEC; ++e) out[e] = finish<OP>(acc[e], full_end - start);
+        const uint64_t o = uint64_t(row) * a.ld + col0 + t * VEC;
+        st_stream<VEC>(a.c + o, out, pol.stream);
+        if (R::kHasArg && a.arg) st_stream_i32<VEC>(a.arg + o, who, pol.stream);
+        if (a.n_peer || a.c_mc) store_replicas<VEC, R::kHasArg>(a, o, out, who);
       }
     }
-    __syncwarp();
-    if (lane == 0)
-      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(empty0 + 8 * st) : "memory");
-  }
-  if (colok) {
-    float out[VEC];
-#pragma unroll
-    for (int e = 0; e < VEC; ++e) out[e] = finish<OP>(acc[e], full_end - start);
-    const uint64_t o = uint64_t(row) * a.ld + col0 + t * VEC;
-    st_stream<VEC>(a.c + o, out, pol.stream);
-    if (R::kHasArg && a.arg) st_stream_i32<VEC>(a.arg + o, who, pol.stream);
-    if (a.n_peer || a.c_mc) store_replicas<VEC, R::kHasArg>(a, o, out, who);
+    gbase += groups;
+    __syncthreads();  // the unit is done (and s_unit read) before the next fetch
   }
 }
 
@@ -587,18 +619,23 @@ constexpr size_t hub_smem_bytes() {
 
 template <class K>
 cudaError_t launch_ex(K kernel, dim3 g, dim3 b, cudaStream_t st, const SpmmArgs& a,
-                      const cudaAccessPolicyWindow* window) {
+                      const cudaAccessPolicyWindow* window, bool pdl = false) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = g;
   cfg.blockDim = b;
   cfg.dynamicSmemBytes = 0;
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   cfg.numAttrs = 0;
   if (window) {
-    attr[0].id = cudaLaunchAttributeAccessPolicyWindow;
-    attr[0].val.accessPolicyWindow = *window;
-    cfg.numAttrs = 1;
+    attr[cfg.numAttrs].id = cudaLaunchAttributeAccessPolicyWindow;
+    attr[cfg.numAttrs].val.accessPolicyWindow = *window;
+    ++cfg.numAttrs;
+  }
+  if (pdl) {  // programmatic dependent launch: may start once the previous kernel triggers
+    attr[cfg.numAttrs].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[cfg.numAttrs].val.programmaticStreamSerializationAllowed = 1;
+    ++cfg.numAttrs;
   }
   cfg.attrs = attr;
   return cudaLaunchKernelEx(&cfg, kernel, a);
@@ -606,7 +643,7 @@ cudaError_t launch_ex(K kernel, dim3 g, dim3 b, cudaStream_t st, const SpmmArgs&
 
 template <int OP, bool FAST>
 cudaError_t warp_dispatch(const WarpShape& s, const SpmmArgs& a, cudaStream_t st,
-                          const cudaAccessPolicyWindow* window) {
+                          const cudaAccessPolicyWindow* window, bool pdl) {
   const uint32_t rpw = 32u / uint32_t(s.lpr);
   const uint64_t groups = (uint64_t(a.n_sched) + rpw - 1) / rpw;
   const uint64_t warps = groups * a.n_tiles;
@@ -619,8 +656,8 @@ cudaError_t warp_dispatch(const WarpShape& s, const SpmmArgs& a, cudaStream_t st
     constexpr bool kHotShape = L == 32; /* hot-column map on full-warp rows only */          \
     const dim3 g{uint32_t(blocks)};                                                          \
     const cudaError_t e =                                                                    \
-        (kHotShape && a.hot) ? launch_ex(k_warp<OP, FAST, V, L, F, kHotShape>, g, b, st, a, window) \
-                             : launch_ex(k_warp<OP, FAST, V, L, F, false>, g, b, st, a, window); \
+        (kHotShape && a.hot) ? launch_ex(k_warp<OP, FAST, V, L, F, kHotShape>, g, b, st, a, window, pdl) \
+                             : launch_ex(k_warp<OP, FAST, V, L, F, false>, g, b, st, a, window, pdl); \
     note_launch();                                                                           \
     return e;                                                                                \
   }
@@ -652,17 +689,69 @@ cudaError_t cta_dispatch(const CtaShape& s, const SpmmArgs& a, cudaStream_t st) 
   return cudaErrorInvalidValue;
 }
 
+// Persistent hub launches pull units from a per-launch counter: a ring of
+// counters per device, zeroed on the launch's stream right before it.
+struct HubCounters {
+  uint32_t* d = nullptr;
+  std::atomic<uint32_t> next{0};
+  int sms = 0;
+};
+constexpr uint32_t kHubCounterRing = 256;
+
+cudaError_t hub_counter(uint32_t** out, int* sms, cudaStream_t st) {
+  static std::mutex mu;
+  static HubCounters per_dev[64];
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+  HubCounters& h = per_dev[dev];
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    if (!h.d) {
+      if ((e = cudaMalloc(reinterpret_cast<void**>(&h.d), sizeof(uint32_t) * kHubCounterRing)) != cudaSuccess)
+        return e;
+      cudaDeviceGetAttribute(&h.sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+  }
+  uint32_t* c = h.d + (h.next.fetch_add(1) % kHubCounterRing);
+  *sms = h.sms;
+  *out = c;
+  return cudaMemsetAsync(c, 0, sizeof(uint32_t), st);
+}
+
 template <int OP, bool FAST>
-cudaError_t hub_dispatch(int vec, const SpmmArgs& a, cudaStream_t st) {
-  const uint64_t blocks = uint64_t(a.n_sched) * a.n_tiles;
-  if (blocks == 0) return cudaSuccess;
-  if (blocks > 0x7fffffffull) return cudaErrorInvalidConfiguration;
+cudaError_t hub_dispatch(int vec, const SpmmArgs& a0, cudaStream_t st) {
+  const uint64_t units = uint64_t(a0.n_sched) * a0.n_tiles;
+  if (units == 0) return cudaSuccess;
+  if (units > 0x7fffffffull) return cudaErrorInvalidConfiguration;
+  SpmmArgs a = a0;
+  // persistent: kHubCtasPerSm CTAs per SM at most, so the warp kernel running
+  // alongside keeps most of each SM (GESPMM_HUB_PERSIST=0: one CTA per unit)
+  static const int per_sm = [] {
+    const char* e = std::getenv("GESPMM_HUB_PERSIST");
+    return e ? std::atoi(e) : 2;
+  }();
+  uint64_t blocks = units;
+  a.work = nullptr;
+  if (per_sm > 0) {
+    int sms = 0;
+    const cudaError_t ec = hub_counter(&a.work, &sms, st);
+    if (ec != cudaSuccess) return ec;
+    blocks = std::min<uint64_t>(units, uint64_t(per_sm) * uint64_t(sms > 0 ? sms : 148));
+  }
 #define GESPMM_H(V)                                                                        \
   if (vec == V) {                                                                          \
     const size_t sm = hub_smem_bytes<V>();                                                 \
-    const cudaError_t e0 = cudaFuncSetAttribute(                                           \
-        k_hub<OP, FAST, V>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));         \
-    if (e0 != cudaSuccess) return e0;                                                      \
+    static bool attr_done[64] = {}; /* once per device: the call is not stream-ordered */   \
+    int dev_ = 0;                                                                          \
+    cudaGetDevice(&dev_);                                                                  \
+    if (dev_ < 0 || dev_ >= 64 || !attr_done[dev_]) {                                      \
+      const cudaError_t e0 = cudaFuncSetAttribute(                                         \
+          k_hub<OP, FAST, V>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));       \
+      if (e0 != cudaSuccess) return e0;                                                    \
+      if (dev_ >= 0 && dev_ < 64) attr_done[dev_] = true;                                  \
+    }                                                                                      \
     k_hub<OP, FAST, V><<<dim3(uint32_t(blocks)), dim3(32 * (kHubConsumers + kHubProducers)), sm, st>>>(a); \
     note_launch();                                                                         \
     return cudaGetLastError();                                                             \
@@ -788,12 +877,12 @@ CtaShape pick_cta_shape(uint32_t n, bool vec4_ok, bool /*vec2_ok*/) {
 }
 
 cudaError_t launch_tuned_warp(const WarpShape& s, int op, bool fast, const SpmmArgs& a,
-                              cudaStream_t st, const cudaAccessPolicyWindow* w) {
+                              cudaStream_t st, const cudaAccessPolicyWindow* w, bool pdl) {
   switch (op) {
-    case kSum: return fast ? warp_dispatch<kSum, true>(s, a, st, w) : warp_dispatch<kSum, false>(s, a, st, w);
-    case kMean: return fast ? warp_dispatch<kMean, true>(s, a, st, w) : warp_dispatch<kMean, false>(s, a, st, w);
-    case kMax: return warp_dispatch<kMax, false>(s, a, st, w);
-    default: return warp_dispatch<kMin, false>(s, a, st, w);
+    case kSum: return fast ? warp_dispatch<kSum, true>(s, a, st, w, pdl) : warp_dispatch<kSum, false>(s, a, st, w, pdl);
+    case kMean: return fast ? warp_dispatch<kMean, true>(s, a, st, w, pdl) : warp_dispatch<kMean, false>(s, a, st, w, pdl);
+    case kMax: return warp_dispatch<kMax, false>(s, a, st, w, pdl);
+    default: return warp_dispatch<kMin, false>(s, a, st, w, pdl);
   }
 }
 

@@ -48,8 +48,11 @@ struct CtaShape {
 bool tuned_shape_supported(const WarpShape& s);
 WarpShape pick_warp_shape(uint32_t n, bool vec4_ok, bool vec2_ok, int rows_per_warp = 1);
 // `window` (nullable): L2 access-policy window attached to the launch.
+// pdl: launched right behind the hub kernel on the same stream, allowed to
+// start while it runs (programmatic dependent launch; rows are disjoint).
 cudaError_t launch_tuned_warp(const WarpShape& s, int op, bool fast, const SpmmArgs& a,
-                              cudaStream_t st, const cudaAccessPolicyWindow* window = nullptr);
+                              cudaStream_t st, const cudaAccessPolicyWindow* window = nullptr,
+                              bool pdl = false);
 bool cta_shape_supported(const CtaShape& s);
 CtaShape pick_cta_shape(uint32_t n, bool vec4_ok, bool vec2_ok);
 cudaError_t launch_tuned_cta(const CtaShape& s, int op, bool fast, const SpmmArgs& a,

@@ -36,6 +36,7 @@ def main():
     p.add_argument("--hub-threshold", type=int, default=0)
     p.add_argument("--reps", type=int, default=7)
     p.add_argument("--json", default=None)
+    p.add_argument("--only-shard", type=int, default=None, help="time only this shard index")
     args = p.parse_args()
     cfg = bench.CONFIGS[args.config]
     dev = torch.device("cuda", 0)
@@ -51,6 +52,8 @@ def main():
         bounds = D.partition_rows(a.row_ptr, g)
         times, descs = [], []
         for r in range(g):
+            if args.only_shard is not None and r != args.only_shard:
+                continue
             sh = D.shard_csr(a, bounds[r], bounds[r + 1]) if g > 1 else a
             d = G.DeviceCsr.from_host(sh, dev)
             c = torch.empty((sh.n_rows, n), dtype=torch.float32, device=dev)
