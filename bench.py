@@ -404,6 +404,44 @@ def run_ours(args, cfg):
     peak, peak_src = hbm_peak()
     traffic, traffic_src = ncu_traffic(args.config)
 
+    # gather ceilings on this box, now (outside the timed region): the same
+    # index stream through gespmm_diag_gather (one 512-B B row per nonzero into
+    # registers, no arithmetic/output/row structure), and every gather hitting
+    # one row (the L1/LSU data path alone).  N = 128 only (the diag kernel's).
+    gather_ceiling = None
+    if n == 128 and rank == 0 and not args.no_ceiling:
+        from paper_2007_03179_b200 import _lib as _L
+        Lg = _L.lib()
+        blocks = 148 * 3
+        sink = torch.empty(blocks * 256, dtype=torch.float32, device=dev)
+        cnt = shard.nnz()
+        res = {}
+        for name, idx in (("csr_order", d.col_ind), ("one_row", torch.zeros_like(d.col_ind))):
+            ts = []
+            for r in range(5):
+                l2_flush.zero_()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                rc = Lg.gespmm_diag_gather(idx.data_ptr(), cnt, bt.data_ptr(), n, sink.data_ptr(),
+                                           blocks, 1, stream.cuda_stream)
+                e1.record(stream)
+                torch.cuda.synchronize()
+                if rc != 0:
+                    raise RuntimeError(_L.last_error())
+                if r >= 2:
+                    ts.append(e0.elapsed_time(e1))
+            res[name] = round(float(statistics.median(ts)), 4)
+        kernel_ms = float(statistics.median(per_step_ms))
+        gather_ceiling = {
+            "bound": "L2->SM / LSU data path: one 512-B B row per nonzero",
+            "index_stream_ms": res["csr_order"], "one_row_ms": res["one_row"],
+            "kernel_median_ms": round(kernel_ms, 4),
+            "kernel_vs_index_stream": round(res["csr_order"] / kernel_ms, 3),
+            "kernel_vs_one_row": round(res["one_row"] / kernel_ms, 3),
+            "gathered_GBps": round(cnt * n * 4 / (kernel_ms * 1e-3) / 1e9, 1),
+            "note": "gespmm_diag_gather on the matrix's own col_ind (L2 flushed) and on an "
+                    "all-zero index stream (every gather an L1 hit); ratio > 1 = kernel faster"}
+
     # end to end: the C-ABI host-buffer call, pinned host buffers, H2D + D2H inside
     e2e = None
     if not args.no_e2e:
@@ -483,10 +521,11 @@ def run_ours(args, cfg):
                          "unit": "GB/s", "frac": round(achieved / peak, 4),
                          "traffic": traffic, "traffic_source": traffic_src,
                          "peak_source": peak_src,
-                         "kernel": "gespmm tuned SpMM step (warp-row kernel with the hub "
-                                   "row-per-CTA kernel on a side stream)",
+                         "kernel": "gespmm tuned SpMM step (warp-row kernel k_warp; hub "
+                                   "rows, if any, through k_hub alongside)",
                          "algorithmic_bytes": alg_bytes, "unique_cols": uniq,
                          "model": "4(M+1)+8nnz+4UN+4MN[+4MN arg], per step"},
+            "gather_ceiling": gather_ceiling,
             "gpu_launches": int(launches),
             "step_ms": {"min": round(min(per_step_ms), 4),
                         "median": round(statistics.median(per_step_ms), 4),
@@ -590,6 +629,7 @@ def main():
     p.add_argument("--no-flush", action="store_true", help="skip the L2 flush between steps")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
+    p.add_argument("--no-ceiling", action="store_true", help="skip the live gather-ceiling probe")
     args = p.parse_args()
     if args.warmup < 3:
         log("[bench] warmup raised to 3 (timing rules)")

@@ -88,7 +88,11 @@ def test_gcn_step_matches_dense_float64_reference(cuda):
     model = gcn.GCN(cfg, cuda)
     ht = torch.from_numpy(h).to(cuda)
     yt = torch.from_numpy(y).to(cuda)
-    z_ref, loss_ref, g1_ref, g2_ref = _dense_reference_step(a, h, y, model.w1, model.w2)
+    # the model pads W2 to 8 zero-filled columns (float4 SpMM lanes); the
+    # reference is the unpadded 7-class model
+    assert model.w2.shape[1] == cfg.classes_padded == 8
+    z_ref, loss_ref, g1_ref, g2_ref = _dense_reference_step(a, h, y, model.w1,
+                                                            model.w2[:, :cfg.classes])
     z = model.forward(ht, adj)
     assert torch.allclose(z.double().cpu(), z_ref, rtol=1e-4, atol=1e-4)
     w1_before = model.w1.detach().clone()
@@ -99,5 +103,6 @@ def test_gcn_step_matches_dense_float64_reference(cuda):
     # a few steps reduce the loss
     losses = [model.step(ht, yt, adj).item() for _ in range(10)]
     assert losses[-1] < loss.item()
+    assert (model.w2.detach()[:, cfg.classes:] == 0).all()  # padding never trains
     assert np.isfinite(losses).all()
     adj.close()
