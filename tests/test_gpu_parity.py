@@ -432,3 +432,42 @@ def test_rows_per_warp_shapes_keep_bits(rpw, n, cuda):
             assert first_divergence(c.data, want) is None, (op, a.n_rows)
             if want_arg:
                 assert np.array_equal(arg, warg), (op, a.n_rows)
+
+
+@pytest.mark.parametrize("share", ["small", "large"])
+@pytest.mark.parametrize("op", OPS)
+def test_hub_launch_modes_keep_bits(share, op, cuda):
+    """Hub rows carrying < 25% of the nonzeros run on the high-priority side
+    stream next to the warp kernel; >= 25% run first on the same stream with
+    the warp kernel as a programmatic dependent launch.  Both bit-exact, device
+    plans and the pipelined host entry."""
+    import torch
+    a, b = _powerlaw(6000, 400000, 5000, 29, 128)
+    deg = np.sort(np.diff(a.row_ptr.astype(np.int64)))[::-1]
+    cum = np.cumsum(deg) / deg.sum()
+    # threshold = degree of the row where the hub share crosses ~10% / ~60%
+    target = 0.10 if share == "small" else 0.60
+    thr = int(deg[int(np.searchsorted(cum, target))])
+    hub_share = deg[deg >= thr].sum() / deg.sum()
+    assert (hub_share < 0.25) if share == "small" else (hub_share >= 0.25)
+    want_arg = op in ("max", "min")
+    want, warg = _oracle(a, b, op, want_arg)
+    ex = G.ExecOptions(hub_threshold=thr)
+    c, arg = G.native_spmm_arg(a, b, G.KernelVariant.tuned(), G.reduce_op_by_name(op), exec=ex,
+                               want_arg=want_arg)
+    assert first_divergence(c.data, want) is None
+    if want_arg:
+        assert np.array_equal(arg, warg)
+    d = G.DeviceCsr.from_host(a, cuda)
+    bt = torch.from_numpy(b.data).to(cuda)
+    plan = G.Plan(d, 128, op, exec=ex)
+    assert f"hub_rows={int((np.diff(a.row_ptr.astype(np.int64)) >= thr).sum())}" in plan.description
+    c2 = torch.empty((a.n_rows, 128), device=cuda)
+    a2 = torch.empty((a.n_rows, 128), dtype=torch.int32, device=cuda) if want_arg else None
+    for _ in range(3):  # repeated launches reuse the persistent-launch counters
+        plan.execute(bt, c2, a2)
+    torch.cuda.synchronize()
+    assert first_divergence(c2.cpu().numpy(), want) is None
+    if want_arg:
+        assert np.array_equal(a2.cpu().numpy(), warg)
+    plan.close()
