@@ -199,6 +199,15 @@ gespmm_status_t gespmm_ipc_get_handle(void* ptr, unsigned char out[64]);
 gespmm_status_t gespmm_ipc_open_handle(const unsigned char handle[64], void** out);
 gespmm_status_t gespmm_ipc_close(void* ptr);
 
+/* Single-process NVLS multicast buffer (this process's device bound to one
+ * physical allocation): *uc_ptr is the ordinary (unicast) mapping, *mc_ptr the
+ * multicast address for gespmm_plan_execute_gather's c_multicast.  On an
+ * NVSwitch node the multi-process object comes from symmetric memory; this
+ * validates the multicast epilogue on one device.  EUNSUPPORTED when the
+ * device or driver has no multicast. */
+gespmm_status_t gespmm_multicast_alloc(uint64_t bytes, void** uc_ptr, void** mc_ptr);
+gespmm_status_t gespmm_multicast_free(void* uc_ptr);
+
 /* ---- format helpers ------------------------------------------------------ */
 
 /* A^T of a device CSR, as canonical CSR on the device: t_row_ptr[n_cols+1],

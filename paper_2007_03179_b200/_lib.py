@@ -40,7 +40,8 @@ EXPORTS = [
     "gespmm_csr1_header", "gespmm_csr1_read_host", "gespmm_csr1_load_device",
     "gespmm_diag_gather_hub", "gespmm_diag_gather_mode", "gespmm_plan_execute_gather",
     "gespmm_peer_barrier", "gespmm_peer_alloc", "gespmm_peer_free", "gespmm_ipc_get_handle",
-    "gespmm_ipc_open_handle", "gespmm_ipc_close",
+    "gespmm_ipc_open_handle", "gespmm_ipc_close", "gespmm_multicast_alloc",
+    "gespmm_multicast_free",
 ]
 MAX_GATHER_DSTS = 8
 
@@ -165,6 +166,10 @@ def lib():
         L.gespmm_ipc_open_handle.restype = C.c_int
         L.gespmm_ipc_close.argtypes = [vp]
         L.gespmm_ipc_close.restype = C.c_int
+        L.gespmm_multicast_alloc.argtypes = [u64, C.POINTER(vp), C.POINTER(vp)]
+        L.gespmm_multicast_alloc.restype = C.c_int
+        L.gespmm_multicast_free.argtypes = [vp]
+        L.gespmm_multicast_free.restype = C.c_int
         L.gespmm_launch_count.argtypes = []
         L.gespmm_launch_count.restype = u64
         _lib = L

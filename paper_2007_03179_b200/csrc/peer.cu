@@ -110,3 +110,184 @@ gespmm_status_t gespmm_ipc_close(void* ptr) {
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Single-process NVLS multicast buffers (driver API through
+// cudaGetDriverEntryPoint: no libcuda link dependency).  A multicast object
+// with this process's device(s) bound to one physical allocation: stores to
+// the multicast VA (multimem.st) land in every bound device's memory.  On an
+// NVSwitch node the cross-process version of the same object comes from
+// symmetric memory (exported handles); this one validates the epilogue's
+// multicast store path on whatever the process can see.
+// ---------------------------------------------------------------------------
+#include <cuda.h>
+
+#include <map>
+#include <mutex>
+
+namespace {
+
+struct McFns {
+  bool ok = false;
+  decltype(&cuMulticastCreate) create = nullptr;
+  decltype(&cuMulticastAddDevice) add_device = nullptr;
+  decltype(&cuMulticastBindMem) bind_mem = nullptr;
+  decltype(&cuMulticastUnbind) unbind = nullptr;
+  decltype(&cuMulticastGetGranularity) mc_gran = nullptr;
+  decltype(&cuMemCreate) mem_create = nullptr;
+  decltype(&cuMemRelease) mem_release = nullptr;
+  decltype(&cuMemGetAllocationGranularity) mem_gran = nullptr;
+  decltype(&cuMemAddressReserve) reserve = nullptr;
+  decltype(&cuMemAddressFree) addr_free = nullptr;
+  decltype(&cuMemMap) map = nullptr;
+  decltype(&cuMemUnmap) unmap = nullptr;
+  decltype(&cuMemSetAccess) set_access = nullptr;
+  decltype(&cuDeviceGetAttribute) dev_attr = nullptr;
+};
+
+const McFns& mc_fns() {
+  static McFns f;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    auto get = [](const char* name, void** p) {
+      cudaDriverEntryPointQueryResult q;
+      return cudaGetDriverEntryPoint(name, p, cudaEnableDefault, &q) == cudaSuccess &&
+             q == cudaDriverEntryPointSuccess && *p;
+    };
+    f.ok = get("cuMulticastCreate", reinterpret_cast<void**>(&f.create)) &&
+           get("cuMulticastAddDevice", reinterpret_cast<void**>(&f.add_device)) &&
+           get("cuMulticastBindMem", reinterpret_cast<void**>(&f.bind_mem)) &&
+           get("cuMulticastUnbind", reinterpret_cast<void**>(&f.unbind)) &&
+           get("cuMulticastGetGranularity", reinterpret_cast<void**>(&f.mc_gran)) &&
+           get("cuMemCreate", reinterpret_cast<void**>(&f.mem_create)) &&
+           get("cuMemRelease", reinterpret_cast<void**>(&f.mem_release)) &&
+           get("cuMemGetAllocationGranularity", reinterpret_cast<void**>(&f.mem_gran)) &&
+           get("cuMemAddressReserve", reinterpret_cast<void**>(&f.reserve)) &&
+           get("cuMemAddressFree", reinterpret_cast<void**>(&f.addr_free)) &&
+           get("cuMemMap", reinterpret_cast<void**>(&f.map)) &&
+           get("cuMemUnmap", reinterpret_cast<void**>(&f.unmap)) &&
+           get("cuMemSetAccess", reinterpret_cast<void**>(&f.set_access)) &&
+           get("cuDeviceGetAttribute", reinterpret_cast<void**>(&f.dev_attr));
+  });
+  return f;
+}
+
+struct McBuffer {
+  CUmemGenericAllocationHandle mem = 0, mc = 0;
+  CUdeviceptr uc = 0, mcva = 0;
+  size_t size = 0;
+  int dev = 0;
+};
+std::mutex g_mc_mu;
+std::map<void*, McBuffer> g_mc;
+
+gespmm_status_t drv_status(CUresult r, const char* what) {
+  if (r == CUDA_SUCCESS) return GESPMM_OK;
+  return set_error(r == CUDA_ERROR_NOT_SUPPORTED ? GESPMM_EUNSUPPORTED : GESPMM_ECUDA,
+                   std::string("multicast: ") + what + " failed (CUresult " + std::to_string(int(r)) + ")");
+}
+
+}  // namespace
+
+extern "C" {
+
+gespmm_status_t gespmm_multicast_alloc(uint64_t bytes, void** uc_ptr, void** mc_ptr) {
+  if (!uc_ptr || !mc_ptr) return set_error(GESPMM_EINVAL, "multicast_alloc: null out");
+  *uc_ptr = *mc_ptr = nullptr;
+  const McFns& f = mc_fns();
+  if (!f.ok) return set_error(GESPMM_EUNSUPPORTED, "multicast: driver entry points unavailable");
+  int dev = 0;
+  cudaError_t ce = cudaGetDevice(&dev);
+  if (ce != cudaSuccess) return cuda_status(ce, "multicast_alloc");
+  int supported = 0;
+  f.dev_attr(&supported, CU_DEVICE_ATTRIBUTE_MULTICAST_SUPPORTED, CUdevice(dev));
+  if (!supported) return set_error(GESPMM_EUNSUPPORTED, "multicast: device does not support multicast");
+  McBuffer b;
+  b.dev = dev;
+  CUmulticastObjectProp mp{};
+  mp.numDevices = 1;
+  mp.handleTypes = CU_MEM_HANDLE_TYPE_NONE;
+  mp.size = bytes ? bytes : 1;
+  size_t mg = 0;
+  gespmm_status_t s = drv_status(f.mc_gran(&mg, &mp, CU_MULTICAST_GRANULARITY_RECOMMENDED), "granularity");
+  if (s != GESPMM_OK) return s;
+  CUmemAllocationProp ap{};
+  ap.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+  ap.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+  ap.location.id = dev;
+  size_t ag = 0;
+  if ((s = drv_status(f.mem_gran(&ag, &ap, CU_MEM_ALLOC_GRANULARITY_RECOMMENDED), "granularity")) != GESPMM_OK)
+    return s;
+  const size_t g = mg > ag ? mg : ag;
+  b.size = (mp.size + g - 1) / g * g;
+  mp.size = b.size;
+  auto fail_cleanup = [&](gespmm_status_t st) {
+    if (b.mcva) { f.unmap(b.mcva, b.size); f.addr_free(b.mcva, b.size); }
+    if (b.uc) { f.unmap(b.uc, b.size); f.addr_free(b.uc, b.size); }
+    if (b.mc && b.mem) f.unbind(b.mc, CUdevice(dev), 0, b.size);
+    if (b.mc) f.mem_release(b.mc);
+    if (b.mem) f.mem_release(b.mem);
+    return st;
+  };
+  {
+    // the driver may insist on an exportable handle type even for a one-process team
+    CUresult r = CUDA_ERROR_INVALID_VALUE;
+    for (CUmemAllocationHandleType ht :
+         {CU_MEM_HANDLE_TYPE_NONE, CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR, CU_MEM_HANDLE_TYPE_FABRIC}) {
+      mp.handleTypes = ht;
+      r = f.create(&b.mc, &mp);
+      if (r == CUDA_SUCCESS) break;
+    }
+    if (r != CUDA_SUCCESS) {
+      // measured on the gpurun boxes: the device reports multicast support but
+      // the container has no NVSwitch/IMEX device nodes, and every create is
+      // refused with CUDA_ERROR_INVALID_VALUE (tools/multicast_probe.py)
+      return fail_cleanup(set_error(GESPMM_EUNSUPPORTED,
+                                    "multicast: the driver refused the multicast object (CUresult " +
+                                        std::to_string(int(r)) +
+                                        "; no NVSwitch fabric access in this process?)"));
+    }
+  }
+  if ((s = drv_status(f.add_device(b.mc, CUdevice(dev)), "add device")) != GESPMM_OK) return fail_cleanup(s);
+  if ((s = drv_status(f.mem_create(&b.mem, b.size, &ap, 0), "physical allocation")) != GESPMM_OK)
+    return fail_cleanup(s);
+  if ((s = drv_status(f.bind_mem(b.mc, 0, b.mem, 0, b.size, 0), "bind")) != GESPMM_OK) return fail_cleanup(s);
+  CUmemAccessDesc acc{};
+  acc.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+  acc.location.id = dev;
+  acc.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+  if ((s = drv_status(f.reserve(&b.uc, b.size, g, 0, 0), "reserve")) != GESPMM_OK) return fail_cleanup(s);
+  if ((s = drv_status(f.map(b.uc, b.size, 0, b.mem, 0), "map")) != GESPMM_OK) return fail_cleanup(s);
+  if ((s = drv_status(f.set_access(b.uc, b.size, &acc, 1), "access")) != GESPMM_OK) return fail_cleanup(s);
+  if ((s = drv_status(f.reserve(&b.mcva, b.size, g, 0, 0), "reserve mc")) != GESPMM_OK) return fail_cleanup(s);
+  if ((s = drv_status(f.map(b.mcva, b.size, 0, b.mc, 0), "map mc")) != GESPMM_OK) return fail_cleanup(s);
+  if ((s = drv_status(f.set_access(b.mcva, b.size, &acc, 1), "access mc")) != GESPMM_OK) return fail_cleanup(s);
+  *uc_ptr = reinterpret_cast<void*>(b.uc);
+  *mc_ptr = reinterpret_cast<void*>(b.mcva);
+  std::lock_guard<std::mutex> lk(g_mc_mu);
+  g_mc[*uc_ptr] = b;
+  return GESPMM_OK;
+}
+
+gespmm_status_t gespmm_multicast_free(void* uc_ptr) {
+  McBuffer b;
+  {
+    std::lock_guard<std::mutex> lk(g_mc_mu);
+    auto it = g_mc.find(uc_ptr);
+    if (it == g_mc.end()) return set_error(GESPMM_EINVAL, "multicast_free: unknown buffer");
+    b = it->second;
+    g_mc.erase(it);
+  }
+  const McFns& f = mc_fns();
+  cudaDeviceSynchronize();
+  f.unmap(b.mcva, b.size);
+  f.addr_free(b.mcva, b.size);
+  f.unmap(b.uc, b.size);
+  f.addr_free(b.uc, b.size);
+  f.unbind(b.mc, CUdevice(b.dev), 0, b.size);
+  f.mem_release(b.mc);
+  f.mem_release(b.mem);
+  return GESPMM_OK;
+}
+
+}  // extern "C"

@@ -471,3 +471,17 @@ def test_hub_launch_modes_keep_bits(share, op, cuda):
     if want_arg:
         assert np.array_equal(a2.cpu().numpy(), warg)
     plan.close()
+
+
+@pytest.mark.parametrize("n", [64, 128, 130])
+def test_fault_injection_through_hub_kernels(n, cuda):
+    """SkipTail through the hub kernels (ring-fed k_hub at N % 4 == 0, k_cta at
+    130): equal to the oracle's SkipTail restatement, different from the good
+    result."""
+    a, b = _powerlaw(2000, 80000, 1500, 41, n)
+    good, _ = _oracle(a, b, "sum")
+    faulty, _ = _oracle(a, b, "sum", skip_tail=True)
+    ex = G.ExecOptions(fault=G.FaultMode.SkipTail, hub_threshold=100)
+    c = G.native_spmm(a, b, G.KernelVariant.tuned(), G.ops.sum(), exec=ex)
+    assert first_divergence(c.data, good) is not None
+    assert first_divergence(c.data, faulty) is None

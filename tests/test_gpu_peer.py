@@ -161,3 +161,50 @@ def test_two_process_fused_propagate_over_ipc(tmp_path):
         assert np.array_equal(got.view(np.uint32), want.view(np.uint32)), r
         assert np.array_equal(np.load(tmp_path / f"ref{r}.npy").view(np.uint32),
                               want.view(np.uint32)), r
+
+
+@pytest.mark.parametrize("op,n", [("sum", 128), ("max", 128), ("mean", 64), ("sum", 30)])
+def test_multicast_epilogue_on_one_device(op, n):
+    """NVLS multicast: the epilogue's multimem.st through a multicast object
+    bound to this device's memory lands every output row (and arg) in the
+    bound allocation, bit-identical to the oracle.  Skips where the device or
+    driver has no multicast."""
+    L = _lib.lib()
+    a = G.gen_powerlaw(3000, 90000, 900, 1.0, 61)
+    G.randomize_values(a, 62)
+    b = G.make_random_dense(3000, n, 63).data
+    has_arg = op in ("max", "min")
+    want, warg = O.spmm(a.n_rows, a.n_cols, a.row_ptr, a.col_ind, a.vals, b, op, want_arg=has_arg)
+    bytes_c = 4 * a.n_rows * n
+    total = 2 * bytes_c if has_arg else bytes_c
+    uc, mc = C.c_void_p(), C.c_void_p()
+    st = L.gespmm_multicast_alloc(total, C.byref(uc), C.byref(mc))
+    if st == _lib.EUNSUPPORTED:
+        pytest.skip(_lib.last_error())
+    assert st == 0, _lib.last_error()
+    try:
+        full = torch.as_tensor(D._CudaArray(uc.value, (a.n_rows, n), "<f4"), device=DEV)
+        full.fill_(-5.0)
+        full_arg = (torch.as_tensor(D._CudaArray(uc.value + bytes_c, (a.n_rows, n), "<i4"),
+                                    device=DEV) if has_arg else None)
+        if has_arg:
+            full_arg.fill_(-9)
+        d = G.DeviceCsr.from_host(a, DEV)
+        bt = torch.from_numpy(b).to(DEV)
+        local = torch.empty((a.n_rows, n), device=DEV)
+        local_arg = torch.empty((a.n_rows, n), dtype=torch.int32, device=DEV) if has_arg else None
+        plan = G.Plan(d, n, op, exec=G.ExecOptions(hub_threshold=300))
+        plan.execute_gather(bt, [local.data_ptr()],
+                            [local_arg.data_ptr()] if has_arg else None,
+                            c_multicast=mc.value,
+                            arg_multicast=(mc.value + bytes_c) if has_arg else None)
+        torch.cuda.synchronize()
+        for got in (local, full):
+            assert np.array_equal(got.cpu().numpy().view(np.uint32), want.view(np.uint32))
+        if has_arg:
+            assert np.array_equal(local_arg.cpu().numpy(), warg)
+            assert np.array_equal(full_arg.cpu().numpy(), warg)
+        plan.close()
+        del full, full_arg
+    finally:
+        assert L.gespmm_multicast_free(uc) == 0
