@@ -347,7 +347,7 @@ def run_ours(args, cfg):
     ex = G.ExecOptions(hub_threshold=args.hub_threshold, exact=not args.fast,
                        l2_persist=args.l2_persist, l2_hints=hints, l2_hot_mb=args.l2_hot_mb,
                        tuned_cf=args.tuned_cf, col_slices=args.col_slices,
-                       rows_per_warp=args.rows_per_warp)
+                       rows_per_warp=args.rows_per_warp, cluster_hot=args.cluster_hot)
     variant = G.variant_by_name(args.variant, args.cf)
     plan = G.Plan(d, n, op, variant=variant, exec=ex)
     log(f"[bench] rank {rank}: rows [{info.lo},{info.hi}) nnz {shard.nnz()} plan: {plan.description}")
@@ -630,6 +630,8 @@ def main():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--no-ceiling", action="store_true", help="skip the live gather-ceiling probe")
+    p.add_argument("--cluster-hot", type=int, default=0,
+                   help="N=128: hot B rows in cluster DSMEM, cluster size 2/4/8/16 (0 off)")
     args = p.parse_args()
     if args.warmup < 3:
         log("[bench] warmup raised to 3 (timing rules)")

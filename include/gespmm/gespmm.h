@@ -106,7 +106,11 @@ typedef struct {
                          S >= 2 explicit */
   int32_t rows_per_warp; /* TUNED plans: rows sharing a warp when N <= 256 (float4 lanes): 0 =
                          auto (4 for low-degree matrices, else as N dictates), 1, 2, 4 or 8 */
-  int32_t reserved[3];
+  int32_t cluster_hot; /* TUNED plans, N = 128: keep the most-gathered B rows in the distributed
+                         shared memory of thread-block clusters of this many CTAs (2, 4, 8 or
+                         16; one CTA per SM, 416 rows each) and gather them over DSMEM; the plan
+                         keeps a remapped copy of col_ind.  0 = off (default) */
+  int32_t reserved[2];
 } gespmm_options_t;
 
 void gespmm_options_default(gespmm_options_t* opts);

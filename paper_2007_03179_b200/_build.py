@@ -29,7 +29,7 @@ CXX_FLAGS = ["-O3", "-std=c++17", "-fPIC", "-ffp-contract=off", "-Wall", "-Wextr
              "-I", INCLUDE, "-I", CSRC, "-I", "/usr/local/cuda/include"]
 
 CU_SOURCES = ["api.cu", "validate.cu", "kernels_faithful.cu", "kernels_tuned.cu", "diag.cu",
-              "transpose.cu", "hotcols.cu", "peer.cu"]
+              "transpose.cu", "hotcols.cu", "peer.cu", "cluster.cu"]
 CXX_SOURCES = ["gen.cpp", "io.cpp"]
 HEADERS = ["common.cuh", "launch.h"]
 

@@ -298,6 +298,7 @@ class ExecOptions:
     tuned_cf: int = 0               # tuned warp kernel merge factor (1/2/4), 0 auto
     col_slices: int = 0             # slice-major column traversal: 0 auto, 1 off, S slices
     rows_per_warp: int = 0          # rows sharing a warp (float4 lanes, N <= 256): 0 auto
+    cluster_hot: int = 0            # N = 128 plans: hot B rows in cluster DSMEM (cluster size), 0 off
 
 
 def _options(variant: KernelVariant, ex: ExecOptions, validate: bool = True) -> _lib.Options:
@@ -308,7 +309,7 @@ def _options(variant: KernelVariant, ex: ExecOptions, validate: bool = True) -> 
                            l2_hints=int(ex.l2_hints), hub_threshold=ex.hub_threshold,
                            l2_persist=int(ex.l2_persist), l2_hot_mb=int(ex.l2_hot_mb),
                            tuned_cf=int(ex.tuned_cf), col_slices=int(ex.col_slices),
-                           rows_per_warp=int(ex.rows_per_warp))
+                           rows_per_warp=int(ex.rows_per_warp), cluster_hot=int(ex.cluster_hot))
 
 
 # ---------------------------------------------------------------------------

@@ -85,6 +85,9 @@ gespmm_status_t validation_status(const ValidateResult& r, uint32_t m, uint32_t 
 }
 
 gespmm_status_t check_opts(const gespmm_options_t& o) {
+  if (o.cluster_hot != 0 && o.cluster_hot != 2 && o.cluster_hot != 4 && o.cluster_hot != 8 &&
+      o.cluster_hot != 16)
+    return fail(GESPMM_EINVAL, "cluster_hot must be 0, 2, 4, 8 or 16");
   if (o.variant < GESPMM_VARIANT_TUNED || o.variant > GESPMM_VARIANT_CRC_CWM)
     return fail(GESPMM_EINVAL, "unknown kernel variant " + std::to_string(o.variant) +
                                    " (naive, crc, crc-cwm, tuned)");
@@ -154,8 +157,10 @@ struct Plan {
   std::string desc;
   uint32_t max_degree = 0;
   double mean_degree = 0.0;
+  ClusterHot ch;             // cluster-DSMEM hot-row cache (o.cluster_hot), col_ind copy
 
   ~Plan() {
+    free_cluster_hot(&ch);
     if (d_order) cudaFree(d_order);
     if (d_hot) cudaFree(d_hot);
     if (ev_fork) cudaEventDestroy(ev_fork);
@@ -396,6 +401,17 @@ gespmm_status_t build_tuned(Plan& p, const uint32_t* host_rp, cudaStream_t st) {
     GESPMM_CUDA(cudaEventCreateWithFlags(&p.ev_fork, cudaEventDisableTiming), "plan_create");
     GESPMM_CUDA(cudaEventCreateWithFlags(&p.ev_join, cudaEventDisableTiming), "plan_create");
   }
+  if (p.o.cluster_hot > 0 && p.n == 128 && p.a.nnz) {
+    // every row goes through the cluster kernel (LPT order, persistent warps)
+    if (!p.d_order && m) {
+      GESPMM_CUDA(cudaMalloc(reinterpret_cast<void**>(&p.d_order), sizeof(uint32_t) * m),
+                  "plan_create");
+      GESPMM_CUDA(cudaMemcpyAsync(p.d_order, order.data(), sizeof(uint32_t) * m,
+                                  cudaMemcpyHostToDevice, st), "plan_create");
+    }
+    GESPMM_CUDA(build_cluster_hot(p.a.col_ind, p.a.nnz, p.a.n_cols, p.o.cluster_hot, st, &p.ch),
+                "plan_create");
+  }
   const uint64_t hot_budget = hot_budget_bytes(p.o, p.a.n_cols, p.n, p.device);
   if (hot_budget && p.o.l2_hints && p.a.nnz) {
     GESPMM_CUDA(build_hot_bitmap(p.a.col_ind, p.a.nnz, p.a.n_cols,
@@ -420,6 +436,12 @@ gespmm_status_t build_tuned(Plan& p, const uint32_t* host_rp, cudaStream_t st) {
     std::snprintf(buf + len, sizeof buf - size_t(len), "; %s",
                   identity ? "identity order" : "degree-sorted (LPT) order");
   len = int(std::strlen(buf));
+  if (p.ch.col_ind && size_t(len) < sizeof buf) {
+    std::snprintf(buf + len, sizeof buf - size_t(len),
+                  "; cluster DSMEM cache: %u hot rows in clusters of %d = %.1f%% of gathers",
+                  p.ch.n_hot, p.ch.cs, 100.0 * p.ch.hot_nnz_frac);
+    len = int(std::strlen(buf));
+  }
   if (p.sh.slices > 1 && size_t(len) < sizeof buf)
     std::snprintf(buf + len, sizeof buf - size_t(len), "; %u column slices of %u", p.sh.slices, sw);
   p.desc = buf;
@@ -529,6 +551,15 @@ gespmm_status_t plan_execute_impl(Plan& p, const float* b, float* c, int32_t* ar
     return GESPMM_OK;
   }
   args.ld = p.n;
+  if (p.ch.col_ind && aligned(b, 16) && aligned(c, 16) && (!arg || aligned(arg, 16))) {
+    args.order = p.d_order;
+    args.n_sched = p.a.n_rows;
+    args.n_tiles = 1;
+    GESPMM_CUDA(resolve_policies(&args, st), "spmm");
+    int clusters = 0;
+    GESPMM_CUDA(launch_cluster_warp(p.ch, p.op, fast, args, st, &clusters), "spmm");
+    return GESPMM_OK;
+  }
   cudaAccessPolicyWindow win{};
   const cudaAccessPolicyWindow* winp = nullptr;
   if (p.o.l2_persist == 2) persist_limits(p.device);  // set-aside only, no window

@@ -75,6 +75,23 @@ cudaError_t build_hot_bitmap(const uint32_t* col_ind, uint64_t nnz, uint32_t k,
                              uint64_t budget_rows, cudaStream_t st, uint32_t** out_bits,
                              HotStats* stats);
 
+// --- cluster-DSMEM hot-row cache (cluster.cu) ---
+struct ClusterHot {
+  uint32_t* col_ind = nullptr;   // remapped col_ind: hot columns = (1 << 31) | slot
+  uint32_t* hot_list = nullptr;  // slot -> column
+  uint32_t n_hot = 0;
+  uint32_t* counter = nullptr;   // persistent row-unit counter
+  int cs = 0;                    // cluster size (CTAs, one per SM)
+  double hot_nnz_frac = 0.0;
+};
+uint32_t cluster_hot_rows(int cs);
+cudaError_t build_cluster_hot(const uint32_t* col_ind, uint64_t nnz, uint32_t k, int cs,
+                              cudaStream_t st, ClusterHot* out);
+void free_cluster_hot(ClusterHot* h);
+// N == 128, 16-byte aligned B/C; a.order/n_sched = every row (LPT order).
+cudaError_t launch_cluster_warp(const ClusterHot& h, int op, bool fast, const SpmmArgs& a,
+                                cudaStream_t st, int* clusters);
+
 // Device canonical check of a device CSR, formatted as the reference's
 // require_canonical(m, who) error (csr.hpp:155-158).  Synchronises `st`.
 gespmm_status_t validate_device_as(const gespmm_csr_t* a, cudaStream_t st, const char* who);

@@ -485,3 +485,31 @@ def test_fault_injection_through_hub_kernels(n, cuda):
     c = G.native_spmm(a, b, G.KernelVariant.tuned(), G.ops.sum(), exec=ex)
     assert first_divergence(c.data, good) is not None
     assert first_divergence(c.data, faulty) is None
+
+
+@pytest.mark.parametrize("cs", [2, 8, 16])
+@pytest.mark.parametrize("op", OPS)
+def test_cluster_dsmem_hot_rows_keep_bits(cs, op, cuda):
+    """cluster_hot: the most-gathered B rows live in the distributed shared
+    memory of CS-CTA clusters and hot gathers go over DSMEM (remapped col_ind);
+    every op with edge and column args bit-identical, repeated launches."""
+    import torch
+    a, b = _powerlaw(20000, 1500000, 9000, 51, 128)
+    want_arg = op in ("max", "min")
+    d = G.DeviceCsr.from_host(a, cuda)
+    bt = torch.from_numpy(b.data).to(cuda)
+    for arg_kind in (("edge", "column") if want_arg else ("edge",)):
+        want, warg = _oracle(a, b, op, want_arg,
+                             arg_kind=O.ARG_COLUMN if arg_kind == "column" else O.ARG_EDGE)
+        plan = G.Plan(d, 128, op, exec=G.ExecOptions(cluster_hot=cs, arg_kind=arg_kind))
+        assert "cluster DSMEM cache" in plan.description, plan.description
+        c = torch.empty((a.n_rows, 128), device=cuda)
+        arg = torch.empty((a.n_rows, 128), dtype=torch.int32, device=cuda) if want_arg else None
+        for _ in range(2):
+            c.fill_(-1.0)
+            plan.execute(bt, c, arg)
+            torch.cuda.synchronize()
+            assert first_divergence(c.cpu().numpy(), want) is None, (cs, op, arg_kind)
+            if want_arg:
+                assert np.array_equal(arg.cpu().numpy(), warg), (cs, op, arg_kind)
+        plan.close()
