@@ -641,6 +641,22 @@ cudaError_t launch_ex(K kernel, dim3 g, dim3 b, cudaStream_t st, const SpmmArgs&
   return cudaLaunchKernelEx(&cfg, kernel, a);
 }
 
+// Shared-memory carve-out preference for the warp kernel (percent of the
+// unified L1/shared array; GESPMM_WARP_CARVEOUT, <0 = driver default).
+int warp_carveout() {
+  static const int v = [] {
+    const char* e = std::getenv("GESPMM_WARP_CARVEOUT");
+    return e ? std::atoi(e) : -1;
+  }();
+  return v;
+}
+
+template <class K>
+void apply_carveout(K kernel) {
+  const int c = warp_carveout();
+  if (c >= 0) cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, c);
+}
+
 template <int OP, bool FAST>
 cudaError_t warp_dispatch(const WarpShape& s, const SpmmArgs& a, cudaStream_t st,
                           const cudaAccessPolicyWindow* window, bool pdl) {
@@ -655,6 +671,7 @@ cudaError_t warp_dispatch(const WarpShape& s, const SpmmArgs& a, cudaStream_t st
   if (s.vec == V && s.lpr == L && s.cf == F) {                                               \
     constexpr bool kHotShape = L == 32; /* hot-column map on full-warp rows only */          \
     const dim3 g{uint32_t(blocks)};                                                          \
+    apply_carveout(k_warp<OP, FAST, V, L, F, false>);                                        \
     const cudaError_t e =                                                                    \
         (kHotShape && a.hot) ? launch_ex(k_warp<OP, FAST, V, L, F, kHotShape>, g, b, st, a, window, pdl) \
                              : launch_ex(k_warp<OP, FAST, V, L, F, false>, g, b, st, a, window, pdl); \
