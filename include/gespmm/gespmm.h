@@ -110,7 +110,10 @@ typedef struct {
                          shared memory of thread-block clusters of this many CTAs (2, 4, 8 or
                          16; one CTA per SM, 416 rows each) and gather them over DSMEM; the plan
                          keeps a remapped copy of col_ind.  0 = off (default) */
-  int32_t reserved[2];
+  int32_t h2d_pack;   /* gespmm_spmm_host: send col_ind as 16-bit row-gap codes (lossless, escapes
+                         for large gaps) and rebuild it on the device: 0 = auto (>= 8M nonzeros),
+                         1 = on, -1 = off */
+  int32_t reserved[1];
 } gespmm_options_t;
 
 void gespmm_options_default(gespmm_options_t* opts);

@@ -29,8 +29,8 @@ CXX_FLAGS = ["-O3", "-std=c++17", "-fPIC", "-ffp-contract=off", "-Wall", "-Wextr
              "-I", INCLUDE, "-I", CSRC, "-I", "/usr/local/cuda/include"]
 
 CU_SOURCES = ["api.cu", "validate.cu", "kernels_faithful.cu", "kernels_tuned.cu", "diag.cu",
-              "transpose.cu", "hotcols.cu", "peer.cu", "cluster.cu"]
-CXX_SOURCES = ["gen.cpp", "io.cpp"]
+              "transpose.cu", "hotcols.cu", "peer.cu", "cluster.cu", "h2dpack.cu"]
+CXX_SOURCES = ["gen.cpp", "io.cpp", "h2dpack_host.cpp"]
 HEADERS = ["common.cuh", "launch.h"]
 
 
@@ -68,6 +68,8 @@ def build(verbose: bool = False, force: bool = False, defines=(), build_dir=None
                     cmd += ["-Xptxas", "-v"]
             else:
                 cmd = ["g++"] + CXX_FLAGS + [f"-D{d}" for d in defines] + ["-c", path, "-o", obj]
+                if src == "h2dpack_host.cpp":
+                    cmd.insert(1, "-fopenmp")
             jobs.append(cmd)
     log = []
     if jobs:
@@ -77,7 +79,7 @@ def build(verbose: bool = False, force: bool = False, defines=(), build_dir=None
                     log.append(out)
     if force or jobs or _stale(LIB, objs):
         _run([NVCC] + ARCH + ["-shared", "-cudart", "static", "-o", LIB] + objs +
-             ["-lpthread"])
+             ["-lgomp", "-lpthread"])
     text = "\n".join(log)
     if verbose and text:
         print(text, file=sys.stderr)

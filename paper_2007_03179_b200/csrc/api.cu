@@ -625,8 +625,13 @@ struct Workspace {
   cudaStream_t side = nullptr;  // hub-row kernels next to the warp kernel of a block
   cudaEvent_t ev_b = nullptr, ev_in[kMaxChunks] = {}, ev_done[kMaxChunks] = {};
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
-  void* buf[8] = {};   // row_ptr, col_ind, vals, B, C, arg, order, validation scratch
-  size_t cap[8] = {};
+  // device: row_ptr, col_ind, vals, B, C, arg, order, validation scratch +
+  // row-start bitmap, packed codes, packed exceptions, scan temp
+  void* buf[11] = {};
+  size_t cap[11] = {};
+  // pinned host staging: packed codes, packed exceptions, row schedule
+  void* hbuf[3] = {};
+  size_t hcap[3] = {};
   cudaError_t reserve(int i, size_t bytes) {
     if (bytes <= cap[i]) return cudaSuccess;
     if (buf[i]) cudaFree(buf[i]);
@@ -634,6 +639,15 @@ struct Workspace {
     cap[i] = 0;
     cudaError_t e = cudaMalloc(&buf[i], bytes);
     if (e == cudaSuccess) cap[i] = bytes;
+    return e;
+  }
+  cudaError_t reserve_host(int i, size_t bytes) {
+    if (bytes <= hcap[i]) return cudaSuccess;
+    if (hbuf[i]) cudaFreeHost(hbuf[i]);
+    hbuf[i] = nullptr;
+    hcap[i] = 0;
+    cudaError_t e = cudaHostAlloc(&hbuf[i], bytes, cudaHostAllocDefault);
+    if (e == cudaSuccess) hcap[i] = bytes;
     return e;
   }
 };
@@ -929,7 +943,9 @@ gespmm_status_t gespmm_spmm_host(const gespmm_csr_t* a, const float* b, uint32_t
   // ---- row blocks balanced by nnz (binary search on the host row_ptr)
   // pipeline depth: more blocks shrink the un-overlapped tail (last block's
   // kernel + C copy-out); 16 measured best at Reddit size (20.0 vs 20.6 ms at 8)
-  int chunks = nnz >= (uint64_t(32) << 20) ? 16 : (nnz >= (uint64_t(8) << 20) ? 8 : 1);
+  // (the paper's Alg. 1-3 kernels keep 8: their hub rows bound every block)
+  const bool tuned_v = o.variant == GESPMM_VARIANT_TUNED;
+  int chunks = (tuned_v && nnz >= (uint64_t(32) << 20)) ? 16 : (nnz >= (uint64_t(8) << 20) ? 8 : 1);
   if (const char* e = std::getenv("GESPMM_CHUNKS")) {  // pipeline depth experiments
     const int v = std::atoi(e);
     if (v >= 1 && v <= kMaxChunks && nnz >= uint64_t(v)) chunks = v;
@@ -960,7 +976,8 @@ gespmm_status_t gespmm_spmm_host(const gespmm_csr_t* a, const float* b, uint32_t
                : (ht < 0 ? 0xffffffffu
                          : auto_hub_threshold(shapes.slice_w, nnz / uint64_t(chunks),
                                               shapes.warp_v.cf, a->n_cols, dev));
-    std::vector<uint32_t> order(m);
+    GESPMM_CUDA(ws->reserve_host(2, sizeof(uint32_t) * m), "spmm");
+    uint32_t* order = static_cast<uint32_t*>(ws->hbuf[2]);  // pinned: no sync after its copy
     uint32_t maxd = 0;
     for (uint64_t r = 0; r < m; ++r) maxd = std::max(maxd, a->row_ptr[r + 1] - a->row_ptr[r]);
     std::vector<uint32_t> count(size_t(maxd) + 2);
@@ -983,34 +1000,86 @@ gespmm_status_t gespmm_spmm_host(const gespmm_csr_t* a, const float* b, uint32_t
         }
       }
     }
-    GESPMM_CUDA(cudaMemcpyAsync(d_order, order.data(), sizeof(uint32_t) * m,
-                                cudaMemcpyHostToDevice, ws->in), "spmm");
-    // order[] lives in a host vector: wait for that copy before it goes away
-    GESPMM_CUDA(cudaStreamSynchronize(ws->in), "spmm");
+    GESPMM_CUDA(cudaMemcpyAsync(d_order, order, sizeof(uint32_t) * m, cudaMemcpyHostToDevice,
+                                ws->in), "spmm");
   }
   tr.mark("row_ptr+B enqueued, schedule built");
   tr.dev("row_ptr + B (+ order) landed", ws->in);
   GESPMM_CUDA(cudaEventRecord(ws->ev_b, ws->in), "spmm");
   GESPMM_CUDA(cudaStreamWaitEvent(ws->stream, ws->ev_b, 0), "spmm");
-  ColCheck* cc = nullptr;
-  if (o.validate && nnz) {
-    GESPMM_CUDA(ws->reserve(7, colcheck_workspace_bytes(nnz)), "spmm");
-    GESPMM_CUDA(colcheck_begin(&cc, nnz, ws->buf[7], ws->stream), "spmm");
+  // packed column indices on the upload (h2dpack.cu): auto for large inputs
+  bool pack = o.h2d_pack > 0 || (o.h2d_pack == 0 && nnz >= (uint64_t(8) << 20));
+  if (const char* e = std::getenv("GESPMM_H2D_PACK")) pack = std::atoi(e) != 0;
+  // the encoder walks the host row_ptr: only once it is known to be sound
+  // (validate=1 checked it above; otherwise a silent pass decides)
+  const bool rp_sound = o.validate || host_rowptr_status(a, "spmm") == GESPMM_OK;
+  pack = pack && rp_sound && nnz > 0 && nnz < 0x7fffffffull;
+  uint16_t *h_enc = nullptr, *d_enc = nullptr;
+  uint32_t *h_exc = nullptr, *d_exc = nullptr, *bits = nullptr;
+  void* scan_tmp = nullptr;
+  size_t scan_bytes = 0;
+  if (pack) {
+    uint64_t max_blk = 0;
+    for (int ch = 0; ch < chunks; ++ch)
+      max_blk = std::max<uint64_t>(max_blk, a->row_ptr[bound[ch + 1]] - a->row_ptr[bound[ch]]);
+    scan_bytes = unpack_temp_bytes(max_blk);
+    GESPMM_CUDA(ws->reserve_host(0, sizeof(uint16_t) * nnz), "spmm");
+    GESPMM_CUDA(ws->reserve_host(1, sizeof(uint32_t) * (nnz / 4 + 2)), "spmm");
+    GESPMM_CUDA(ws->reserve(8, sizeof(uint16_t) * nnz), "spmm");
+    GESPMM_CUDA(ws->reserve(9, sizeof(uint32_t) * (nnz / 4 + 2)), "spmm");
+    GESPMM_CUDA(ws->reserve(10, std::max<size_t>(scan_bytes, 1)), "spmm");
+    h_enc = static_cast<uint16_t*>(ws->hbuf[0]);
+    h_exc = static_cast<uint32_t*>(ws->hbuf[1]);
+    d_enc = static_cast<uint16_t*>(ws->buf[8]);
+    d_exc = static_cast<uint32_t*>(ws->buf[9]);
+    scan_tmp = ws->buf[10];
   }
+  ColCheck* cc = nullptr;
+  if ((o.validate || pack) && nnz) {
+    GESPMM_CUDA(ws->reserve(7, colcheck_workspace_bytes(nnz)), "spmm");
+    bits = reinterpret_cast<uint32_t*>(static_cast<char*>(ws->buf[7]) + 256);
+    if (o.validate)
+      GESPMM_CUDA(colcheck_begin(&cc, nnz, ws->buf[7], ws->stream), "spmm");
+    else
+      GESPMM_CUDA(cudaMemsetAsync(bits, 0, sizeof(uint32_t) * (nnz / 32 + 1), ws->stream), "spmm");
+  }
+  uint64_t exc_off = 0;  // exception pairs used so far
 
   const bool fast = o.exact == 0;
   for (int ch = 0; ch < chunks; ++ch) {
     const uint32_t lo = bound[ch], hi = bound[ch + 1];
     const uint64_t ps = a->row_ptr[lo], pe = a->row_ptr[hi];
-    if (pe > ps) {
+    uint64_t nexc = UINT64_MAX;  // exceptions of this block when it travels packed
+    if (pe > ps && pack) {
+      tr.mark("pack block");
+      nexc = pack_cols_block(a->row_ptr, a->col_ind, lo, hi, h_enc + ps, h_exc + 2 * exc_off,
+                             (pe - ps) / 8);
+    }
+    if (pe > ps && nexc != UINT64_MAX) {
+      GESPMM_CUDA(cudaMemcpyAsync(d_enc + ps, h_enc + ps, sizeof(uint16_t) * (pe - ps),
+                                  cudaMemcpyHostToDevice, ws->in), "spmm");
+      if (nexc)
+        GESPMM_CUDA(cudaMemcpyAsync(d_exc + 2 * exc_off, h_exc + 2 * exc_off,
+                                    sizeof(uint32_t) * 2 * nexc, cudaMemcpyHostToDevice, ws->in),
+                    "spmm");
+    } else if (pe > ps) {
       GESPMM_CUDA(cudaMemcpyAsync(d_ci + ps, a->col_ind + ps, sizeof(uint32_t) * (pe - ps),
                                   cudaMemcpyHostToDevice, ws->in), "spmm");
+    }
+    if (pe > ps) {
       GESPMM_CUDA(cudaMemcpyAsync(d_v + ps, a->vals + ps, sizeof(float) * (pe - ps),
                                   cudaMemcpyHostToDevice, ws->in), "spmm");
     }
     tr.dev("block " + std::to_string(ch) + " CSR landed", ws->in);
     GESPMM_CUDA(cudaEventRecord(ws->ev_in[ch], ws->in), "spmm");
     GESPMM_CUDA(cudaStreamWaitEvent(ws->stream, ws->ev_in[ch], 0), "spmm");
+    if (pe > ps && nexc != UINT64_MAX) {
+      GESPMM_CUDA(unpack_cols(d_enc + ps, reinterpret_cast<const uint2*>(d_exc + 2 * exc_off),
+                              uint32_t(nexc), d_rp + lo, hi - lo, ps, pe, nnz, bits, d_ci,
+                              scan_tmp, scan_bytes, ws->stream),
+                  "spmm");
+      exc_off += nexc;
+    }
     if (cc)
       GESPMM_CUDA(colcheck_rows(cc, d_rp + lo, hi - lo, ps, pe, d_ci, a->n_cols, nnz, ws->stream),
                   "spmm");

@@ -1,0 +1,63 @@
+// Packed column indices for the host entry's PCIe upload (host side; the
+// device side and the format are described in h2dpack.cu).  Encoding runs on
+// all host threads (OpenMP) while the copy engine moves the previous block.
+#include <omp.h>
+#include <stdint.h>
+
+#include <algorithm>
+#include <cstring>
+#include <vector>
+
+namespace gespmm {
+
+// Encodes positions [row_ptr[lo], row_ptr[hi]) of rows [lo, hi) into enc
+// (relative positions) and appends escaped (relative position, value) pairs to
+// exc in position order.  Returns the number of exceptions, or UINT64_MAX when
+// they exceed max_exc (the caller then sends the block raw).
+uint64_t pack_cols_block(const uint32_t* row_ptr, const uint32_t* col_ind, uint32_t lo,
+                         uint32_t hi, uint16_t* enc, uint32_t* exc /* pairs */, uint64_t max_exc) {
+  const uint64_t ps = row_ptr[lo];
+  const int nt = std::max(1, omp_get_max_threads());
+  // rows split by nnz across threads
+  std::vector<uint32_t> cut(size_t(nt) + 1, hi);
+  cut[0] = lo;
+  const uint64_t total = uint64_t(row_ptr[hi]) - ps;
+  for (int t = 1; t < nt; ++t) {
+    const uint64_t target = ps + total * uint64_t(t) / uint64_t(nt);
+    const uint32_t* it = std::lower_bound(row_ptr + lo, row_ptr + hi + 1, uint32_t(target));
+    cut[size_t(t)] = std::max(cut[size_t(t) - 1], uint32_t(std::min<ptrdiff_t>(it - row_ptr, hi)));
+  }
+  std::vector<std::vector<uint32_t>> local(static_cast<size_t>(nt));
+#pragma omp parallel num_threads(nt)
+  {
+    const int t = omp_get_thread_num();
+    std::vector<uint32_t>& ex = local[size_t(t)];
+    for (uint32_t r = cut[size_t(t)]; r < cut[size_t(t) + 1]; ++r) {
+      const uint64_t s = row_ptr[r], e = row_ptr[r + 1];
+      uint32_t prev = 0;
+      for (uint64_t p = s; p < e; ++p) {
+        const uint32_t c = col_ind[p];
+        const int64_t d = p == s ? int64_t(c) : int64_t(c) - int64_t(prev) - 1;
+        if (d >= 0 && d < 0xFFFF) {
+          enc[p - ps] = uint16_t(d);
+        } else {
+          enc[p - ps] = 0xFFFFu;
+          ex.push_back(uint32_t(p - ps));
+          ex.push_back(c);
+        }
+        prev = c;
+      }
+    }
+  }
+  uint64_t n = 0;
+  for (const auto& v : local) n += v.size() / 2;
+  if (n > max_exc) return UINT64_MAX;
+  uint64_t off = 0;
+  for (const auto& v : local) {
+    if (!v.empty()) std::memcpy(exc + off, v.data(), v.size() * sizeof(uint32_t));
+    off += v.size();
+  }
+  return n;
+}
+
+}  // namespace gespmm

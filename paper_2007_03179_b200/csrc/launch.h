@@ -92,6 +92,17 @@ void free_cluster_hot(ClusterHot* h);
 cudaError_t launch_cluster_warp(const ClusterHot& h, int op, bool fast, const SpmmArgs& a,
                                 cudaStream_t st, int* clusters);
 
+// --- packed column indices for the host entry's upload (h2dpack*.cpp/cu) ---
+uint64_t pack_cols_block(const uint32_t* row_ptr, const uint32_t* col_ind, uint32_t lo,
+                         uint32_t hi, uint16_t* enc, uint32_t* exc, uint64_t max_exc);
+size_t unpack_temp_bytes(uint64_t max_len);
+// rows [0, m_block) of row_ptr_block own positions [ps, pe); bits: zeroed
+// row-start bitmap over all nnz positions (shared with the column check).
+cudaError_t unpack_cols(const uint16_t* enc, const uint2* exc, uint32_t n_exc,
+                        const uint32_t* row_ptr_block, uint32_t m_block, uint64_t ps, uint64_t pe,
+                        uint64_t nnz, uint32_t* bits, uint32_t* col, void* temp, size_t temp_bytes,
+                        cudaStream_t st);
+
 // Device canonical check of a device CSR, formatted as the reference's
 // require_canonical(m, who) error (csr.hpp:155-158).  Synchronises `st`.
 gespmm_status_t validate_device_as(const gespmm_csr_t* a, cudaStream_t st, const char* who);

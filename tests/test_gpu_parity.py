@@ -513,3 +513,74 @@ def test_cluster_dsmem_hot_rows_keep_bits(cs, op, cuda):
             if want_arg:
                 assert np.array_equal(arg.cpu().numpy(), warg), (cs, op, arg_kind)
         plan.close()
+
+
+def _gappy(rows, k, per_row, seed, far_every=0):
+    """Sorted random rows over k columns; with far_every, every far_every-th
+    row also gets a column near k (a gap >= 65535: an escape code)."""
+    rng = np.random.default_rng(seed)
+    rp = np.zeros(rows + 1, np.uint32)
+    cols = []
+    for r in range(rows):
+        c = np.sort(rng.choice(k, per_row, replace=False)).astype(np.uint32)
+        if far_every and r % far_every == 0:
+            c = np.unique(np.concatenate([c, [k - 1 - (r % 7)]])).astype(np.uint32)
+        cols.append(c)
+        rp[r + 1] = rp[r] + len(c)
+    a = G.CsrMatrix(rows, k, rp, np.concatenate(cols), np.zeros(int(rp[-1]), np.float32))
+    G.randomize_values(a, seed + 1)
+    return a
+
+
+@pytest.mark.parametrize("kind", ["powerlaw", "uniform", "escapes", "raw_fallback"])
+@pytest.mark.parametrize("op", ["sum", "max"])
+def test_packed_upload_keeps_bits(kind, op, cuda):
+    """Host entry with the col_ind upload as 16-bit gap codes (h2d_pack=1):
+    rebuilt on the device by a segmented scan, bit-identical results; escape
+    codes for gaps >= 65535 (every 10th row of "escapes"), and blocks with too
+    many escapes sent raw ("raw_fallback": gaps ~75k everywhere)."""
+    if kind == "powerlaw":
+        a = G.gen_powerlaw(6000, 300000, 3000, 1.0, 71)
+        G.randomize_values(a, 72)
+    elif kind == "uniform":
+        a = G.gen_uniform_random(G.GraphGenSpec(8000, 120000, 73))
+        G.randomize_values(a, 74)
+    elif kind == "escapes":
+        a = _gappy(4000, 100_000, 50, 75, far_every=10)
+    else:
+        a = _gappy(300, 3_000_000, 40, 76)
+    b = G.make_random_dense(a.n_cols, 32, 79)
+    want, warg = _oracle(a, b, op, op == "max")
+    for pack in (1, -1):
+        c, arg = G.native_spmm_arg(a, b, G.KernelVariant.tuned(), G.reduce_op_by_name(op),
+                                   exec=G.ExecOptions(h2d_pack=pack), want_arg=op == "max")
+        assert first_divergence(c.data, want) is None, (kind, pack)
+        if op == "max":
+            assert np.array_equal(arg, warg), (kind, pack)
+
+
+def test_packed_upload_reports_the_same_violations(cuda):
+    """Non-canonical inputs travel losslessly (escapes), so the device check
+    reports the reference's first violation whether or not the upload is packed."""
+    a = G.gen_uniform_random(G.GraphGenSpec(3000, 60000, 81))
+    G.randomize_values(a, 82)
+    b = G.make_random_dense(3000, 16, 83)
+    rp = a.row_ptr.astype(np.int64)
+    cases = []
+    bad = a.col_ind.copy(); p = int(rp[1500]) + 3; bad[p] = bad[p - 1]          # duplicate
+    cases.append(bad)
+    bad = a.col_ind.copy(); p = int(rp[2000]) + 2; bad[p], bad[p + 1] = bad[p + 1], bad[p]  # swap
+    cases.append(bad)
+    bad = a.col_ind.copy(); bad[int(rp[2500]) + 1] = 3000 + 70000                # out of range
+    cases.append(bad)
+    for ci in cases:
+        m = G.CsrMatrix(a.n_rows, a.n_cols, a.row_ptr, ci, a.vals)
+        msgs = []
+        for pack in (1, -1):
+            with pytest.raises(G.Error) as ei:
+                G.native_spmm(m, b, G.KernelVariant.tuned(), G.ops.sum(),
+                              exec=G.ExecOptions(h2d_pack=pack))
+            msgs.append(str(ei.value))
+        assert msgs[0] == msgs[1] and "not canonical" in msgs[0]
+        want_n, want_msg = O.validate(m.n_rows, m.n_cols, m.row_ptr, m.col_ind, m.vals)
+        assert msgs[0] == "spmm: matrix is not canonical CSR: " + want_msg
