@@ -317,7 +317,7 @@ gespmm_status_t launch_tuned_rows(const TunedShapes& t, int op, bool fast, const
       if (tma && (hub_pdl || !side)) {
         // same stream; the warp kernel follows as a programmatic dependent
         // launch, so the hub CTAs are resident first and both run together
-        GESPMM_CUDA(launch_tuned_hub(op, fast, h, st), "spmm");
+        GESPMM_CUDA(launch_tuned_hub(op, fast, h, st, true), "spmm");
         hub_then_pdl = true;
       } else {
         cudaStream_t hs = side ? side : st;
@@ -326,7 +326,7 @@ gespmm_status_t launch_tuned_rows(const TunedShapes& t, int op, bool fast, const
           GESPMM_CUDA(cudaStreamWaitEvent(side, fork, 0), "spmm");
         }
         if (tma)
-          GESPMM_CUDA(launch_tuned_hub(op, fast, h, hs), "spmm");
+          GESPMM_CUDA(launch_tuned_hub(op, fast, h, hs, false), "spmm");
         else
           GESPMM_CUDA(launch_tuned_cta(cs, op, fast, h, hs), "spmm");
         if (side) {

@@ -388,25 +388,30 @@ __global__ void __launch_bounds__(WARPS * 32) k_cta(SpmmArgs a) {
 #ifndef GESPMM_HUB_PRODUCERS
 #define GESPMM_HUB_PRODUCERS 4
 #endif
-#ifndef GESPMM_HUB_RING_KB
-#define GESPMM_HUB_RING_KB 32
-#endif
 constexpr int kHubConsumers = GESPMM_HUB_CONSUMERS;  // consumer warps (lane owns VEC columns)
 constexpr int kHubProducers = GESPMM_HUB_PRODUCERS;  // producer (LDGSTS) warps
-#ifndef GESPMM_HUB_GROUP
-#define GESPMM_HUB_GROUP 16
-#endif
-constexpr int kHubGroup = GESPMM_HUB_GROUP;  // nonzeros per stage (one full/empty barrier pair)
-constexpr int kHubRingBytes = GESPMM_HUB_RING_KB * 1024;
+// Two ring geometries (BIG = the hub kernel carries the step, launched ahead of
+// the warp kernel; small = a side job next to it): 16 nonzeros per stage in a
+// 32 KB ring, or 32 per stage in 64 KB.  Fewer, larger stages halve the barrier
+// round trips per nonzero (8-way Reddit shard 0.69 -> 0.58 ms) but the larger
+// ring takes L1 capacity from a warp kernel running alongside (2-way shard 1.63
+// -> 1.82 ms, products 4-way 3.69 -> 4.01 ms; profiles/r1_shard_emulation.md).
+template <bool BIG>
+struct HubRing {
+  static constexpr int GROUP = BIG ? 32 : 16;       // nonzeros per stage (one full/empty pair)
+  static constexpr int BYTES = (BIG ? 64 : 32) * 1024;
+};
 
-template <int VEC>
+template <int VEC, bool BIG>
 struct HubGeom {
+  static constexpr int G = HubRing<BIG>::GROUP;
+  static constexpr int RING = HubRing<BIG>::BYTES;
   static constexpr int TW = 32 * kHubConsumers * VEC;          // columns per tile
   static constexpr int ROW_BYTES = TW * 4;                     // bytes per staged B slice
   static constexpr int CHUNKS = ROW_BYTES / 16;                // 16-byte copies per slice
-  static constexpr int STAGES = kHubRingBytes / (ROW_BYTES * kHubGroup);
+  static constexpr int STAGES = RING / (ROW_BYTES * G);
   static_assert(STAGES >= kHubProducers, "every producer warp needs a stage of its own");
-  static_assert((kHubGroup * CHUNKS) % 32 == 0, "a stage is whole warp-wide copy rounds");
+  static_assert((G * CHUNKS) % 32 == 0, "a stage is whole warp-wide copy rounds");
 };
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
@@ -449,15 +454,15 @@ __device__ __forceinline__ Vec<VEC> lds_vec(const float* p) {
   return r;
 }
 
-template <int OP, bool FAST, int VEC>
+template <int OP, bool FAST, int VEC, bool BIG>
 __global__ void __launch_bounds__(32 * (kHubConsumers + kHubProducers))
 k_hub(SpmmArgs a) {
   using R = Reduce<OP>;
-  using H = HubGeom<VEC>;
-  constexpr int S = H::STAGES, G = kHubGroup;
+  using H = HubGeom<VEC, BIG>;
+  constexpr int S = H::STAGES, G = H::G;
   extern __shared__ __align__(128) unsigned char hub_smem[];
   float* ring = reinterpret_cast<float*>(hub_smem);                       // [S][G][TW]
-  float* s_val = reinterpret_cast<float*>(hub_smem + kHubRingBytes);      // [S*G]
+  float* s_val = reinterpret_cast<float*>(hub_smem + H::RING);            // [S*G]
   uint32_t* s_col = reinterpret_cast<uint32_t*>(s_val + S * G);           // [S*G]
   uint64_t* bars = reinterpret_cast<uint64_t*>(s_col + S * G);            // full[S], empty[S]
 
@@ -609,10 +614,10 @@ k_hub(SpmmArgs a) {
   }
 }
 
-template <int VEC>
+template <int VEC, bool BIG>
 constexpr size_t hub_smem_bytes() {
-  using H = HubGeom<VEC>;
-  return size_t(kHubRingBytes) + size_t(H::STAGES) * kHubGroup * 8 + size_t(H::STAGES) * 16;
+  using H = HubGeom<VEC, BIG>;
+  return size_t(H::RING) + size_t(H::STAGES) * H::G * 8 + size_t(H::STAGES) * 16;
 }
 
 // ---- dispatch tables ------------------------------------------------------
@@ -738,7 +743,7 @@ cudaError_t hub_counter(uint32_t** out, int* sms, cudaStream_t st) {
 }
 
 template <int OP, bool FAST>
-cudaError_t hub_dispatch(int vec, const SpmmArgs& a0, cudaStream_t st) {
+cudaError_t hub_dispatch(int vec, bool big, const SpmmArgs& a0, cudaStream_t st) {
   const uint64_t units = uint64_t(a0.n_sched) * a0.n_tiles;
   if (units == 0) return cudaSuccess;
   if (units > 0x7fffffffull) return cudaErrorInvalidConfiguration;
@@ -757,23 +762,24 @@ cudaError_t hub_dispatch(int vec, const SpmmArgs& a0, cudaStream_t st) {
     if (ec != cudaSuccess) return ec;
     blocks = std::min<uint64_t>(units, uint64_t(per_sm) * uint64_t(sms > 0 ? sms : 148));
   }
-#define GESPMM_H(V)                                                                        \
-  if (vec == V) {                                                                          \
-    const size_t sm = hub_smem_bytes<V>();                                                 \
+#define GESPMM_H(V, BIG)                                                                   \
+  if (vec == V && big == BIG) {                                                            \
+    const size_t sm = hub_smem_bytes<V, BIG>();                                            \
     static bool attr_done[64] = {}; /* once per device: the call is not stream-ordered */   \
     int dev_ = 0;                                                                          \
     cudaGetDevice(&dev_);                                                                  \
     if (dev_ < 0 || dev_ >= 64 || !attr_done[dev_]) {                                      \
       const cudaError_t e0 = cudaFuncSetAttribute(                                         \
-          k_hub<OP, FAST, V>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));       \
+          k_hub<OP, FAST, V, BIG>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));  \
       if (e0 != cudaSuccess) return e0;                                                    \
       if (dev_ >= 0 && dev_ < 64) attr_done[dev_] = true;                                  \
     }                                                                                      \
-    k_hub<OP, FAST, V><<<dim3(uint32_t(blocks)), dim3(32 * (kHubConsumers + kHubProducers)), sm, st>>>(a); \
+    k_hub<OP, FAST, V, BIG><<<dim3(uint32_t(blocks)), dim3(32 * (kHubConsumers + kHubProducers)), sm, st>>>(a); \
     note_launch();                                                                         \
     return cudaGetLastError();                                                             \
   }
-  GESPMM_H(1) GESPMM_H(2) GESPMM_H(4)
+  GESPMM_H(1, false) GESPMM_H(2, false) GESPMM_H(4, false)
+  GESPMM_H(1, true) GESPMM_H(2, true) GESPMM_H(4, true)
 #undef GESPMM_H
   return cudaErrorInvalidValue;
 }
@@ -922,13 +928,13 @@ uint32_t hub_tile_width(uint32_t n, uint32_t n_hub) {
   return uint32_t(32 * kHubConsumers * hub_vec(n, n_hub));
 }
 
-cudaError_t launch_tuned_hub(int op, bool fast, const SpmmArgs& a, cudaStream_t st) {
+cudaError_t launch_tuned_hub(int op, bool fast, const SpmmArgs& a, cudaStream_t st, bool big) {
   const int v = hub_vec(a.n, a.n_sched);
   switch (op) {
-    case kSum: return fast ? hub_dispatch<kSum, true>(v, a, st) : hub_dispatch<kSum, false>(v, a, st);
-    case kMean: return fast ? hub_dispatch<kMean, true>(v, a, st) : hub_dispatch<kMean, false>(v, a, st);
-    case kMax: return hub_dispatch<kMax, false>(v, a, st);
-    default: return hub_dispatch<kMin, false>(v, a, st);
+    case kSum: return fast ? hub_dispatch<kSum, true>(v, big, a, st) : hub_dispatch<kSum, false>(v, big, a, st);
+    case kMean: return fast ? hub_dispatch<kMean, true>(v, big, a, st) : hub_dispatch<kMean, false>(v, big, a, st);
+    case kMax: return hub_dispatch<kMax, false>(v, big, a, st);
+    default: return hub_dispatch<kMin, false>(v, big, a, st);
   }
 }
 

@@ -60,7 +60,9 @@ cudaError_t launch_tuned_cta(const CtaShape& s, int op, bool fast, const SpmmArg
 // TMA-ring row-per-CTA kernel for hub rows (N % 4 == 0, 16-byte aligned B/C):
 // tile width hub_tile_width(n, n_hub) columns per CTA (a.n_sched = n_hub).
 uint32_t hub_tile_width(uint32_t n, uint32_t n_hub);
-cudaError_t launch_tuned_hub(int op, bool fast, const SpmmArgs& a, cudaStream_t st);
+// big: the 64 KB / 32-per-stage ring (hub kernel ahead of the warp kernel) or
+// the 32 KB / 16-per-stage one (side job next to it).
+cudaError_t launch_tuned_hub(int op, bool fast, const SpmmArgs& a, cudaStream_t st, bool big);
 
 // --- frequency-aware L2 policy (hotcols.cu) ---
 struct HotStats {
