@@ -152,6 +152,8 @@ typedef struct gespmm_plan_s* gespmm_plan_t;
 gespmm_status_t gespmm_plan_create(const gespmm_csr_t* a, uint32_t n, gespmm_reduce_t op,
                                    const gespmm_options_t* opts, void* stream,
                                    gespmm_plan_t* out);
+/* Executions of one plan must not overlap on different streams (the plan owns
+ * its side stream, events and work counters); use one plan per stream. */
 gespmm_status_t gespmm_plan_execute(gespmm_plan_t plan, const float* b, float* c, int32_t* arg,
                                     void* stream);
 /* Human-readable description of the chosen shape (static storage per plan). */
