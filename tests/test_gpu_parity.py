@@ -584,3 +584,35 @@ def test_packed_upload_reports_the_same_violations(cuda):
         assert msgs[0] == msgs[1] and "not canonical" in msgs[0]
         want_n, want_msg = O.validate(m.n_rows, m.n_cols, m.row_ptr, m.col_ind, m.vals)
         assert msgs[0] == "spmm: matrix is not canonical CSR: " + want_msg
+
+
+@pytest.mark.parametrize("ht", [0, 300, -1])
+def test_plan_execute_is_graph_capturable(ht, cuda):
+    """A plan's execute captured into a CUDA graph and replayed (the GNN-layer
+    pattern): hub kernel ahead of the warp kernel as a programmatic dependent
+    launch (ht=300), side stream, or warp kernel alone; replays bit-exact, with
+    a changed B between replays."""
+    import torch
+    a, b = _powerlaw(5000, 300000, 4000, 91, 128)
+    d = G.DeviceCsr.from_host(a, cuda)
+    bt = torch.from_numpy(b.data).to(cuda)
+    c = torch.empty((a.n_rows, 128), device=cuda)
+    plan = G.Plan(d, 128, "sum", exec=G.ExecOptions(hub_threshold=ht))
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        plan.execute(bt, c, stream=s)  # warm-up: policies resolved, attributes set
+    torch.cuda.current_stream().wait_stream(s)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        plan.execute(bt, c)
+    for seed in (92, 93):
+        b2 = G.make_random_dense(a.n_cols, 128, seed)
+        bt.copy_(torch.from_numpy(b2.data))
+        c.fill_(-1.0)
+        g.replay()
+        torch.cuda.synchronize()
+        want, _ = _oracle(a, b2, "sum")
+        assert first_divergence(c.cpu().numpy(), want) is None, (ht, seed)
+    plan.close()
