@@ -146,7 +146,7 @@ class ClockSampler:
     def stop(self):
         if self.thread is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [self.error or "not sampled"]}
-        time.sleep(0.02)
+        time.sleep(0.25)  # NVML readings lag: keep sampling briefly after the region
         self._stop.set()
         self.thread.join(timeout=2)
         t0 = self.t0 if self.t0 is not None else -1e30
@@ -160,6 +160,8 @@ class ClockSampler:
                     f.write(f"{x[0] - t0:.4f},{x[1]},{x[2]},{x[3]:.1f},{x[4]:#x},"
                             f"{int(t0 <= x[0] <= t1)}\n")
         reasons = sorted({name for x in inside for name, bit in self.REASONS if x[4] & bit})
+        after = [x for x in self.samples if t1 < x[0] <= t1 + 0.25]
+        reasons_after = sorted({name for x in after for name, bit in self.REASONS if x[4] & bit})
         sm = [x[1] for x in inside]
         return {"sm_mhz": statistics.median(sm) if sm else None,
                 "sm_min_mhz": min(sm) if sm else None,
@@ -167,7 +169,9 @@ class ClockSampler:
                 "mem_mhz": statistics.median([x[2] for x in inside]) if inside else None,
                 "power_w_max": max(x[3] for x in inside) if inside else None,
                 "samples": len(inside), "source": "nvml, timed region only",
-                "reasons": reasons}
+                "reasons": reasons,
+                "reasons_next_250ms": reasons_after,
+                "sm_mhz_next_250ms": statistics.median([x[1] for x in after]) if after else None}
 
 
 def hbm_peak():
