@@ -551,12 +551,13 @@ def test_packed_upload_keeps_bits(kind, op, cuda):
         a = _gappy(300, 3_000_000, 40, 76)
     b = G.make_random_dense(a.n_cols, 32, 79)
     want, warg = _oracle(a, b, op, op == "max")
-    for pack in (1, -1):
-        c, arg = G.native_spmm_arg(a, b, G.KernelVariant.tuned(), G.reduce_op_by_name(op),
-                                   exec=G.ExecOptions(h2d_pack=pack), want_arg=op == "max")
-        assert first_divergence(c.data, want) is None, (kind, pack)
-        if op == "max":
-            assert np.array_equal(arg, warg), (kind, pack)
+    for v in (G.KernelVariant.tuned(), G.KernelVariant.crc_cwm(2)):
+        for pack in (1, -1):
+            c, arg = G.native_spmm_arg(a, b, v, G.reduce_op_by_name(op),
+                                       exec=G.ExecOptions(h2d_pack=pack), want_arg=op == "max")
+            assert first_divergence(c.data, want) is None, (kind, pack, v)
+            if op == "max":
+                assert np.array_equal(arg, warg), (kind, pack, v)
 
 
 def test_packed_upload_reports_the_same_violations(cuda):
