@@ -82,13 +82,17 @@ def test_new_ops_and_args_every_variant(op, cuda):
         want_arg = op in ("max", "min")
         for kind in ((O.ARG_EDGE, O.ARG_COLUMN) if want_arg else (O.ARG_EDGE,)):
             want, warg = _oracle(a, b, op, want_arg, kind)
-            ex = G.ExecOptions(arg_kind="column" if kind == O.ARG_COLUMN else "edge")
-            for v in ALL_VARIANTS:
-                c, arg = G.native_spmm_arg(a, b, v, G.reduce_op_by_name(op), exec=ex,
+            ak = "column" if kind == O.ARG_COLUMN else "edge"
+            ex = G.ExecOptions(arg_kind=ak)
+            runs = [(v, ex) for v in ALL_VARIANTS]
+            # every row through the hub kernels too (ring-fed k_hub / LDG k_cta)
+            runs.append((G.KernelVariant.tuned(), G.ExecOptions(arg_kind=ak, hub_threshold=1)))
+            for v, e in runs:
+                c, arg = G.native_spmm_arg(a, b, v, G.reduce_op_by_name(op), exec=e,
                                            want_arg=want_arg)
-                assert first_divergence(c.data, want) is None, (op, v, rows, n)
+                assert first_divergence(c.data, want) is None, (op, v, rows, n, e.hub_threshold)
                 if want_arg:
-                    assert np.array_equal(arg, warg), (op, v, kind)
+                    assert np.array_equal(arg, warg), (op, v, kind, e.hub_threshold)
 
 
 N_SWEEP = [1, 2, 3, 4, 5, 8, 12, 16, 24, 31, 32, 33, 48, 64, 66, 96, 100, 127, 128, 129, 192,
