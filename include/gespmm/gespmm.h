@@ -79,7 +79,7 @@ typedef struct {
   int32_t variant;    /* gespmm_variant_t, default TUNED */
   uint32_t cf;        /* CRC_CWM coarsening factor: 2, 4 or 8 (check_config, kernel.hpp:83-92) */
   int32_t exact;      /* 1 (default): ordered fold, separate mul/add -> bit-exact for all ops.
-                         0: sum/mean may use FFMA and split hub rows (1e-5 rel. tolerance). */
+                         0: sum/mean use FFMA (1e-5 relative tolerance). */
   int32_t arg_kind;   /* gespmm_arg_kind_t, default EDGE (CSR position) */
   int32_t validate;   /* 1 (default for *_host): canonical-CSR check before the launch */
   int32_t fault_skip_tail; /* negative-test hook: FaultMode::SkipTail (kernel.hpp:167-182) */
