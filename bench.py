@@ -514,7 +514,7 @@ def run_ours(args, cfg):
                "step_ms": {"min": round(min(e2e_each), 3),
                            "median": round(statistics.median(e2e_each), 3),
                            "max": round(max(e2e_each), 3)},
-               "path": "gespmm_spmm_host: row_ptr+B H2D, then 16 nnz-balanced row blocks pipelined "
+               "path": "gespmm_spmm_host: row_ptr+B H2D, then 12 nnz-balanced row blocks pipelined "
                        "(host packs col_ind to 16-bit gap codes | codes+vals H2D | device unpack+"
                        "validate+kernel | C D2H); h2d_bytes = bytes that crossed PCIe, "
                        "input_bytes = the caller's CSR + B"}

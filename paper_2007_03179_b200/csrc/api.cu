@@ -942,10 +942,13 @@ gespmm_status_t gespmm_spmm_host(const gespmm_csr_t* a, const float* b, uint32_t
 
   // ---- row blocks balanced by nnz (binary search on the host row_ptr)
   // pipeline depth: more blocks shrink the un-overlapped tail (last block's
-  // kernel + C copy-out); 16 measured best at Reddit size (20.0 vs 20.6 ms at 8)
+  // kernel + C copy-out) but each block's compute carries its hub rows' critical
+  // path; with the packed upload (~0.9 ms of copy per block at 16 blocks) the
+  // per-block compute (~0.8 ms) nears the copy once clocks drop under the power
+  // cap, so 12 blocks keep a margin (Reddit: 16.2-16.5 ms vs 16.4-17.1 at 16).
   // (the paper's Alg. 1-3 kernels keep 8: their hub rows bound every block)
   const bool tuned_v = o.variant == GESPMM_VARIANT_TUNED;
-  int chunks = (tuned_v && nnz >= (uint64_t(32) << 20)) ? 16 : (nnz >= (uint64_t(8) << 20) ? 8 : 1);
+  int chunks = (tuned_v && nnz >= (uint64_t(32) << 20)) ? 12 : (nnz >= (uint64_t(8) << 20) ? 8 : 1);
   if (const char* e = std::getenv("GESPMM_CHUNKS")) {  // pipeline depth experiments
     const int v = std::atoi(e);
     if (v >= 1 && v <= kMaxChunks && nnz >= uint64_t(v)) chunks = v;
