@@ -11,9 +11,6 @@
 // starts — the validation's row-start bitmap — and at escapes) turns the codes
 // back into columns.
 #include <cub/cub.cuh>
-#include <thrust/iterator/counting_iterator.h>
-#include <thrust/iterator/transform_iterator.h>
-#include <thrust/iterator/transform_output_iterator.h>
 
 #include "common.cuh"
 #include "launch.h"
@@ -46,10 +43,6 @@ struct Decode {
   }
 };
 
-struct TakeV {
-  __host__ __device__ uint32_t operator()(const SegVal& s) const { return s.v; }
-};
-
 __global__ void k_scatter_exceptions(const uint2* __restrict__ exc, uint32_t n, uint64_t ps,
                                      uint32_t* __restrict__ col) {
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
@@ -65,17 +58,122 @@ __global__ void k_mark_starts_p(const uint32_t* __restrict__ rp, uint32_t m, uin
   }
 }
 
-using DecodeIt = thrust::transform_iterator<Decode, thrust::counting_iterator<uint64_t>>;
-using OutIt = thrust::transform_output_iterator<TakeV, uint32_t*>;
+// Three passes over 2048-element chunks (one 256-thread CTA per chunk, 8
+// consecutive elements per thread): per-chunk aggregates, one CTA scanning
+// the aggregates into carries, then the chunk-local scan with its carry.  (A
+// single cub::DeviceScan over a transform iterator of this 8-byte pair ran
+// at ~80 G elements/s, 91 us per Reddit block; this reads the codes twice
+// and writes the columns once.)
+constexpr int kUnpackThreads = 256;
+constexpr int kUnpackItems = 8;
+constexpr uint32_t kUnpackChunk = kUnpackThreads * kUnpackItems;
+
+using BlockScanT = cub::BlockScan<SegVal, kUnpackThreads>;
+using BlockLoadT = cub::BlockLoad<uint16_t, kUnpackThreads, kUnpackItems, cub::BLOCK_LOAD_WARP_TRANSPOSE>;
+using BlockStoreT = cub::BlockStore<uint32_t, kUnpackThreads, kUnpackItems, cub::BLOCK_STORE_WARP_TRANSPOSE>;
+union UnpackSmem {
+  typename BlockScanT::TempStorage scan;
+  typename BlockLoadT::TempStorage load;
+  typename BlockStoreT::TempStorage store;
+};
+
+// The chunk's codes, coalesced through shared memory into 8 consecutive
+// elements per thread, decoded (row-start bit, escapes from col).
+__device__ __forceinline__ void load_decode(const Decode& d, uint64_t len, UnpackSmem& sm,
+                                            SegVal (&x)[kUnpackItems]) {
+  const uint64_t c0 = uint64_t(blockIdx.x) * kUnpackChunk;
+  const uint64_t rem = len - c0;
+  const int valid = int(rem < kUnpackChunk ? rem : kUnpackChunk);
+  uint16_t e[kUnpackItems];
+  BlockLoadT(sm.load).Load(d.enc + c0, e, valid, uint16_t(0));
+  __syncthreads();
+  const uint64_t i0 = c0 + uint64_t(threadIdx.x) * kUnpackItems;
+#pragma unroll
+  for (int j = 0; j < kUnpackItems; ++j) {
+    const uint64_t i = i0 + j;
+    if (i >= len) {
+      x[j] = SegVal{0u, 0u};
+      continue;
+    }
+    const uint64_t p = d.ps + i;
+    const bool first = (d.bits[p >> 5] >> (p & 31u)) & 1u;
+    x[j] = e[j] == 0xFFFFu ? SegVal{d.col[p], 1u}
+                           : (first ? SegVal{e[j], 1u} : SegVal{uint32_t(e[j]) + 1u, 0u});
+  }
+}
+
+__global__ void __launch_bounds__(kUnpackThreads) k_unpack_agg(Decode d, uint64_t len,
+                                                               SegVal* __restrict__ aggs) {
+  __shared__ UnpackSmem sm;
+  SegVal x[kUnpackItems];
+  load_decode(d, len, sm, x);
+  SegVal t{0u, 0u};
+#pragma unroll
+  for (int j = 0; j < kUnpackItems; ++j) t = SegAdd{}(t, x[j]);
+  SegVal incl, total;
+  BlockScanT(sm.scan).InclusiveScan(t, incl, SegAdd{}, total);
+  if (threadIdx.x == 0) aggs[blockIdx.x] = total;
+}
+
+struct RunningPrefix {
+  SegVal run;
+  __device__ SegVal operator()(SegVal block_total) {
+    const SegVal old = run;
+    run = SegAdd{}(run, block_total);
+    return old;
+  }
+};
+
+// one CTA: exclusive segmented scan of the chunk aggregates (identity {0, 0}),
+// 2048 aggregates per round (8 consecutive per thread)
+__global__ void __launch_bounds__(kUnpackThreads) k_unpack_carry(const SegVal* __restrict__ aggs,
+                                                                 uint32_t n, SegVal* __restrict__ carry) {
+  __shared__ typename BlockScanT::TempStorage tmp;
+  RunningPrefix pre{SegVal{0u, 0u}};
+  for (uint32_t base = 0; base < n; base += kUnpackChunk) {
+    const uint32_t c0 = base + threadIdx.x * kUnpackItems;
+    SegVal x[kUnpackItems], ex[kUnpackItems];
+#pragma unroll
+    for (int j = 0; j < kUnpackItems; ++j)
+      x[j] = c0 + j < n ? aggs[c0 + j] : SegVal{0u, 0u};
+    BlockScanT(tmp).ExclusiveScan(x, ex, SegAdd{}, pre);
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < kUnpackItems; ++j)
+      if (c0 + j < n) carry[c0 + j] = ex[j];
+  }
+}
+
+__global__ void __launch_bounds__(kUnpackThreads) k_unpack_apply(Decode d, uint64_t len,
+                                                                 const SegVal* __restrict__ carry,
+                                                                 uint32_t* __restrict__ col) {
+  __shared__ UnpackSmem sm;
+  SegVal x[kUnpackItems];
+  load_decode(d, len, sm, x);
+  SegVal t{0u, 0u};
+#pragma unroll
+  for (int j = 0; j < kUnpackItems; ++j) t = SegAdd{}(t, x[j]);
+  RunningPrefix pre{carry[blockIdx.x]};
+  SegVal ex;
+  BlockScanT(sm.scan).ExclusiveScan(t, ex, SegAdd{}, pre);
+  uint32_t out[kUnpackItems];
+  SegVal run = ex;
+#pragma unroll
+  for (int j = 0; j < kUnpackItems; ++j) {
+    run = SegAdd{}(run, x[j]);
+    out[j] = run.v;
+  }
+  __syncthreads();  // scan storage is reused by the store
+  const uint64_t c0 = uint64_t(blockIdx.x) * kUnpackChunk;
+  const uint64_t rem = len - c0;
+  BlockStoreT(sm.store).Store(col + d.ps + c0, out, int(rem < kUnpackChunk ? rem : kUnpackChunk));
+}
 
 }  // namespace
 
 size_t unpack_temp_bytes(uint64_t max_len) {
-  size_t bytes = 0;
-  DecodeIt in(thrust::counting_iterator<uint64_t>(0), Decode{nullptr, nullptr, nullptr, 0});
-  OutIt out(static_cast<uint32_t*>(nullptr), TakeV{});
-  cub::DeviceScan::InclusiveScan(nullptr, bytes, in, out, SegAdd{}, int(max_len));
-  return bytes;
+  const uint64_t chunks = (max_len + kUnpackChunk - 1) / kUnpackChunk;
+  return size_t(2 * chunks + 2) * sizeof(SegVal);
 }
 
 cudaError_t unpack_cols(const uint16_t* enc, const uint2* exc, uint32_t n_exc,
@@ -83,7 +181,10 @@ cudaError_t unpack_cols(const uint16_t* enc, const uint2* exc, uint32_t n_exc,
                         uint64_t nnz, uint32_t* bits, uint32_t* col, void* temp, size_t temp_bytes,
                         cudaStream_t st) {
   if (pe <= ps) return cudaSuccess;
-  if (pe - ps > 0x7fffffffull) return cudaErrorInvalidValue;
+  const uint64_t len = pe - ps;
+  const uint64_t chunks = (len + kUnpackChunk - 1) / kUnpackChunk;
+  if (chunks > 0x7fffffffull || temp_bytes < size_t(2 * chunks) * sizeof(SegVal))
+    return cudaErrorInvalidValue;
   const uint64_t mb = (uint64_t(m_block) + 255) / 256;
   if (m_block) {
     k_mark_starts_p<<<uint32_t(mb < 148 * 8 ? mb : 148 * 8), 256, 0, st>>>(row_ptr_block, m_block,
@@ -95,12 +196,15 @@ cudaError_t unpack_cols(const uint16_t* enc, const uint2* exc, uint32_t n_exc,
     k_scatter_exceptions<<<eb < 148 * 8 ? eb : 148 * 8, 256, 0, st>>>(exc, n_exc, ps, col);
     note_launch();
   }
-  DecodeIt in(thrust::counting_iterator<uint64_t>(0), Decode{enc, col, bits, ps});
-  OutIt out(col + ps, TakeV{});
-  size_t bytes = temp_bytes;
-  cudaError_t e = cub::DeviceScan::InclusiveScan(temp, bytes, in, out, SegAdd{}, int(pe - ps), st);
+  SegVal* aggs = static_cast<SegVal*>(temp);
+  SegVal* carry = aggs + chunks;
+  const Decode d{enc, col, bits, ps};
+  k_unpack_agg<<<uint32_t(chunks), kUnpackThreads, 0, st>>>(d, len, aggs);
+  k_unpack_carry<<<1, kUnpackThreads, 0, st>>>(aggs, uint32_t(chunks), carry);
+  k_unpack_apply<<<uint32_t(chunks), kUnpackThreads, 0, st>>>(d, len, carry, col);
   note_launch();
-  if (e != cudaSuccess) return e;
+  note_launch();
+  note_launch();
   return cudaGetLastError();
 }
 
