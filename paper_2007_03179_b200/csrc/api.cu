@@ -189,7 +189,9 @@ namespace {
 // tools/shard_emulation.py (profiles/r1_shard_emulation.md): factor 1.5 keeps
 // the 1-GPU step unchanged and halves the 8-shard step (1.51 -> 0.79 ms).
 uint32_t auto_hub_threshold(uint32_t n, uint64_t nnz, int cf, uint32_t k, int dev) {
-  if (n < 64) return 0xffffffffu;  // narrow rows: one warp already covers the row cheaply
+  // narrow rows stay on warps: at N = 44 (the GCN's class width) hub rows
+  // through k_hub measured 2.75 ms against 2.32 ms without (tools/gcn_width_probe.py)
+  if (n < 64) return 0xffffffffu;
   // gather rate: ~19 TB/s while B (mostly) fits the L2, ~9.5 TB/s once the
   // gathers miss to HBM (ogbn-products N=256: B = 2.5 GB)
   int l2 = 0;
