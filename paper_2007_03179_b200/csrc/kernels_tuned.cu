@@ -60,9 +60,12 @@ constexpr int warp_min_blocks() {
 }
 
 template <int LPR, int CF>
+#ifndef GESPMM_U_NARROW
+#define GESPMM_U_NARROW 8
+#endif
 struct WarpGeom {
   static constexpr int RPW = 32 / LPR;                     // rows per warp
-  static constexpr int U0 = 8 / CF;
+  static constexpr int U0 = (LPR == 16 ? GESPMM_U_NARROW : 8) / CF;
   static constexpr int U = U0 < LPR ? U0 : LPR;            // gather batch; LPR % U == 0
   static constexpr int W = U < 4 ? U : 4;                  // LDS width (entries per read)
   static_assert(LPR % U == 0 && U % W == 0, "batch geometry");
