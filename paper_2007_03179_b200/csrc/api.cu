@@ -188,17 +188,18 @@ namespace {
 // one block of the pipelined host entry.  Measured with
 // tools/shard_emulation.py (profiles/r1_shard_emulation.md): factor 1.5 keeps
 // the 1-GPU step unchanged and halves the 8-shard step (1.51 -> 0.79 ms).
-uint32_t auto_hub_threshold(uint32_t n, uint64_t nnz, int cf, uint32_t k, int dev) {
-  // narrow rows stay on warps: at N = 44 (the GCN's class width) hub rows
-  // through k_hub measured 2.75 ms against 2.32 ms without (tools/gcn_width_probe.py)
-  if (n < 64) return 0xffffffffu;
+uint32_t auto_hub_threshold(uint32_t n, uint64_t nnz, int cf, uint32_t k, int dev,
+                            uint32_t tile_cols) {
+  if (n < 8) return 0xffffffffu;  // too narrow for a CTA per row
+  // the warp kernel moves whole lane tiles (N = 44 -> 64 columns of float4 lanes)
+  const uint32_t moved = std::max(n, tile_cols);
   // gather rate: ~19 TB/s while B (mostly) fits the L2, ~9.5 TB/s once the
   // gathers miss to HBM (ogbn-products N=256: B = 2.5 GB)
   int l2 = 0;
   cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev);
   const double b_bytes = double(k) * double(n) * 4.0;
   const double rate = (l2 > 0 && b_bytes > 1.5 * double(l2)) ? 9.5e12 : 19e12;
-  const double t_launch = double(nnz) * 4.0 * double(n) / rate;
+  const double t_launch = double(nnz) * 4.0 * double(moved) / rate;
   const double t_nnz = 0.7e-6 * double(cf < 1 ? 1 : cf) / 8.0;
   double f = 1.5;  // GESPMM_HUB_FACTOR: tuning experiments (tools/shard_emulation.py)
   if (const char* e = std::getenv("GESPMM_HUB_FACTOR")) f = std::max(0.05, std::atof(e));
@@ -376,7 +377,8 @@ gespmm_status_t build_tuned(Plan& p, const uint32_t* host_rp, cudaStream_t st) {
   p.hub_threshold = ht > 0 ? uint32_t(ht)
                            : (ht < 0 ? 0xffffffffu
                                      : auto_hub_threshold(sw, host_rp[m], p.sh.warp_v.cf,
-                                                          p.a.n_cols, p.device));
+                                                          p.a.n_cols, p.device,
+                                                          p.sh.warp_v.tile_width()));
   uint32_t n_hub = 0;
   uint64_t hub_nnz = 0;
   while (n_hub < m && deg[order[n_hub]] >= p.hub_threshold) hub_nnz += deg[order[n_hub++]];
@@ -980,7 +982,8 @@ gespmm_status_t gespmm_spmm_host(const gespmm_csr_t* a, const float* b, uint32_t
         ht > 0 ? uint32_t(ht)
                : (ht < 0 ? 0xffffffffu
                          : auto_hub_threshold(shapes.slice_w, nnz / uint64_t(chunks),
-                                              shapes.warp_v.cf, a->n_cols, dev));
+                                              shapes.warp_v.cf, a->n_cols, dev,
+                                              shapes.warp_v.tile_width()));
     GESPMM_CUDA(ws->reserve_host(2, sizeof(uint32_t) * m), "spmm");
     uint32_t* order = static_cast<uint32_t*>(ws->hbuf[2]);  // pinned: no sync after its copy
     uint32_t maxd = 0;

@@ -6,7 +6,10 @@ dev = torch.device("cuda", 0)
 a = gcn.normalize_adjacency(bench.make_inputs(bench.CONFIGS["reddit"]))
 d = G.DeviceCsr.from_host(a, dev)
 flush = torch.empty(128 * 1024 * 1024, device=dev)
-for n, ht, rpw in ((44, -1, 0), (44, -1, 2), (44, -1, 4), (48, -1, 0), (44, 0, 0), (256, 0, 0)):
+cases = [(44, -1, 0), (44, 8000, 0), (44, 12000, 0), (44, 16000, 0), (44, 19000, 0), (256, 0, 0)]
+if os.environ.get("PROBE_CASES"):
+    cases = [tuple(int(v) for v in c.split(":")) for c in os.environ["PROBE_CASES"].split(",")]
+for n, ht, rpw in cases:
     b = torch.randn(a.n_cols, n, device=dev)
     c = torch.empty(a.n_rows, n, device=dev)
     if True:
