@@ -385,13 +385,9 @@ __global__ void __launch_bounds__(WARPS * 32) k_cta(SpmmArgs a) {
 //   producer warp: 0.87 ms for a 21,657-nonzero row — the per-SM bulk-copy
 //   engine keeps too few 512-B copies in flight; tools/longrow_probe.py.)
 //   Needs N % 4 == 0 and 16-byte aligned B/C (16-byte copy units).
-#ifndef GESPMM_HUB_CONSUMERS
-#define GESPMM_HUB_CONSUMERS 1
-#endif
 #ifndef GESPMM_HUB_PRODUCERS
 #define GESPMM_HUB_PRODUCERS 4
 #endif
-constexpr int kHubConsumers = GESPMM_HUB_CONSUMERS;  // consumer warps (lane owns VEC columns)
 constexpr int kHubProducers = GESPMM_HUB_PRODUCERS;  // producer (LDGSTS) warps
 // Two ring geometries (BIG = the hub kernel carries the step, launched ahead of
 // the warp kernel; small = a side job next to it): 16 nonzeros per stage in a
@@ -405,11 +401,11 @@ struct HubRing {
   static constexpr int BYTES = (BIG ? 64 : 32) * 1024;
 };
 
-template <int VEC, bool BIG>
+template <int VEC, bool BIG, int C>
 struct HubGeom {
   static constexpr int G = HubRing<BIG>::GROUP;
   static constexpr int RING = HubRing<BIG>::BYTES;
-  static constexpr int TW = 32 * kHubConsumers * VEC;          // columns per tile
+  static constexpr int TW = 32 * C * VEC;                      // columns per tile
   static constexpr int ROW_BYTES = TW * 4;                     // bytes per staged B slice
   static constexpr int CHUNKS = ROW_BYTES / 16;                // 16-byte copies per slice
   static constexpr int STAGES = RING / (ROW_BYTES * G);
@@ -457,11 +453,11 @@ __device__ __forceinline__ Vec<VEC> lds_vec(const float* p) {
   return r;
 }
 
-template <int OP, bool FAST, int VEC, bool BIG>
-__global__ void __launch_bounds__(32 * (kHubConsumers + kHubProducers))
+template <int OP, bool FAST, int VEC, bool BIG, int C>
+__global__ void __launch_bounds__(32 * (C + kHubProducers))
 k_hub(SpmmArgs a) {
   using R = Reduce<OP>;
-  using H = HubGeom<VEC, BIG>;
+  using H = HubGeom<VEC, BIG, C>;
   constexpr int S = H::STAGES, G = H::G;
   extern __shared__ __align__(128) unsigned char hub_smem[];
   float* ring = reinterpret_cast<float*>(hub_smem);                       // [S][G][TW]
@@ -481,7 +477,7 @@ k_hub(SpmmArgs a) {
       // arrival per consumer warp
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 32;" ::"r"(full0 + 8 * i));
       asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(empty0 + 8 * i),
-                   "r"(kHubConsumers));
+                   "r"(C));
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -513,10 +509,10 @@ k_hub(SpmmArgs a) {
     const uint32_t chunks = tw / 4u;                            // 16-byte copies per slice
     const uint32_t groups = (len + G - 1) / G;
 
-    if (warp >= kHubConsumers) {
+    if (warp >= uint32_t(C)) {
       // ---- producer warp pw fills groups q = pw, pw + P, ...; the group's
       // (col, val) are loaded one group ahead of the copies they address.
-      const uint32_t pw = warp - kHubConsumers;
+      const uint32_t pw = warp - uint32_t(C);
       const uint32_t* ci = a.col_ind + start;
       const float* vs = a.vals + start;
       const char* bsrc = reinterpret_cast<const char*>(a.b + col0);
@@ -556,7 +552,7 @@ k_hub(SpmmArgs a) {
       }
     } else {
       // ---- consumer warps: thread t owns columns col0 + t*VEC .. +VEC
-      const uint32_t t = threadIdx.x;                    // 0 .. 32*kHubConsumers-1
+      const uint32_t t = threadIdx.x;                    // 0 .. 32*C-1
       const bool colok = t * uint32_t(VEC) < tw;
       float acc[VEC];
       int32_t who[VEC];
@@ -617,9 +613,9 @@ k_hub(SpmmArgs a) {
   }
 }
 
-template <int VEC, bool BIG>
+template <int VEC, bool BIG, int C>
 constexpr size_t hub_smem_bytes() {
-  using H = HubGeom<VEC, BIG>;
+  using H = HubGeom<VEC, BIG, C>;
   return size_t(H::RING) + size_t(H::STAGES) * H::G * 8 + size_t(H::STAGES) * 16;
 }
 
@@ -746,7 +742,7 @@ cudaError_t hub_counter(uint32_t** out, int* sms, cudaStream_t st) {
 }
 
 template <int OP, bool FAST>
-cudaError_t hub_dispatch(int vec, bool big, const SpmmArgs& a0, cudaStream_t st) {
+cudaError_t hub_dispatch(int vec, int cons, bool big, const SpmmArgs& a0, cudaStream_t st) {
   const uint64_t units = uint64_t(a0.n_sched) * a0.n_tiles;
   if (units == 0) return cudaSuccess;
   if (units > 0x7fffffffull) return cudaErrorInvalidConfiguration;
@@ -765,24 +761,29 @@ cudaError_t hub_dispatch(int vec, bool big, const SpmmArgs& a0, cudaStream_t st)
     if (ec != cudaSuccess) return ec;
     blocks = std::min<uint64_t>(units, uint64_t(per_sm) * uint64_t(sms > 0 ? sms : 148));
   }
-#define GESPMM_H(V, BIG)                                                                   \
-  if (vec == V && big == BIG) {                                                            \
-    const size_t sm = hub_smem_bytes<V, BIG>();                                            \
+#define GESPMM_H(V, BIG, C)                                                                \
+  if (vec == V && big == BIG && cons == C) {                                               \
+    const size_t sm = hub_smem_bytes<V, BIG, C>();                                         \
     static bool attr_done[64] = {}; /* once per device: the call is not stream-ordered */   \
     int dev_ = 0;                                                                          \
     cudaGetDevice(&dev_);                                                                  \
     if (dev_ < 0 || dev_ >= 64 || !attr_done[dev_]) {                                      \
       const cudaError_t e0 = cudaFuncSetAttribute(                                         \
-          k_hub<OP, FAST, V, BIG>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));  \
+          k_hub<OP, FAST, V, BIG, C>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)); \
       if (e0 != cudaSuccess) return e0;                                                    \
       if (dev_ >= 0 && dev_ < 64) attr_done[dev_] = true;                                  \
     }                                                                                      \
-    k_hub<OP, FAST, V, BIG><<<dim3(uint32_t(blocks)), dim3(32 * (kHubConsumers + kHubProducers)), sm, st>>>(a); \
+    k_hub<OP, FAST, V, BIG, C><<<dim3(uint32_t(blocks)), dim3(32 * (C + kHubProducers)), sm, st>>>(a); \
     note_launch();                                                                         \
     return cudaGetLastError();                                                             \
   }
-  GESPMM_H(1, false) GESPMM_H(2, false) GESPMM_H(4, false)
-  GESPMM_H(1, true) GESPMM_H(2, true) GESPMM_H(4, true)
+  // tile of 32 * C * V columns: one consumer warp with V-wide lanes, or C
+  // consumer warps sharing the tile's columns (fewer instructions per warp
+  // per nonzero, folds on C schedulers at once)
+  GESPMM_H(1, false, 1) GESPMM_H(2, false, 1) GESPMM_H(4, false, 1)
+  GESPMM_H(1, true, 1) GESPMM_H(2, true, 1) GESPMM_H(4, true, 1)
+  GESPMM_H(1, false, 2) GESPMM_H(2, false, 2) GESPMM_H(1, false, 4)
+  GESPMM_H(1, true, 2) GESPMM_H(2, true, 2) GESPMM_H(1, true, 4)
 #undef GESPMM_H
   return cudaErrorInvalidValue;
 }
@@ -921,23 +922,39 @@ int hub_vec(uint32_t n, uint32_t n_hub) {
     if (v == 1 || v == 2 || v == 4) return v;
   }
   for (int v : {4, 2}) {
-    const uint64_t tw = 32u * uint64_t(kHubConsumers) * uint64_t(v);
+    const uint64_t tw = 32u * uint64_t(v);
     const uint64_t tiles = (uint64_t(n) + tw - 1) / tw;
     if (uint64_t(n_hub) * tiles >= 2ull * 148ull) return v;
   }
   return 1;
 }
+// Consumer warps sharing a tile of 32 * width columns (the lane width shrinks
+// accordingly): 2 when the hub kernel leads the step (the consumer's fold rate
+// bounds it: 8-way Reddit shard 0.578 -> 0.541 ms, 4000 rows x 2000 nonzeros
+// 9.1 -> 10.8 TB/s), 1 as a side job (4-way shard 1.006 vs 1.088 ms with 2).
+// GESPMM_HUB_SPLIT = 1, 2 or 4 forces it (tuning experiments).
+int hub_split(int width, bool big) {
+  static const int forced = [] {
+    const char* e = std::getenv("GESPMM_HUB_SPLIT");
+    return e ? std::atoi(e) : 0;
+  }();
+  int c = (forced == 1 || forced == 2 || forced == 4) ? forced : (big ? 2 : 1);
+  while (c > width) c >>= 1;
+  return c;
+}
 uint32_t hub_tile_width(uint32_t n, uint32_t n_hub) {
-  return uint32_t(32 * kHubConsumers * hub_vec(n, n_hub));
+  return uint32_t(32 * hub_vec(n, n_hub));
 }
 
 cudaError_t launch_tuned_hub(int op, bool fast, const SpmmArgs& a, cudaStream_t st, bool big) {
-  const int v = hub_vec(a.n, a.n_sched);
+  const int w = hub_vec(a.n, a.n_sched);  // tile = 32 * w columns
+  const int c = hub_split(w, big);
+  const int v = w / c;
   switch (op) {
-    case kSum: return fast ? hub_dispatch<kSum, true>(v, big, a, st) : hub_dispatch<kSum, false>(v, big, a, st);
-    case kMean: return fast ? hub_dispatch<kMean, true>(v, big, a, st) : hub_dispatch<kMean, false>(v, big, a, st);
-    case kMax: return hub_dispatch<kMax, false>(v, big, a, st);
-    default: return hub_dispatch<kMin, false>(v, big, a, st);
+    case kSum: return fast ? hub_dispatch<kSum, true>(v, c, big, a, st) : hub_dispatch<kSum, false>(v, c, big, a, st);
+    case kMean: return fast ? hub_dispatch<kMean, true>(v, c, big, a, st) : hub_dispatch<kMean, false>(v, c, big, a, st);
+    case kMax: return hub_dispatch<kMax, false>(v, c, big, a, st);
+    default: return hub_dispatch<kMin, false>(v, c, big, a, st);
   }
 }
 
