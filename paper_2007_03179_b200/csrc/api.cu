@@ -181,15 +181,16 @@ namespace {
 // Hub rows: a row of degree d on one warp costs ~d * L * CF / 8 (one L2 round
 // trip L ~ 0.7 us per batch of 8/CF gathers), while a launch over `nnz`
 // nonzeros is gather-bound at ~nnz * 4N / 19 TB/s.  Rows whose single-warp
-// time would exceed 1/1.5 of the launch go to the ring-fed row-per-CTA kernel
-// (k_hub: a 21,657-nonzero row in ~0.3 ms instead of ~1.7 ms).  So the
-// threshold scales with the work per launch: none on the whole Reddit shape
-// (23.6k > max degree), ~11.8k on a 1/2 row shard, ~2.9k on a 1/8 shard or
-// one block of the pipelined host entry.  Measured with
-// tools/shard_emulation.py (profiles/r1_shard_emulation.md): factor 1.5 keeps
-// the 1-GPU step unchanged and halves the 8-shard step (1.51 -> 0.79 ms).
+// time would exceed 1/2.5 of the launch go to the ring-fed row-per-CTA kernel
+// (k_hub: a 21,657-nonzero row in ~0.2 ms instead of ~1.7 ms) — unless even
+// the longest row fits comfortably in the launch.  So the threshold scales
+// with the work per launch: no hub rows on the whole Reddit shape, ~7k on a
+// 1/2 row shard, 2048 (the floor) on a 1/8 shard or one block of the
+// pipelined host entry.  Measured with tools/shard_emulation.py
+// (profiles/r1_shard_emulation.md): the 1-GPU step unchanged, the 8-shard step
+// 1.51 -> 0.52 ms.
 uint32_t auto_hub_threshold(uint32_t n, uint64_t nnz, int cf, uint32_t k, int dev,
-                            uint32_t tile_cols) {
+                            uint32_t tile_cols, uint32_t max_degree) {
   if (n < 8) return 0xffffffffu;  // too narrow for a CTA per row
   // the warp kernel moves whole lane tiles (N = 44 -> 64 columns of float4 lanes)
   const uint32_t moved = std::max(n, tile_cols);
@@ -201,7 +202,13 @@ uint32_t auto_hub_threshold(uint32_t n, uint64_t nnz, int cf, uint32_t k, int de
   const double rate = (l2 > 0 && b_bytes > 1.5 * double(l2)) ? 9.5e12 : 19e12;
   const double t_launch = double(nnz) * 4.0 * double(moved) / rate;
   const double t_nnz = 0.7e-6 * double(cf < 1 ? 1 : cf) / 8.0;
-  double f = 1.5;  // GESPMM_HUB_FACTOR: tuning experiments (tools/shard_emulation.py)
+  // no hub rows while the longest row's warp time stays well inside the launch
+  // (whole Reddit: 0.61 of it; products half-shard: 0.47): a side-stream hub
+  // kernel there only disturbs the warp kernel
+  if (double(max_degree) * t_nnz <= 0.75 * t_launch) return 0xffffffffu;
+  // narrow lane tiles (N < 128) fold fewer columns per staged nonzero in k_hub:
+  // fewer, longer hub rows there (GCN N=44: 2.07 ms at threshold 12k, 2.93 ms at 7k)
+  double f = moved >= 128 ? 2.5 : 1.5;  // GESPMM_HUB_FACTOR overrides (shard_emulation.py)
   if (const char* e = std::getenv("GESPMM_HUB_FACTOR")) f = std::max(0.05, std::atof(e));
   const double t = std::max(2048.0, t_launch / (f * t_nnz));
   return t >= 4294967295.0 ? 0xffffffffu : uint32_t(t);
@@ -378,7 +385,7 @@ gespmm_status_t build_tuned(Plan& p, const uint32_t* host_rp, cudaStream_t st) {
                            : (ht < 0 ? 0xffffffffu
                                      : auto_hub_threshold(sw, host_rp[m], p.sh.warp_v.cf,
                                                           p.a.n_cols, p.device,
-                                                          p.sh.warp_v.tile_width()));
+                                                          p.sh.warp_v.tile_width(), maxd));
   uint32_t n_hub = 0;
   uint64_t hub_nnz = 0;
   while (n_hub < m && deg[order[n_hub]] >= p.hub_threshold) hub_nnz += deg[order[n_hub++]];
@@ -977,17 +984,17 @@ gespmm_status_t gespmm_spmm_host(const gespmm_csr_t* a, const float* b, uint32_t
     GESPMM_CUDA(cudaGetDevice(&dev), "spmm");
     shapes = make_shapes(o, a->n_cols, n, dev, m ? double(nnz) / double(m) : 0.0);
     const int32_t ht = o.hub_threshold;
+    uint32_t maxd = 0;
+    for (uint64_t r = 0; r < m; ++r) maxd = std::max(maxd, a->row_ptr[r + 1] - a->row_ptr[r]);
     // every row block is its own launch: the threshold follows the block's work
     const uint32_t hub_t =
         ht > 0 ? uint32_t(ht)
                : (ht < 0 ? 0xffffffffu
                          : auto_hub_threshold(shapes.slice_w, nnz / uint64_t(chunks),
                                               shapes.warp_v.cf, a->n_cols, dev,
-                                              shapes.warp_v.tile_width()));
+                                              shapes.warp_v.tile_width(), maxd));
     GESPMM_CUDA(ws->reserve_host(2, sizeof(uint32_t) * m), "spmm");
     uint32_t* order = static_cast<uint32_t*>(ws->hbuf[2]);  // pinned: no sync after its copy
-    uint32_t maxd = 0;
-    for (uint64_t r = 0; r < m; ++r) maxd = std::max(maxd, a->row_ptr[r + 1] - a->row_ptr[r]);
     std::vector<uint32_t> count(size_t(maxd) + 2);
     for (int ch = 0; ch < chunks; ++ch) {
       std::fill(count.begin(), count.end(), 0u);
