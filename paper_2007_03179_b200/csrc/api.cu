@@ -1088,14 +1088,17 @@ gespmm_status_t gespmm_spmm_host(const gespmm_csr_t* a, const float* b, uint32_t
     tr.dev("block " + std::to_string(ch) + " CSR landed", ws->in);
     GESPMM_CUDA(cudaEventRecord(ws->ev_in[ch], ws->in), "spmm");
     GESPMM_CUDA(cudaStreamWaitEvent(ws->stream, ws->ev_in[ch], 0), "spmm");
-    if (pe > ps && nexc != UINT64_MAX) {
+    const bool packed_blk = pe > ps && nexc != UINT64_MAX;
+    if (packed_blk) {
+      // the unpack also runs the column check on the rebuilt columns
       GESPMM_CUDA(unpack_cols(d_enc + ps, reinterpret_cast<const uint2*>(d_exc + 2 * exc_off),
                               uint32_t(nexc), d_rp + lo, hi - lo, ps, pe, nnz, bits, d_ci,
-                              scan_tmp, scan_bytes, ws->stream),
+                              scan_tmp, scan_bytes, ws->stream, a->n_cols,
+                              cc ? colcheck_key(cc) : nullptr),
                   "spmm");
       exc_off += nexc;
     }
-    if (cc)
+    if (cc && !packed_blk)
       GESPMM_CUDA(colcheck_rows(cc, d_rp + lo, hi - lo, ps, pe, d_ci, a->n_cols, nnz, ws->stream),
                   "spmm");
     SpmmArgs args{};

@@ -144,9 +144,14 @@ __global__ void __launch_bounds__(kUnpackThreads) k_unpack_carry(const SegVal* _
   }
 }
 
+// Writes the block's columns; with bad_key also runs the column part of the
+// canonical check on them (k_check_positions' job, without re-reading col_ind):
+// key 2p = column out of range at p, 2p + 1 = not increasing within its row.
 __global__ void __launch_bounds__(kUnpackThreads) k_unpack_apply(Decode d, uint64_t len,
                                                                  const SegVal* __restrict__ carry,
-                                                                 uint32_t* __restrict__ col) {
+                                                                 uint32_t* __restrict__ col,
+                                                                 uint32_t k_cols,
+                                                                 unsigned long long* bad_key) {
   __shared__ UnpackSmem sm;
   SegVal x[kUnpackItems];
   load_decode(d, len, sm, x);
@@ -158,10 +163,23 @@ __global__ void __launch_bounds__(kUnpackThreads) k_unpack_apply(Decode d, uint6
   BlockScanT(sm.scan).ExclusiveScan(t, ex, SegAdd{}, pre);
   uint32_t out[kUnpackItems];
   SegVal run = ex;
+  unsigned long long worst = ~0ull;
+  const uint64_t i0 = uint64_t(blockIdx.x) * kUnpackChunk + uint64_t(threadIdx.x) * kUnpackItems;
 #pragma unroll
   for (int j = 0; j < kUnpackItems; ++j) {
+    const uint32_t prev = run.v;  // the previous position's column
     run = SegAdd{}(run, x[j]);
     out[j] = run.v;
+    if (bad_key && i0 + j < len) {
+      const uint64_t p = d.ps + i0 + j;
+      const bool first = (d.bits[p >> 5] >> (p & 31u)) & 1u;
+      if (run.v >= k_cols) worst = min(worst, 2ull * p);
+      else if (!first && run.v <= prev) worst = min(worst, 2ull * p + 1);
+    }
+  }
+  if (bad_key) {
+    for (int o = 16; o; o >>= 1) worst = min(worst, __shfl_xor_sync(0xffffffffu, worst, o));
+    if ((threadIdx.x & 31) == 0 && worst != ~0ull) atomicMin(bad_key, worst);
   }
   __syncthreads();  // scan storage is reused by the store
   const uint64_t c0 = uint64_t(blockIdx.x) * kUnpackChunk;
@@ -179,7 +197,7 @@ size_t unpack_temp_bytes(uint64_t max_len) {
 cudaError_t unpack_cols(const uint16_t* enc, const uint2* exc, uint32_t n_exc,
                         const uint32_t* row_ptr_block, uint32_t m_block, uint64_t ps, uint64_t pe,
                         uint64_t nnz, uint32_t* bits, uint32_t* col, void* temp, size_t temp_bytes,
-                        cudaStream_t st) {
+                        cudaStream_t st, uint32_t k_cols, unsigned long long* bad_key) {
   if (pe <= ps) return cudaSuccess;
   const uint64_t len = pe - ps;
   const uint64_t chunks = (len + kUnpackChunk - 1) / kUnpackChunk;
@@ -201,7 +219,7 @@ cudaError_t unpack_cols(const uint16_t* enc, const uint2* exc, uint32_t n_exc,
   const Decode d{enc, col, bits, ps};
   k_unpack_agg<<<uint32_t(chunks), kUnpackThreads, 0, st>>>(d, len, aggs);
   k_unpack_carry<<<1, kUnpackThreads, 0, st>>>(aggs, uint32_t(chunks), carry);
-  k_unpack_apply<<<uint32_t(chunks), kUnpackThreads, 0, st>>>(d, len, carry, col);
+  k_unpack_apply<<<uint32_t(chunks), kUnpackThreads, 0, st>>>(d, len, carry, col, k_cols, bad_key);
   note_launch();
   note_launch();
   note_launch();

@@ -100,10 +100,12 @@ uint64_t pack_cols_block(const uint32_t* row_ptr, const uint32_t* col_ind, uint3
 size_t unpack_temp_bytes(uint64_t max_len);
 // rows [0, m_block) of row_ptr_block own positions [ps, pe); bits: zeroed
 // row-start bitmap over all nnz positions (shared with the column check).
+// bad_key (nullable): also check the rebuilt columns (bounds k_cols, strictly
+// increasing within rows) into the column check's first-violation key.
 cudaError_t unpack_cols(const uint16_t* enc, const uint2* exc, uint32_t n_exc,
                         const uint32_t* row_ptr_block, uint32_t m_block, uint64_t ps, uint64_t pe,
                         uint64_t nnz, uint32_t* bits, uint32_t* col, void* temp, size_t temp_bytes,
-                        cudaStream_t st);
+                        cudaStream_t st, uint32_t k_cols = 0, unsigned long long* bad_key = nullptr);
 
 // Device canonical check of a device CSR, formatted as the reference's
 // require_canonical(m, who) error (csr.hpp:155-158).  Synchronises `st`.
@@ -125,6 +127,7 @@ cudaError_t validate_csr_device(uint32_t m, uint32_t k, uint64_t nnz, const uint
 // the block's first row_ptr entry; positions stay global), end (locates the
 // first violation's row, synchronises `st`, frees).
 struct ColCheck;
+unsigned long long* colcheck_key(ColCheck* c);  // its first-violation key (device)
 size_t colcheck_workspace_bytes(uint64_t nnz);
 cudaError_t colcheck_begin(ColCheck** out, uint64_t nnz, void* ws, cudaStream_t st);
 // rows [0, m_chunk) of row_ptr_chunk own positions [ps, pe)

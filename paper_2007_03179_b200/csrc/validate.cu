@@ -167,6 +167,8 @@ cudaError_t colcheck_begin(ColCheck** out, uint64_t nnz, void* ws, cudaStream_t 
   return cudaSuccess;
 }
 
+unsigned long long* colcheck_key(ColCheck* c) { return &c->s->first_bad_key; }
+
 cudaError_t colcheck_rows(ColCheck* c, const uint32_t* row_ptr_chunk, uint32_t m_chunk,
                           uint64_t ps, uint64_t pe, const uint32_t* col_ind, uint32_t k,
                           uint64_t usable, cudaStream_t st) {
