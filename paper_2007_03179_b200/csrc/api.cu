@@ -320,8 +320,12 @@ gespmm_status_t launch_tuned_rows(const TunedShapes& t, int op, bool fast, const
       h.n_sched = n_hub;
       // TMA-ring hub kernel when bulk copies can address the B slices (16-byte
       // units: N % 4 == 0, ld % 4 == 0, 16-byte aligned B/C/arg at this offset)
-      const bool tma = w % 4 == 0 && a.ld % 4 == 0 && aligned(sa.b, 16) && aligned(sa.c, 16) &&
-                       (!sa.arg || aligned(sa.arg, 16));
+      static const bool force_cta = [] {  // GESPMM_HUB_KCTA=1: A/B against the LDG CTA kernel
+        const char* e = std::getenv("GESPMM_HUB_KCTA");
+        return e && e[0] == '1';
+      }();
+      const bool tma = !force_cta && w % 4 == 0 && a.ld % 4 == 0 && aligned(sa.b, 16) &&
+                       aligned(sa.c, 16) && (!sa.arg || aligned(sa.arg, 16));
       const uint32_t tw = tma ? hub_tile_width(w, n_hub) : uint32_t(cs.vec * cs.warps * 32);
       h.n_tiles = (w + tw - 1) / tw;
       if (tma && (hub_pdl || !side)) {
