@@ -320,6 +320,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_cta(SpmmArgs a) {
   __syncthreads();
 
   const float* bcol = a.b + col0;
+  const float* bsafe = colok ? bcol : a.b;
   for (uint32_t off = 0, buf = 0; off < len; off += CHUNK, buf ^= 1u) {
     // issue the next chunk's sparse loads before consuming this one
     uint2 nxt[PER_T];
@@ -336,12 +337,14 @@ __global__ void __launch_bounds__(WARPS * 32) k_cta(SpmmArgs a) {
       uint2 kv[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) kv[u] = s_kv[buf][kk + u];
+      // unpredicated gathers (slots past the chunk re-read the batch's first
+      // row, lanes past N read column 0): predicated loads let ptxas interleave
+      // them with the folds, and the U loads in flight collapse to ~1
       Vec<VEC> bv[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-#pragma unroll
-        for (int e = 0; e < VEC; ++e) bv[u].x[e] = 0.0f;
-        if (colok && kk + u < n_cur) bv[u] = ld_keep<VEC>(bcol + uint64_t(kv[u].x) * a.ld, pol.keep);
+        const uint32_t k = (kk + u < n_cur) ? kv[u].x : kv[0].x;
+        bv[u] = ld_keep<VEC>(bsafe + uint64_t(k) * a.ld, pol.keep);
       }
 #pragma unroll
       for (int u = 0; u < U; ++u) {
