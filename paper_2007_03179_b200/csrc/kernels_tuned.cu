@@ -2,8 +2,8 @@
 //
 // k_warp — row per (sub)warp.  Coalesced Row Caching: the LPR lanes that own a
 //   row load the next LPR (col, val) pairs of the row with one coalesced load
-//   each (prefetched one chunk ahead) and broadcast them with shuffles, so
-//   col_ind/vals are read once per row tile.  Lanes own VEC contiguous columns
+//   each (prefetched one chunk ahead) into a per-warp shared tile and read them
+//   back with broadcast LDS.128, so col_ind/vals are read once per row tile.  Lanes own VEC contiguous columns
 //   and gather B rows with 16-byte (float4) loads.  Coarse-grained Warp
 //   Merging: each lane owns CF column sub-tiles, so one staged nonzero feeds
 //   CF vector gathers.  U nonzeros are gathered before any is folded (memory-
@@ -11,12 +11,17 @@
 //   element is still reduced by one thread in CSR order, so results are
 //   bit-identical to the reference fold (kernel.hpp:287-343) in exact mode.
 //
-// k_cta — row per CTA, for hub rows of power-law graphs.  The CTA stages the
-//   row's sparse segment into shared memory (double-buffered), and its warps
-//   split the COLUMNS of the row (never the nonzeros), keeping the per-element
-//   ascending fold and with it bit-exactness; a deeper gather batch (32 scalar
-//   or 8 vector loads per lane) gives the hub the latency hiding a single warp
-//   cannot.
+// k_hub — row per CTA for hub rows (the rows whose single-warp time would
+//   bound a launch): producer warps stream the row's B slices into a
+//   shared-memory ring with LDGSTS + mbarriers, consumer warps fold them in
+//   order (see the comment at the kernel).
+//
+// k_cta — row per CTA for hub rows the ring cannot address (N % 4 != 0,
+//   misaligned B/C).  The CTA stages the row's sparse segment into shared
+//   memory (double-buffered), and its warps split the COLUMNS of the row (never
+//   the nonzeros), keeping the per-element ascending fold and with it
+//   bit-exactness; a deeper gather batch (32 scalar or 8 vector loads per lane)
+//   gives the hub the latency hiding a single warp cannot.
 #include <algorithm>
 #include <atomic>
 #include <cstdlib>
