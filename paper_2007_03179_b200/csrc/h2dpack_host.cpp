@@ -1,11 +1,13 @@
 // Packed column indices for the host entry's PCIe upload (host side; the
 // device side and the format are described in h2dpack.cu).  Encoding runs on
-// all host threads (OpenMP) while the copy engine moves the previous block.
+// most host threads (OpenMP) while the copy engine moves the previous block.
 #include <omp.h>
 #include <stdint.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
+#include <thread>
 #include <vector>
 
 namespace gespmm {
@@ -17,7 +19,15 @@ namespace gespmm {
 uint64_t pack_cols_block(const uint32_t* row_ptr, const uint32_t* col_ind, uint32_t lo,
                          uint32_t hi, uint16_t* enc, uint32_t* exc /* pairs */, uint64_t max_exc) {
   const uint64_t ps = row_ptr[lo];
-  const int nt = std::max(1, omp_get_max_threads());
+  // three quarters of the host threads unless OMP_NUM_THREADS says otherwise:
+  // with every core packing, the packing contends with the copy engine's reads
+  // of host memory and with the CUDA driver threads (Reddit, 16 cores: 17.9 ms
+  // at 16 threads, 16.3 ms at 12, 16.7-19.3 ms at 8; tools/e2e_threads.py)
+  static const int nt = [] {
+    if (std::getenv("OMP_NUM_THREADS")) return std::max(1, omp_get_max_threads());
+    const int hw = int(std::thread::hardware_concurrency());
+    return std::max(1, hw > 4 ? hw * 3 / 4 : hw);
+  }();
   // rows split by nnz across threads
   std::vector<uint32_t> cut(size_t(nt) + 1, hi);
   cut[0] = lo;
