@@ -60,8 +60,14 @@ constexpr int kWarpBlock = 4;  // warps per CTA: 72-register kernel -> 7 CTAs = 
 // max/min carry 2*CF*VEC accumulator registers (value + arg): 6 CTAs per SM
 // (85 registers; 4 at CF=4) instead of spilling under the 7-CTA cap.
 template <int OP, int CF>
+// CF=4 sum/mean shapes (low-degree rows, e.g. Pubmed): 6 CTAs per SM; 7 or 8
+// (<= 64 registers, spills) measured no faster on Pubmed N=128 (14.4 vs
+// 14.4/15.2/16.4 us median)
+#ifndef GESPMM_CF4_BLOCKS
+#define GESPMM_CF4_BLOCKS 6
+#endif
 constexpr int warp_min_blocks() {
-  return Reduce<OP>::kHasArg ? (CF >= 4 ? 4 : 6) : (CF >= 4 ? 6 : 7);
+  return Reduce<OP>::kHasArg ? (CF >= 4 ? 4 : 6) : (CF >= 4 ? GESPMM_CF4_BLOCKS : 7);
 }
 
 template <int LPR, int CF>
