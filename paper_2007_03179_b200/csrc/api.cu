@@ -248,7 +248,10 @@ TunedShapes make_shapes(const gespmm_options_t& o, uint32_t k, uint32_t n, int d
   t.n = n;
   t.slices = pick_slices(o, k, n, dev);
   uint32_t w = (n + t.slices - 1) / t.slices;
-  if (n % 4 == 0) w = (w + 3) & ~3u;  // slice offsets keep float4 alignment
+  // slice offsets keep the lanes' vector alignment (float4 at N % 4 == 0,
+  // float2 at even N; an odd offset made float2 loads fault — fuzz test)
+  if (n % 4 == 0) w = (w + 3) & ~3u;
+  else if (n % 2 == 0) w = (w + 1) & ~1u;
   t.slice_w = std::max<uint32_t>(1, std::min(w, n));
   t.slices = (n + t.slice_w - 1) / t.slice_w;
   const uint32_t sw = t.slice_w;
@@ -299,9 +302,11 @@ gespmm_status_t launch_tuned_rows(const TunedShapes& t, int op, bool fast, const
     WarpShape wsc = narrow ? pick_warp_shape(w, false, false) : t.warp_s;
     const CtaShape cv = narrow ? pick_cta_shape(w, n4, n2) : t.cta_v;
     const CtaShape csc = narrow ? pick_cta_shape(w, false, false) : t.cta_s;
-    const WarpShape& ws = v_ok ? wv : wsc;
-    const CtaShape& cs = v_ok ? cv : csc;
-    const WarpShape& wsel = (ws.vec == 2 && !v2_ok) ? wsc : ws;
+    // the slice's own offset must keep the vector alignment too
+    const bool sv_ok = v_ok && off % 4 == 0, sv2_ok = v2_ok && off % 2 == 0;
+    const WarpShape& ws = sv_ok ? wv : wsc;
+    const CtaShape& cs = sv_ok ? cv : csc;
+    const WarpShape& wsel = (ws.vec == 2 && !sv2_ok) ? wsc : ws;
     SpmmArgs sa = a;
     sa.b = a.b + off;
     sa.c = a.c + off;

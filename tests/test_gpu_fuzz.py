@@ -1,0 +1,129 @@
+"""GPU: randomized parity sweep (hypothesis, fixed seed, bounded examples).
+Random canonical CSR shapes (empty rows, single-entry rows, a long row),
+random N (odd and even, 1..300), every op with edge/column args, every
+kernel variant and the tuned path's options (hub threshold, rows per warp,
+column slices, packed upload); exact mode must equal the oracle bit for bit."""
+import os
+
+import numpy as np
+import pytest
+from hypothesis import HealthCheck, given, seed, settings
+from hypothesis import strategies as st
+
+import oracle as O
+import paper_2007_03179_b200 as G
+from conftest import first_divergence
+
+pytestmark = pytest.mark.gpu
+
+
+def _matrix(rng, m, k, density, long_row):
+    rp = [0]
+    cols = []
+    for r in range(m):
+        d = int(rng.binomial(k, density))
+        if long_row and r == m // 2:
+            d = k
+        c = np.sort(rng.choice(k, size=min(d, k), replace=False)) if d else np.zeros(0, np.int64)
+        cols.append(c.astype(np.uint32))
+        rp.append(rp[-1] + len(c))
+    ci = np.concatenate(cols) if cols else np.zeros(0, np.uint32)
+    a = G.CsrMatrix(m, k, np.asarray(rp, np.uint32), ci, np.zeros(len(ci), np.float32))
+    G.randomize_values(a, int(rng.integers(1 << 30)))
+    return a
+
+
+VARIANTS = [G.KernelVariant.tuned(), G.KernelVariant.naive(), G.KernelVariant.crc(),
+            G.KernelVariant.crc_cwm(2), G.KernelVariant.crc_cwm(4), G.KernelVariant.crc_cwm(8)]
+
+
+@seed(20261017)
+@settings(max_examples=int(os.environ.get("FUZZ_EXAMPLES", "60")), deadline=None, suppress_health_check=[HealthCheck.too_slow])
+@given(m=st.integers(0, 300), k=st.integers(1, 400), density=st.floats(0.0, 0.3),
+       long_row=st.booleans(), n=st.integers(1, 300), op=st.sampled_from(["sum", "mean", "max", "min"]),
+       column_arg=st.booleans(), vi=st.integers(0, len(VARIANTS) - 1),
+       hub=st.sampled_from([0, 1, 5, -1]), rpw=st.sampled_from([0, 1, 2, 4]),
+       slices=st.sampled_from([0, 1, 2, 3]), pack=st.sampled_from([0, 1, -1]),
+       data=st.integers(0, 1 << 30))
+def test_random_shapes_every_path_bit_exact(m, k, density, long_row, n, op, column_arg, vi, hub,
+                                            rpw, slices, pack, data):
+    if os.environ.get("FUZZ_LOG"):  # a CUDA fault poisons the context: log before running
+        with open(os.environ["FUZZ_LOG"], "a") as f:
+            f.write(repr(dict(m=m, k=k, density=density, long_row=long_row, n=n, op=op,
+                              column_arg=column_arg, vi=vi, hub=hub, rpw=rpw, slices=slices,
+                              pack=pack, data=data)) + "\n")
+    rng = np.random.default_rng(data)
+    a = _matrix(rng, m, k, density, long_row)
+    b = G.make_random_dense(k, n, data + 1)
+    want_arg = op in ("max", "min")
+    kind = O.ARG_COLUMN if column_arg else O.ARG_EDGE
+    want, warg = O.spmm(a.n_rows, a.n_cols, a.row_ptr, a.col_ind, a.vals, b.data, op,
+                        want_arg=want_arg, arg_kind=kind)
+    ex = G.ExecOptions(arg_kind="column" if column_arg else "edge", hub_threshold=hub,
+                       rows_per_warp=rpw, col_slices=slices, h2d_pack=pack)
+    try:
+        c, arg = G.native_spmm_arg(a, b, VARIANTS[vi], G.reduce_op_by_name(op), exec=ex,
+                                   want_arg=want_arg)
+    except G.Error as e:
+        if os.environ.get("FUZZ_LOG"):
+            with open(os.environ["FUZZ_LOG"], "a") as f:
+                f.write(f"FAIL {e}\n")
+        raise
+    assert first_divergence(c.data, want) is None
+    if want_arg:
+        assert np.array_equal(arg, warg)
+
+
+@seed(20261018)
+@settings(max_examples=int(os.environ.get("FUZZ_EXAMPLES", "60")), deadline=None,
+          suppress_health_check=[HealthCheck.too_slow])
+@given(m=st.integers(1, 400), k=st.integers(1, 600), density=st.floats(0.0, 0.2),
+       long_row=st.booleans(), n=st.one_of(st.integers(1, 300), st.integers(500, 1100)),
+       op=st.sampled_from(["sum", "mean", "max", "min"]), column_arg=st.booleans(),
+       hub=st.sampled_from([0, 1, 7, -1]), rpw=st.sampled_from([0, 1, 2, 4, 8]),
+       slices=st.sampled_from([0, 1, 2, 5]), tuned_cf=st.sampled_from([0, 1, 2, 4]),
+       hot=st.sampled_from([0, 1]), replicas=st.sampled_from([1, 1, 3]),
+       data=st.integers(0, 1 << 30))
+def test_random_device_plans_bit_exact(m, k, density, long_row, n, op, column_arg, hub, rpw, slices,
+                                       tuned_cf, hot, replicas, data):
+    """Device plans (tuned) over random shapes and options, executed plain or
+    with the fused all-gather epilogue into extra replicas."""
+    import torch
+    if os.environ.get("FUZZ_LOG"):
+        with open(os.environ["FUZZ_LOG"], "a") as f:
+            f.write(repr(dict(plan=1, m=m, k=k, density=density, long_row=long_row, n=n, op=op,
+                              column_arg=column_arg, hub=hub, rpw=rpw, slices=slices,
+                              tuned_cf=tuned_cf, hot=hot, replicas=replicas, data=data)) + "\n")
+    rng = np.random.default_rng(data)
+    a = _matrix(rng, m, k, density, long_row)
+    b = G.make_random_dense(k, n, data + 1)
+    want_arg = op in ("max", "min")
+    kind = O.ARG_COLUMN if column_arg else O.ARG_EDGE
+    want, warg = O.spmm(a.n_rows, a.n_cols, a.row_ptr, a.col_ind, a.vals, b.data, op,
+                        want_arg=want_arg, arg_kind=kind)
+    dev = torch.device("cuda:0")
+    d = G.DeviceCsr.from_host(a, dev)
+    bt = torch.from_numpy(b.data).to(dev)
+    ex = G.ExecOptions(arg_kind="column" if column_arg else "edge", hub_threshold=hub,
+                       rows_per_warp=rpw, col_slices=slices, tuned_cf=tuned_cf, l2_hot_mb=hot)
+    plan = G.Plan(d, n, op, exec=ex)
+    cs = [torch.full((m, n), -3.0, device=dev) for _ in range(replicas)]
+    args = [torch.full((m, n), -5, dtype=torch.int32, device=dev) for _ in range(replicas)] \
+        if want_arg else None
+    try:
+        if replicas == 1:
+            plan.execute(bt, cs[0], args[0] if args else None)
+        else:
+            plan.execute_gather(bt, [c.data_ptr() for c in cs],
+                                [x.data_ptr() for x in args] if args else None)
+        torch.cuda.synchronize()
+    except G.Error as e:
+        if os.environ.get("FUZZ_LOG"):
+            with open(os.environ["FUZZ_LOG"], "a") as f:
+                f.write(f"FAIL {e}\n")
+        raise
+    for i in range(replicas):
+        assert first_divergence(cs[i].cpu().numpy(), want) is None, i
+        if want_arg:
+            assert np.array_equal(args[i].cpu().numpy(), warg), i
+    plan.close()
