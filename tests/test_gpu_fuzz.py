@@ -83,17 +83,23 @@ def test_random_shapes_every_path_bit_exact(m, k, density, long_row, n, op, colu
        hub=st.sampled_from([0, 1, 7, -1]), rpw=st.sampled_from([0, 1, 2, 4, 8]),
        slices=st.sampled_from([0, 1, 2, 5]), tuned_cf=st.sampled_from([0, 1, 2, 4]),
        hot=st.sampled_from([0, 1]), replicas=st.sampled_from([1, 1, 3]),
-       data=st.integers(0, 1 << 30))
+       misalign=st.booleans(), exact=st.sampled_from([True, True, False]),
+       cluster=st.sampled_from([0, 0, 0, 2, 8]), data=st.integers(0, 1 << 30))
 def test_random_device_plans_bit_exact(m, k, density, long_row, n, op, column_arg, hub, rpw, slices,
-                                       tuned_cf, hot, replicas, data):
+                                       tuned_cf, hot, replicas, misalign, exact, cluster, data):
     """Device plans (tuned) over random shapes and options, executed plain or
-    with the fused all-gather epilogue into extra replicas."""
+    with the fused all-gather epilogue into extra replicas; B/C based 4 bytes
+    off 16-byte alignment (scalar fallbacks); the cluster-DSMEM cache at N=128;
+    fast mode (FFMA) for sum/mean within the documented tolerance."""
     import torch
+    if cluster and n != 128:
+        n = 128
     if os.environ.get("FUZZ_LOG"):
         with open(os.environ["FUZZ_LOG"], "a") as f:
             f.write(repr(dict(plan=1, m=m, k=k, density=density, long_row=long_row, n=n, op=op,
                               column_arg=column_arg, hub=hub, rpw=rpw, slices=slices,
-                              tuned_cf=tuned_cf, hot=hot, replicas=replicas, data=data)) + "\n")
+                              tuned_cf=tuned_cf, hot=hot, replicas=replicas, misalign=misalign,
+                              exact=exact, cluster=cluster, data=data)) + "\n")
     rng = np.random.default_rng(data)
     a = _matrix(rng, m, k, density, long_row)
     b = G.make_random_dense(k, n, data + 1)
@@ -103,13 +109,20 @@ def test_random_device_plans_bit_exact(m, k, density, long_row, n, op, column_ar
                         want_arg=want_arg, arg_kind=kind)
     dev = torch.device("cuda:0")
     d = G.DeviceCsr.from_host(a, dev)
-    bt = torch.from_numpy(b.data).to(dev)
+    sh = 1 if misalign else 0
+
+    def buf(shape, fill, dtype=torch.float32):  # optionally 4 bytes past 16-byte alignment
+        flat = torch.full((shape[0] * shape[1] + sh,), fill, dtype=dtype, device=dev)
+        return flat[sh:].view(shape)
+    bt = buf((k, n), 0.0)
+    bt.copy_(torch.from_numpy(b.data))
+    fast = not exact and op in ("sum", "mean")
     ex = G.ExecOptions(arg_kind="column" if column_arg else "edge", hub_threshold=hub,
-                       rows_per_warp=rpw, col_slices=slices, tuned_cf=tuned_cf, l2_hot_mb=hot)
+                       rows_per_warp=rpw, col_slices=slices, tuned_cf=tuned_cf, l2_hot_mb=hot,
+                       exact=not fast, cluster_hot=cluster)
     plan = G.Plan(d, n, op, exec=ex)
-    cs = [torch.full((m, n), -3.0, device=dev) for _ in range(replicas)]
-    args = [torch.full((m, n), -5, dtype=torch.int32, device=dev) for _ in range(replicas)] \
-        if want_arg else None
+    cs = [buf((m, n), -3.0) for _ in range(replicas)]
+    args = [buf((m, n), -5, torch.int32) for _ in range(replicas)] if want_arg else None
     try:
         if replicas == 1:
             plan.execute(bt, cs[0], args[0] if args else None)
@@ -122,8 +135,18 @@ def test_random_device_plans_bit_exact(m, k, density, long_row, n, op, column_ar
             with open(os.environ["FUZZ_LOG"], "a") as f:
                 f.write(f"FAIL {e}\n")
         raise
-    for i in range(replicas):
-        assert first_divergence(cs[i].cpu().numpy(), want) is None, i
-        if want_arg:
-            assert np.array_equal(args[i].cpu().numpy(), warg), i
+    if fast:  # |delta| <= 1e-5 * max(|want|, sum |v * b|)
+        mag, _ = O.spmm(a.n_rows, a.n_cols, a.row_ptr, a.col_ind, np.abs(a.vals),
+                        np.abs(b.data), "sum")
+        if op == "mean":
+            deg = np.maximum(np.diff(a.row_ptr.astype(np.int64)), 1).astype(np.float32)
+            mag = mag / deg[:, None]
+        for i in range(replicas):
+            got = cs[i].cpu().numpy()
+            assert np.all(np.abs(got - want) <= 1e-5 * np.maximum(np.abs(want), mag) + 1e-30), i
+    else:
+        for i in range(replicas):
+            assert first_divergence(cs[i].cpu().numpy(), want) is None, i
+            if want_arg:
+                assert np.array_equal(args[i].cpu().numpy(), warg), i
     plan.close()
