@@ -1123,6 +1123,7 @@ gespmm_status_t gespmm_spmm_host(const gespmm_csr_t* a, const float* b, uint32_t
       GESPMM_CUDA(colcheck_rows(cc, d_rp + lo, hi - lo, ps, pe, d_ci, a->n_cols, nnz, ws->stream),
                   "spmm");
     SpmmArgs args{};
+    args.abort_if = cc ? colcheck_key(cc) : nullptr;  // skip the block's kernels on a violation
     args.row_ptr = d_rp + lo;  // positions stay global; rows and outputs are block-local
     args.col_ind = d_ci;
     args.vals = d_v;

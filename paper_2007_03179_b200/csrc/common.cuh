@@ -335,7 +335,16 @@ struct SpmmArgs {
   float* c_mc;
   int32_t* arg_mc;
   uint32_t* work;  // hub kernel: unit counter of a persistent launch (zeroed before it), or null
+  // Host entry's pipelined validation: the column check of a row block runs
+  // just before its kernels on the same stream; a kernel returns at once when
+  // this key (the first violation found so far, ~0 = none) is set, so
+  // non-canonical columns are never dereferenced.  Null: no check.
+  const unsigned long long* abort_if;
 };
+
+__device__ __forceinline__ bool aborted(const SpmmArgs& a) {
+  return a.abort_if && *reinterpret_cast<const volatile unsigned long long*>(a.abort_if) != ~0ull;
+}
 
 // Epilogue replicas of one output vector (element offset o from c / arg).
 template <int VEC, bool ARG>

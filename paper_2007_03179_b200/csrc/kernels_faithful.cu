@@ -18,6 +18,7 @@ constexpr int kBatch = 4;          // nonzeros gathered per batch in every varia
 // column index and value, then one unit-stride B load per lane.
 template <int OP, bool FAST>
 __global__ void __launch_bounds__(256) k_naive(SpmmArgs a) {
+  if (aborted(a)) return;
   using R = Reduce<OP>;
   const uint64_t warp = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const uint32_t lane = threadIdx.x & 31;
@@ -75,6 +76,7 @@ __global__ void __launch_bounds__(256) k_naive(SpmmArgs a) {
 // column slices of 32 lanes.  CF = 1 is plain CRC.
 template <int OP, bool FAST, int CF>
 __global__ void __launch_bounds__(256) k_crc(SpmmArgs a) {
+  if (aborted(a)) return;
   using R = Reduce<OP>;
   __shared__ uint32_t s_col[kWarpsPerBlock][32];
   __shared__ float s_val[kWarpsPerBlock][32];

@@ -267,6 +267,7 @@ __global__ void __launch_bounds__(32 * kWarpBlock, warp_min_blocks<OP, CF>()) k_
   const uint64_t unit = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const uint64_t groups = (uint64_t(a.n_sched) + WarpGeom<LPR, CF>::RPW - 1) / WarpGeom<LPR, CF>::RPW;
   if (unit >= groups * a.n_tiles) return;  // warp-uniform exit
+  if (aborted(a)) return;
   const Policies pol = args_policies(a);
   // (group, tile) without a 64-bit division in the common cases
   uint32_t group, tile;
@@ -300,7 +301,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_cta(SpmmArgs a) {
   const uint32_t unit = blockIdx.x;
   const uint32_t sidx = unit / a.n_tiles;
   const uint32_t tile = unit % a.n_tiles;
-  if (sidx >= a.n_sched) return;
+  if (sidx >= a.n_sched || aborted(a)) return;
   const Policies pol = make_policies(a.hints);
   const uint32_t row = a.order ? a.order[sidx] : sidx;
   const uint32_t start = a.row_ptr[row];
@@ -480,6 +481,10 @@ k_hub(SpmmArgs a) {
   uint64_t* bars = reinterpret_cast<uint64_t*>(s_col + S * G);            // full[S], empty[S]
 
   __shared__ uint32_t s_unit;
+  if (aborted(a)) {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    return;
+  }
   const Policies pol = args_policies(a);
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t full0 = smem_addr(bars), empty0 = smem_addr(bars + S);

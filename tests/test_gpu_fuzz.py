@@ -150,3 +150,48 @@ def test_random_device_plans_bit_exact(m, k, density, long_row, n, op, column_ar
             if want_arg:
                 assert np.array_equal(args[i].cpu().numpy(), warg), i
     plan.close()
+
+
+@seed(20261019)
+@settings(max_examples=int(os.environ.get("FUZZ_EXAMPLES", "60")), deadline=None,
+          suppress_health_check=[HealthCheck.too_slow])
+@given(m=st.integers(2, 300), k=st.integers(2, 3000), density=st.floats(0.01, 0.2),
+       faults=st.lists(st.tuples(st.sampled_from(["oob", "dup", "swap", "big"]),
+                                 st.floats(0.0, 1.0)), min_size=1, max_size=4),
+       pack=st.sampled_from([1, -1]), data=st.integers(0, 1 << 30))
+def test_random_violations_report_the_reference_message(m, k, density, faults, pack, data):
+    """Random non-canonical inputs through the host entry (packed upload on or
+    off): the error is the reference's first-violation message, or the result
+    is correct when the corruption happened to keep the matrix canonical."""
+    if os.environ.get("FUZZ_LOG"):
+        with open(os.environ["FUZZ_LOG"], "a") as f:
+            f.write(repr(dict(viol=1, m=m, k=k, density=density, faults=faults, pack=pack,
+                              data=data)) + "\n")
+    rng = np.random.default_rng(data)
+    a = _matrix(rng, m, k, density, False)
+    if a.nnz() < 2:
+        return
+    ci = a.col_ind.copy()
+    for kind, where in faults:
+        p = min(int(where * a.nnz()), a.nnz() - 1)
+        if kind == "oob":
+            ci[p] = k + int(rng.integers(0, 100000))
+        elif kind == "big":
+            ci[p] = np.uint32(0xFFFFFFF0)
+        elif kind == "dup" and p > 0:
+            ci[p] = ci[p - 1]
+        elif kind == "swap" and p > 0:
+            ci[p - 1], ci[p] = ci[p], ci[p - 1]
+    bad = G.CsrMatrix(a.n_rows, a.n_cols, a.row_ptr, ci, a.vals)
+    b = G.make_random_dense(k, 8, data + 1)
+    n_viol, msg = O.validate(bad.n_rows, bad.n_cols, bad.row_ptr, bad.col_ind, bad.vals)
+    if n_viol == 0:
+        c = G.native_spmm(bad, b, G.KernelVariant.tuned(), G.ops.sum(),
+                          exec=G.ExecOptions(h2d_pack=pack))
+        want, _ = O.spmm(bad.n_rows, bad.n_cols, bad.row_ptr, bad.col_ind, bad.vals, b.data, "sum")
+        assert first_divergence(c.data, want) is None
+        return
+    with pytest.raises(G.Error) as ei:
+        G.native_spmm(bad, b, G.KernelVariant.tuned(), G.ops.sum(),
+                      exec=G.ExecOptions(h2d_pack=pack))
+    assert str(ei.value) == "spmm: matrix is not canonical CSR: " + msg
