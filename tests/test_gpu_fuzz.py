@@ -195,3 +195,35 @@ def test_random_violations_report_the_reference_message(m, k, density, faults, p
         G.native_spmm(bad, b, G.KernelVariant.tuned(), G.ops.sum(),
                       exec=G.ExecOptions(h2d_pack=pack))
     assert str(ei.value) == "spmm: matrix is not canonical CSR: " + msg
+
+
+@seed(20261020)
+@settings(max_examples=int(os.environ.get("FUZZ_EXAMPLES", "60")), deadline=None,
+          suppress_health_check=[HealthCheck.too_slow])
+@given(m=st.integers(0, 500), k=st.integers(1, 700), density=st.floats(0.0, 0.3),
+       long_row=st.booleans(), data=st.integers(0, 1 << 30))
+def test_random_transpose_matches_numpy_and_round_trips(m, k, density, long_row, data):
+    """gespmm_csr_transpose_device on random shapes (empty rows/columns, a
+    dense row): equal to a stable numpy transpose, canonical, and its
+    transpose is the input again."""
+    import torch
+    rng = np.random.default_rng(data)
+    a = _matrix(rng, m, k, density, long_row) if m else G.CsrMatrix(0, k, np.zeros(1, np.uint32),
+                                                                     np.zeros(0, np.uint32),
+                                                                     np.zeros(0, np.float32))
+    d = G.DeviceCsr.from_host(a, torch.device("cuda:0"))
+    t = d.transpose()
+    torch.cuda.synchronize()
+    th = t.to_host()
+    rows = np.repeat(np.arange(m, dtype=np.int64), np.diff(a.row_ptr.astype(np.int64)))
+    cols = a.col_ind.astype(np.int64)
+    order = np.lexsort((rows, cols))  # by column, then row: the canonical transpose
+    want_rp = np.concatenate([[0], np.cumsum(np.bincount(cols, minlength=k))]).astype(np.uint32)
+    assert th.n_rows == k and th.n_cols == m
+    assert np.array_equal(th.row_ptr, want_rp)
+    assert np.array_equal(th.col_ind[:a.nnz()], rows[order].astype(np.uint32))
+    assert np.array_equal(th.vals[:a.nnz()].view(np.uint32), a.vals[order].view(np.uint32))
+    back = t.transpose().to_host()
+    assert np.array_equal(back.row_ptr, a.row_ptr)
+    assert np.array_equal(back.col_ind[:a.nnz()], a.col_ind)
+    assert np.array_equal(back.vals[:a.nnz()].view(np.uint32), a.vals.view(np.uint32))
