@@ -195,6 +195,12 @@ def test_random_violations_report_the_reference_message(m, k, density, faults, p
         G.native_spmm(bad, b, G.KernelVariant.tuned(), G.ops.sum(),
                       exec=G.ExecOptions(h2d_pack=pack))
     assert str(ei.value) == "spmm: matrix is not canonical CSR: " + msg
+    # the device entry with validate=1 checks before any kernel runs
+    import torch
+    d = G.DeviceCsr.from_host(bad, torch.device("cuda:0"))
+    with pytest.raises(G.Error) as ei:
+        G.spmm(d, torch.from_numpy(b.data).cuda(), "sum", validate=True)
+    assert str(ei.value) == "spmm: matrix is not canonical CSR: " + msg
 
 
 @seed(20261020)
