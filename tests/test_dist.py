@@ -124,3 +124,25 @@ def test_two_rank_cuda_shards_equal_oracle(tmp_path, op):
     for r in range(world):
         got = np.load(tmp_path / f"cuda_rank{r}.npy")
         assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
+
+
+from hypothesis import given, seed, settings  # noqa: E402
+from hypothesis import strategies as st  # noqa: E402
+
+
+@seed(20261022)
+@settings(max_examples=200, deadline=None)
+@given(degs=st.lists(st.integers(0, 5000), min_size=0, max_size=400), parts=st.integers(1, 16))
+def test_partition_rows_properties_random(degs, parts):
+    """Every row in exactly one contiguous shard; each shard's nonzeros within
+    one max-degree row of the ideal nnz/parts split."""
+    rp = np.concatenate([[0], np.cumsum(np.asarray(degs, np.int64))]).astype(np.uint32)
+    b = D.partition_rows(rp, parts)
+    m = len(degs)
+    assert len(b) == parts + 1 and b[0] == 0 and b[-1] == m
+    assert all(b[i] <= b[i + 1] for i in range(parts))
+    nnz = int(rp[-1])
+    maxd = max(degs) if degs else 0
+    loads = np.diff(rp.astype(np.int64)[b])
+    assert loads.sum() == nnz
+    assert np.all(loads <= nnz / parts + maxd + 1)
