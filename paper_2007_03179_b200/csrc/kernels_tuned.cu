@@ -66,8 +66,14 @@ template <int OP, int CF>
 #ifndef GESPMM_CF4_BLOCKS
 #define GESPMM_CF4_BLOCKS 6
 #endif
+// CF=1 sum/mean (the Reddit N=128 shape): 8 CTAs per SM fit 64 registers
+// without spills: 32 warps/SM, best step 2.80 vs 2.84 ms at 7 CTAs
+#ifndef GESPMM_CF1_BLOCKS
+#define GESPMM_CF1_BLOCKS 8
+#endif
 constexpr int warp_min_blocks() {
-  return Reduce<OP>::kHasArg ? (CF >= 4 ? 4 : 6) : (CF >= 4 ? GESPMM_CF4_BLOCKS : 7);
+  return Reduce<OP>::kHasArg ? (CF >= 4 ? 4 : 6)
+                             : (CF >= 4 ? GESPMM_CF4_BLOCKS : (CF == 1 ? GESPMM_CF1_BLOCKS : 7));
 }
 
 template <int LPR, int CF>
