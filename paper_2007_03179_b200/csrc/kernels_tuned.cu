@@ -71,9 +71,16 @@ template <int OP, int CF>
 #ifndef GESPMM_CF1_BLOCKS
 #define GESPMM_CF1_BLOCKS 8
 #endif
+#ifndef GESPMM_CF2_BLOCKS
+#define GESPMM_CF2_BLOCKS 7
+#endif
+#ifndef GESPMM_ARG_BLOCKS
+#define GESPMM_ARG_BLOCKS 6
+#endif
 constexpr int warp_min_blocks() {
-  return Reduce<OP>::kHasArg ? (CF >= 4 ? 4 : 6)
-                             : (CF >= 4 ? GESPMM_CF4_BLOCKS : (CF == 1 ? GESPMM_CF1_BLOCKS : 7));
+  return Reduce<OP>::kHasArg ? (CF >= 4 ? 4 : GESPMM_ARG_BLOCKS)
+                             : (CF >= 4 ? GESPMM_CF4_BLOCKS
+                                        : (CF == 1 ? GESPMM_CF1_BLOCKS : GESPMM_CF2_BLOCKS));
 }
 
 template <int LPR, int CF>
