@@ -1070,14 +1070,17 @@ gespmm_status_t gespmm_spmm_host(const gespmm_csr_t* a, const float* b, uint32_t
     d_exc = static_cast<uint32_t*>(ws->buf[9]);
     scan_tmp = ws->buf[10];
   }
+  ColCheck cc_view;
   ColCheck* cc = nullptr;
   if ((o.validate || pack) && nnz) {
     GESPMM_CUDA(ws->reserve(7, colcheck_workspace_bytes(nnz)), "spmm");
     bits = reinterpret_cast<uint32_t*>(static_cast<char*>(ws->buf[7]) + 256);
-    if (o.validate)
-      GESPMM_CUDA(colcheck_begin(&cc, nnz, ws->buf[7], ws->stream), "spmm");
-    else
+    if (o.validate) {
+      cc = &cc_view;
+      GESPMM_CUDA(colcheck_begin(cc, nnz, ws->buf[7], ws->stream), "spmm");
+    } else {
       GESPMM_CUDA(cudaMemsetAsync(bits, 0, sizeof(uint32_t) * (nnz / 32 + 1), ws->stream), "spmm");
+    }
   }
   uint64_t exc_off = 0;  // exception pairs used so far
 

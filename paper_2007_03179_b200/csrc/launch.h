@@ -125,11 +125,14 @@ cudaError_t validate_csr_device(uint32_t m, uint32_t k, uint64_t nnz, const uint
 
 // Chunked column check: begin, one call per row block (row_ptr_chunk points at
 // the block's first row_ptr entry; positions stay global), end (locates the
-// first violation's row, synchronises `st`, frees).
-struct ColCheck;
+// first violation's row, synchronises `st`).
+struct ColCheck {  // views into the caller's workspace (no ownership)
+  void* scratch = nullptr;   // first-violation minima (validate.cu)
+  uint32_t* bits = nullptr;  // row-start bitmap over all nnz positions
+};
 unsigned long long* colcheck_key(ColCheck* c);  // its first-violation key (device)
 size_t colcheck_workspace_bytes(uint64_t nnz);
-cudaError_t colcheck_begin(ColCheck** out, uint64_t nnz, void* ws, cudaStream_t st);
+cudaError_t colcheck_begin(ColCheck* out, uint64_t nnz, void* ws, cudaStream_t st);
 // rows [0, m_chunk) of row_ptr_chunk own positions [ps, pe)
 cudaError_t colcheck_rows(ColCheck* c, const uint32_t* row_ptr_chunk, uint32_t m_chunk,
                           uint64_t ps, uint64_t pe, const uint32_t* col_ind, uint32_t k,

@@ -141,11 +141,6 @@ cudaError_t validate_csr_device(uint32_t m, uint32_t k, uint64_t nnz, const uint
 
 // ---- chunked column check (the host pipeline validates row blocks as their
 // col_ind arrives; row_ptr itself is checked on the host) --------------------
-struct ColCheck {
-  Scratch* s = nullptr;
-  uint32_t* bits = nullptr;  // row-start bitmap over all nnz positions
-};
-
 size_t colcheck_workspace_bytes(uint64_t nnz) {
   return 256 + sizeof(uint32_t) * (nnz / 32 + 1);
 }
@@ -153,26 +148,23 @@ size_t colcheck_workspace_bytes(uint64_t nnz) {
 // `ws` (colcheck_workspace_bytes(nnz), caller-owned device memory, 256-byte
 // aligned) holds the scratch minima and the bitmap: no allocation per call
 // (stream-ordered allocations released at every sync made host calls stall).
-cudaError_t colcheck_begin(ColCheck** out, uint64_t nnz, void* ws, cudaStream_t st) {
-  auto* c = new ColCheck();
-  c->s = static_cast<Scratch*>(ws);
+cudaError_t colcheck_begin(ColCheck* c, uint64_t nnz, void* ws, cudaStream_t st) {
+  c->scratch = ws;
   c->bits = reinterpret_cast<uint32_t*>(static_cast<char*>(ws) + 256);
   cudaError_t e = cudaMemsetAsync(c->bits, 0, sizeof(uint32_t) * (nnz / 32 + 1), st);
-  if (e == cudaSuccess) e = cudaMemsetAsync(c->s, 0xff, sizeof(Scratch), st);  // minima start at ~0
-  if (e != cudaSuccess) {
-    delete c;
-    return e;
-  }
-  *out = c;
-  return cudaSuccess;
+  if (e == cudaSuccess) e = cudaMemsetAsync(ws, 0xff, sizeof(Scratch), st);  // minima start at ~0
+  return e;
 }
 
-unsigned long long* colcheck_key(ColCheck* c) { return &c->s->first_bad_key; }
+unsigned long long* colcheck_key(ColCheck* c) {
+  return &static_cast<Scratch*>(c->scratch)->first_bad_key;
+}
 
 cudaError_t colcheck_rows(ColCheck* c, const uint32_t* row_ptr_chunk, uint32_t m_chunk,
                           uint64_t ps, uint64_t pe, const uint32_t* col_ind, uint32_t k,
                           uint64_t usable, cudaStream_t st) {
-  return launch_colcheck(row_ptr_chunk, m_chunk, col_ind, k, ps, pe, usable, c->bits, c->s, st);
+  return launch_colcheck(row_ptr_chunk, m_chunk, col_ind, k, ps, pe, usable, c->bits,
+                         static_cast<Scratch*>(c->scratch), st);
 }
 
 cudaError_t colcheck_end(ColCheck* c, const uint32_t* row_ptr, const uint32_t* col_ind, uint32_t m,
@@ -181,13 +173,13 @@ cudaError_t colcheck_end(ColCheck* c, const uint32_t* row_ptr, const uint32_t* c
   Scratch host{};
   cudaError_t e = cudaSuccess;
   if (m > 0) {
-    k_locate<<<1, 32, 0, st>>>(row_ptr, col_ind, m, c->s);
+    k_locate<<<1, 32, 0, st>>>(row_ptr, col_ind, m, static_cast<Scratch*>(c->scratch));
     note_launch();
     e = cudaGetLastError();
   }
-  if (e == cudaSuccess) e = cudaMemcpyAsync(&host, c->s, sizeof(host), cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(&host, c->scratch, sizeof(host), cudaMemcpyDeviceToHost, st);
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);
-  delete c;
   *first_bad_key = e == cudaSuccess ? host.first_bad_key : ~0ull;
   *bad_row = host.bad_row;
   *bad_col = host.bad_col;
