@@ -50,11 +50,12 @@ def main():
     base = None
     for g in [int(x) for x in args.shards.split(",")]:
         bounds = D.partition_rows(a.row_ptr, g)
-        times, descs = [], []
+        times, descs, alg = [], [], 0
         for r in range(g):
             if args.only_shard is not None and r != args.only_shard:
                 continue
             sh = D.shard_csr(a, bounds[r], bounds[r + 1]) if g > 1 else a
+            alg += bench.algorithmic_bytes(sh, n, want_arg)[0]
             d = G.DeviceCsr.from_host(sh, dev)
             c = torch.empty((sh.n_rows, n), dtype=torch.float32, device=dev)
             arg = torch.empty((sh.n_rows, n), dtype=torch.int32, device=dev) if want_arg else None
@@ -78,8 +79,11 @@ def main():
         if g == 1:
             base = gf
         eff = gf / (g * base) if base else None
+        peak, _ = bench.hbm_peak()
+        hbm = alg / (step * 1e-3) / 1e9  # minimum-traffic bytes of all shards / step
         run = {"gpus": g, "shard_ms": [round(t, 4) for t in times], "step_ms": round(step, 4),
                "gflops": round(gf, 1), "efficiency_vs_1gpu": round(eff, 3) if eff else None,
+               "hbm_gbs": round(hbm, 1), "roofline_frac": round(hbm / (g * peak), 4),
                "plan_shard0": descs[0]}
         out["runs"].append(run)
         print(json.dumps(run), flush=True)
