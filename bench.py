@@ -575,6 +575,8 @@ def run_gcn(args):
     cfg = CONFIGS["reddit"]
     a = gcn.normalize_adjacency(make_inputs(cfg))  # D^-1/2 (A + I) D^-1/2
     gcfg = gcn.GCNConfig(in_features=602, hidden=256, classes=41)
+    if args.gcn_pad > 0:
+        gcfg.pad_to = args.gcn_pad
     adj, info = gcn.build_adjacency(a, dev, rank, world, G.ExecOptions(exact=not args.fast))
     h, y = gcn.synthetic_features(a.n_rows, gcfg.in_features, gcfg.classes)
     ht = torch.from_numpy(h[info.lo:info.hi]).to(dev)
@@ -646,6 +648,8 @@ def main():
     p.add_argument("--l2-hot-mb", type=int, default=0,
                    help="hot-column map budget in MB (0 auto, <0 off)")
     p.add_argument("--no-flush", action="store_true", help="skip the L2 flush between steps")
+    p.add_argument("--gcn-pad", type=int, default=0,
+                   help="GCN: pad the class width to a multiple of this (default GCNConfig.pad_to)")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--no-ceiling", action="store_true", help="skip the live gather-ceiling probe")

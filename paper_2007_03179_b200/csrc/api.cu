@@ -200,7 +200,11 @@ uint32_t auto_hub_threshold(uint32_t n, uint64_t nnz, int cf, uint32_t k, int de
   cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev);
   const double b_bytes = double(k) * double(n) * 4.0;
   const double rate = (l2 > 0 && b_bytes > 1.5 * double(l2)) ? 9.5e12 : 19e12;
-  const double t_launch = double(nnz) * 4.0 * double(moved) / rate;
+  // narrow tiles are not byte-bound: below ~90 columns the warp kernel runs at
+  // ~18 ps per nonzero whatever the width (Reddit shape, 115M nonzeros: N=24/32
+  // 1.8 ms, N=44/48/64 2.1-2.3 ms; tools/gcn_width_probe.py).  Without this
+  // floor N=32 got ~2600 hub rows and took 3.1 ms instead of 1.7 ms.
+  const double t_launch = std::max(double(nnz) * 4.0 * double(moved) / rate, double(nnz) * 18e-12);
   const double t_nnz = 0.7e-6 * double(cf < 1 ? 1 : cf) / 8.0;
   // no hub rows while the longest row's warp time stays well inside the launch
   // (whole Reddit: 0.61 of it; products half-shard: 0.47): a side-stream hub
