@@ -653,3 +653,42 @@ def test_reddit_scale_host_entry_and_shards_equal_device_plan(cuda):
         assert first_divergence(c.cpu().numpy(), want[bounds[r]:bounds[r + 1]]) is None, r
         plan.close()
     assert hubs > 0  # the shards really went through the hub kernel
+
+
+@pytest.mark.slow
+def test_reddit_scale_hub_threshold_by_width(cuda):
+    """The auto hub threshold on the whole Reddit shape: no hub rows at N=128
+    (the longest row fits inside the byte-bound launch) and only the very
+    longest rows at narrow widths, whose launch is bound per nonzero rather
+    than per byte (N=32 took 3.1 ms with ~2600 hub rows, 1.44 ms with the
+    per-nonzero floor; profiles/r1_narrow_widths_*.txt).  A sampled row check
+    keeps the narrow hub path honest."""
+    import torch
+    a = G.gen_powerlaw(232965, 114_800_000, 21657, 1.0, 1)
+    G.randomize_values(a, 2)
+    d = G.DeviceCsr.from_host(a, cuda)
+
+    def hub_rows(desc):
+        return int(desc.split("hub_rows=")[1].split(" ")[0])
+
+    p128 = G.Plan(d, 128, "sum")
+    assert hub_rows(p128.description) == 0
+    p128.close()
+    b = G.make_random_dense(a.n_cols, 32, 42)
+    bt = torch.from_numpy(b.data).to(cuda)
+    p32 = G.Plan(d, 32, "sum")
+    h = hub_rows(p32.description)
+    assert 0 < h < 1000, p32.description
+    c = torch.empty((a.n_rows, 32), device=cuda)
+    p32.execute(bt, c)
+    torch.cuda.synchronize()
+    got = c.cpu().numpy()
+    p32.close()
+    deg = np.diff(a.row_ptr.astype(np.int64))
+    rows = np.concatenate([np.argsort(-deg)[:8], np.random.default_rng(5).integers(0, a.n_rows, 24)])
+    for r in rows:
+        lo, hi = int(a.row_ptr[r]), int(a.row_ptr[r + 1])
+        want = np.zeros(32, np.float32)
+        for p in range(lo, hi):  # ordered fold v*b then add, as the reference
+            want = (want + np.float32(a.vals[p]) * b.data[a.col_ind[p]]).astype(np.float32)
+        assert np.array_equal(got[r], want), int(r)
