@@ -89,18 +89,23 @@ template <int LPR, int CF>
 #endif
 struct WarpGeom {
   static constexpr int RPW = 32 / LPR;                     // rows per warp
+  // staged entries per lane per chunk: 4-lane rows (N = 16) stage 8 entries
+  // per row per chunk, not 4, so a chunk's col/val round trip is hidden behind
+  // 8 gathers in flight (Reddit shape N=16: 2.65 ms at 4 per chunk)
+  static constexpr int E = LPR == 4 ? 2 : 1;
+  static constexpr int CH = LPR * E;                       // entries per row per chunk
   static constexpr int U0 = (LPR == 16 ? GESPMM_U_NARROW : 8) / CF;
-  static constexpr int U = U0 < LPR ? U0 : LPR;            // gather batch; LPR % U == 0
+  static constexpr int U = U0 < CH ? U0 : CH;              // gather batch; CH % U == 0
   static constexpr int W = U < 4 ? U : 4;                  // LDS width (entries per read)
-  static_assert(LPR % U == 0 && U % W == 0, "batch geometry");
+  static_assert(CH % U == 0 && U % W == 0, "batch geometry");
 };
 
 // Row metadata of one (sub)warp unit for this lane: the row, its CSR range,
 // and this lane's entry of the row's first staged chunk.
 struct UnitMeta {
   uint32_t row, start, full_end;
-  uint32_t k0;
-  float v0;
+  uint32_t k0[2];  // this lane's chunk-0 entries (WarpGeom::E of them)
+  float v0[2];
   bool row_ok;
 };
 
@@ -118,16 +123,20 @@ __device__ __forceinline__ void unit_rows(const SpmmArgs& a, uint32_t group, Uni
 
 // Issues this lane's chunk-0 (col, val) loads; slots past the row end hold
 // column 0 (a valid row).
-template <int LPR, bool HOT>
+template <int LPR, int E, bool HOT>
 __device__ __forceinline__ void unit_chunk0(const SpmmArgs& a, const Policies& pol, UnitMeta& m) {
   const uint32_t sl = (threadIdx.x & 31) % LPR;
   const uint32_t len = faulted_end(m.start, m.full_end, a.skip_tail) - m.start;
-  m.k0 = 0;
-  m.v0 = 0.0f;
-  if (sl < len) {
-    m.k0 = ld_stream_u32(a.col_ind + m.start + sl, pol.stream);
-    m.v0 = ld_stream_f32(a.vals + m.start + sl, pol.stream);
-    if (HOT) m.k0 |= cold_mark(a.hot, m.k0);
+#pragma unroll
+  for (int j = 0; j < E; ++j) {
+    const uint32_t i = uint32_t(j * LPR) + sl;
+    m.k0[j] = 0;
+    m.v0[j] = 0.0f;
+    if (i < len) {
+      m.k0[j] = ld_stream_u32(a.col_ind + m.start + i, pol.stream);
+      m.v0[j] = ld_stream_f32(a.vals + m.start + i, pol.stream);
+      if (HOT) m.k0[j] |= cold_mark(a.hot, m.k0[j]);
+    }
   }
 }
 
@@ -142,7 +151,8 @@ __device__ __forceinline__ void warp_unit(const SpmmArgs& a, const Policies& pol
                                           const UnitMeta& m, uint32_t* my_col, float* my_val) {
   using R = Reduce<OP>;
   using G = WarpGeom<LPR, CF>;
-  constexpr int RPW = G::RPW, U = G::U, W = G::W;
+  constexpr int RPW = G::RPW, U = G::U, W = G::W, E = G::E, CH = G::CH;
+  constexpr uint32_t TILE = 32u * E;                // staged entries per buffer
   constexpr uint32_t SUB = uint32_t(VEC * LPR);     // columns per sub-tile
   constexpr uint32_t TW = SUB * CF;                 // columns per tile
   const uint32_t lane = threadIdx.x & 31;
@@ -177,23 +187,32 @@ __device__ __forceinline__ void warp_unit(const SpmmArgs& a, const Policies& pol
   const float* vs = a.vals + start;
 
   __syncwarp();  // the previous unit's reads of the tile are done
-  my_col[lane] = m.k0;  // phase 1 of chunk 0
-  my_val[lane] = m.v0;
+  const uint32_t slot = sub * uint32_t(CH) + sl;  // this lane's first entry in a buffer
+#pragma unroll
+  for (int j = 0; j < E; ++j) {  // phase 1 of chunk 0
+    my_col[slot + j * LPR] = m.k0[j];
+    my_val[slot + j * LPR] = m.v0[j];
+  }
   uint32_t buf = 0;
-  for (uint32_t off = 0; off < maxlen; off += LPR) {
+  for (uint32_t off = 0; off < maxlen; off += CH) {
     // issue the next chunk's sparse loads before consuming this one
-    uint32_t kn = 0;
-    float vn = 0.0f;
-    const uint32_t nxt = off + LPR + sl;
-    if (nxt < len) {
-      kn = ld_stream_u32(ci + nxt, pol.stream);
-      vn = ld_stream_f32(vs + nxt, pol.stream);
-      if (HOT) kn |= cold_mark(a.hot, kn);
+    uint32_t kn[E];
+    float vn[E];
+#pragma unroll
+    for (int j = 0; j < E; ++j) {
+      kn[j] = 0;
+      vn[j] = 0.0f;
+      const uint32_t nxt = off + CH + uint32_t(j * LPR) + sl;
+      if (nxt < len) {
+        kn[j] = ld_stream_u32(ci + nxt, pol.stream);
+        vn[j] = ld_stream_f32(vs + nxt, pol.stream);
+        if (HOT) kn[j] |= cold_mark(a.hot, kn[j]);
+      }
     }
     __syncwarp();
-    const uint32_t* cs = my_col + buf * 32 + sub * LPR;
-    const float* vsm = my_val + buf * 32 + sub * LPR;
-    const uint32_t chunk = min(uint32_t(LPR), maxlen - off);
+    const uint32_t* cs = my_col + buf * TILE + sub * CH;
+    const float* vsm = my_val + buf * TILE + sub * CH;
+    const uint32_t chunk = min(uint32_t(CH), maxlen - off);
     for (uint32_t kk = 0; kk < chunk; kk += U) {
       uint32_t k[U];
       float v[U];
@@ -251,8 +270,11 @@ __device__ __forceinline__ void warp_unit(const SpmmArgs& a, const Policies& pol
       }
     }
     buf ^= 1u;
-    my_col[buf * 32 + lane] = kn;  // phase 1 of the next chunk (buffer last read before
-    my_val[buf * 32 + lane] = vn;  // this iteration's __syncwarp)
+#pragma unroll
+    for (int j = 0; j < E; ++j) {  // phase 1 of the next chunk (buffer last read
+      my_col[buf * TILE + slot + j * LPR] = kn[j];  // before this iteration's __syncwarp)
+      my_val[buf * TILE + slot + j * LPR] = vn[j];
+    }
   }
 
   const uint32_t row_len = full_end - start;
@@ -271,11 +293,11 @@ __device__ __forceinline__ void warp_unit(const SpmmArgs& a, const Policies& pol
 
 template <int OP, bool FAST, int VEC, int LPR, int CF, bool HOT>
 __global__ void __launch_bounds__(32 * kWarpBlock, warp_min_blocks<OP, CF>()) k_warp(SpmmArgs a) {
-  // Staged sparse tile, double-buffered per warp: phase 1 writes one (col, val)
+  // Staged sparse tile, double-buffered per warp: phase 1 writes E (col, val)
   // per lane, phase 2 reads them back with broadcast LDS of W entries — 2/W
   // shared-pipe wavefronts per nonzero instead of two shuffles.
-  __shared__ __align__(16) uint32_t s_col[kWarpBlock][2][32];
-  __shared__ __align__(16) float s_val[kWarpBlock][2][32];
+  __shared__ __align__(16) uint32_t s_col[kWarpBlock][2][32 * WarpGeom<LPR, CF>::E];
+  __shared__ __align__(16) float s_val[kWarpBlock][2][32 * WarpGeom<LPR, CF>::E];
   const uint32_t wib = threadIdx.x >> 5;
   const uint64_t unit = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const uint64_t groups = (uint64_t(a.n_sched) + WarpGeom<LPR, CF>::RPW - 1) / WarpGeom<LPR, CF>::RPW;
@@ -296,7 +318,7 @@ __global__ void __launch_bounds__(32 * kWarpBlock, warp_min_blocks<OP, CF>()) k_
   }
   UnitMeta m;
   unit_rows<LPR>(a, group, m);
-  unit_chunk0<LPR, HOT>(a, pol, m);
+  unit_chunk0<LPR, WarpGeom<LPR, CF>::E, HOT>(a, pol, m);
   warp_unit<OP, FAST, VEC, LPR, CF, HOT>(a, pol, tile, m, &s_col[wib][0][0], &s_val[wib][0][0]);
 }
 
