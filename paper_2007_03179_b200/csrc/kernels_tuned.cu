@@ -87,25 +87,30 @@ template <int LPR, int CF>
 #ifndef GESPMM_U_NARROW
 #define GESPMM_U_NARROW 8
 #endif
+#ifndef GESPMM_STAGE_MIN
+#define GESPMM_STAGE_MIN 8  // staged entries per row per chunk, at least
+#endif
 struct WarpGeom {
   static constexpr int RPW = 32 / LPR;                     // rows per warp
   // staged entries per lane per chunk: 4-lane rows (N = 16) stage 8 entries
   // per row per chunk, not 4, so a chunk's col/val round trip is hidden behind
   // 8 gathers in flight (Reddit shape N=16: 2.65 ms at 4 per chunk)
-  static constexpr int E = LPR == 4 ? 2 : 1;
+  // (scalar 1- and 2-lane rows, N < 4, keep one entry per lane)
+  static constexpr int E = (LPR >= GESPMM_STAGE_MIN || LPR < 4) ? 1 : GESPMM_STAGE_MIN / LPR;
   static constexpr int CH = LPR * E;                       // entries per row per chunk
   static constexpr int U0 = (LPR == 16 ? GESPMM_U_NARROW : 8) / CF;
   static constexpr int U = U0 < CH ? U0 : CH;              // gather batch; CH % U == 0
   static constexpr int W = U < 4 ? U : 4;                  // LDS width (entries per read)
-  static_assert(CH % U == 0 && U % W == 0, "batch geometry");
+  static_assert(CH % U == 0 && U % W == 0 && E <= (GESPMM_STAGE_MIN / 4 > 1 ? GESPMM_STAGE_MIN / 4 : 1),
+                "batch geometry");
 };
 
 // Row metadata of one (sub)warp unit for this lane: the row, its CSR range,
 // and this lane's entry of the row's first staged chunk.
 struct UnitMeta {
   uint32_t row, start, full_end;
-  uint32_t k0[2];  // this lane's chunk-0 entries (WarpGeom::E of them)
-  float v0[2];
+  uint32_t k0[GESPMM_STAGE_MIN / 4 > 1 ? GESPMM_STAGE_MIN / 4 : 1];  // this lane's chunk-0
+  float v0[GESPMM_STAGE_MIN / 4 > 1 ? GESPMM_STAGE_MIN / 4 : 1];     // entries (WarpGeom::E)
   bool row_ok;
 };
 
