@@ -131,8 +131,10 @@ def test_hub_rows_row_per_cta(n, op, cuda):
 
 
 def test_row_length_boundaries(cuda):
-    """Rows of length 0, 1, 31, 32, 33, 255, 256, 257, 513 and one of 20000."""
-    lens = [0, 1, 31, 32, 33, 255, 256, 257, 513, 20000, 0, 7]
+    """Rows of length 0, 1, 7-9, 15-17, 31-33, 255-257, 513 and one of 20000
+    (chunk edges of every staged-tile geometry: 8 entries per row at 4 and 8
+    lanes, 16 and 32 above); N=12/16 run the 4-lane rows."""
+    lens = [0, 1, 31, 32, 33, 255, 256, 257, 513, 20000, 0, 7, 8, 9, 15, 16, 17]
     k = 25000
     rng = np.random.default_rng(5)
     rp = np.zeros(len(lens) + 1, np.uint32)
@@ -142,7 +144,7 @@ def test_row_length_boundaries(cuda):
         rp[i + 1] = rp[i] + L
     a = G.CsrMatrix(len(lens), k, rp, np.concatenate(cols), np.zeros(int(rp[-1]), np.float32))
     G.randomize_values(a, 9)
-    for n in (16, 128, 256):
+    for n in (12, 16, 44, 128, 256):
         b = G.make_random_dense(k, n, 3)
         for ht in (0, 30, -1):
             for op in OPS:
