@@ -333,7 +333,8 @@ gespmm_status_t launch_tuned_rows(const TunedShapes& t, int op, bool fast, const
         const char* e = std::getenv("GESPMM_HUB_KCTA");
         return e && e[0] == '1';
       }();
-      const bool tma = !force_cta && w % 4 == 0 && a.ld % 4 == 0 && aligned(sa.b, 16) &&
+      const bool tma = !force_cta && w % 4 == 0 && a.ld % 4 == 0 && a.ldb % 4 == 0 &&
+                       aligned(sa.b, 16) &&
                        aligned(sa.c, 16) && (!sa.arg || aligned(sa.arg, 16));
       const uint32_t tw = tma ? hub_tile_width(w, n_hub) : uint32_t(cs.vec * cs.warps * 32);
       h.n_tiles = (w + tw - 1) / tw;
@@ -569,12 +570,12 @@ gespmm_status_t plan_execute_impl(Plan& p, const float* b, float* c, int32_t* ar
   if (p.o.variant != GESPMM_VARIANT_TUNED) {
     args.order = nullptr;
     args.n_sched = p.a.n_rows;
-    args.ld = p.n;
+    args.ld = args.ldb = p.n;
     args.n_tiles = faithful_tiles(p.o.variant, p.o.cf, p.n);
     GESPMM_CUDA(launch_faithful(p.o.variant, p.o.cf, p.op, fast, args, st), "spmm");
     return GESPMM_OK;
   }
-  args.ld = p.n;
+  args.ld = args.ldb = p.n;
   if (p.ch.col_ind && aligned(b, 16) && aligned(c, 16) && (!arg || aligned(arg, 16))) {
     args.order = p.d_order;
     args.n_sched = p.a.n_rows;
@@ -588,7 +589,7 @@ gespmm_status_t plan_execute_impl(Plan& p, const float* b, float* c, int32_t* ar
   const cudaAccessPolicyWindow* winp = nullptr;
   if (p.o.l2_persist == 2) persist_limits(p.device);  // set-aside only, no window
   if (p.o.l2_persist == 1) {
-    const size_t b_bytes = size_t(p.a.n_cols) * p.n * sizeof(float);
+    const size_t b_bytes = size_t(p.a.n_cols) * args.ldb * sizeof(float);
     const PersistLimits lim = persist_limits(p.device);
     if (lim.max_window > 0 && lim.set_aside > 0 && b_bytes > 0) {
       win.base_ptr = const_cast<float*>(b);
@@ -1138,7 +1139,7 @@ gespmm_status_t gespmm_spmm_host(const gespmm_csr_t* a, const float* b, uint32_t
     args.c = d_c + uint64_t(lo) * n;
     args.arg = d_arg ? d_arg + uint64_t(lo) * n : nullptr;
     args.n = n;
-    args.ld = n;
+    args.ld = args.ldb = n;
     args.arg_col = o.arg_kind == GESPMM_ARG_COLUMN;
     args.skip_tail = o.fault_skip_tail;
     args.hints = o.l2_hints;

@@ -77,7 +77,7 @@ __global__ void __launch_bounds__(kClWarps * 32, 1) k_warp_cluster(SpmmArgs a, C
     const uint32_t j = i >> 5, s = j * CS + rank;
     if (s < c.n_hot) {
       const uint32_t col = c.hot_list[s];
-      hot[i] = *reinterpret_cast<const float4*>(a.b + uint64_t(col) * a.ld + (i & 31u) * 4u);
+      hot[i] = *reinterpret_cast<const float4*>(a.b + uint64_t(col) * a.ldb + (i & 31u) * 4u);
     }
   }
   cluster_sync_all();  // every CTA's slice is in place before any DSMEM read
@@ -86,7 +86,7 @@ __global__ void __launch_bounds__(kClWarps * 32, 1) k_warp_cluster(SpmmArgs a, C
   uint32_t* my_col = s_col + wib * 64;
   float* my_val = s_val + wib * 64;
   const char* bl = reinterpret_cast<const char*>(a.b + lane * 4u);
-  const uint32_t stride = a.ld * 4u;
+  const uint32_t stride = a.ldb * 4u;
   for (;;) {
     uint32_t unit = 0;
     if (lane == 0) unit = atomicAdd(c.counter, 1u);

@@ -314,7 +314,8 @@ struct SpmmArgs {
   const uint32_t* order;  // row schedule (nullable -> identity)
   uint32_t n_sched;       // rows in the schedule
   uint32_t n;             // dense width N (of this launch's column slice)
-  uint32_t ld;            // row stride of B, C and arg in elements (>= n)
+  uint32_t ld;            // row stride of C and arg in elements (>= n)
+  uint32_t ldb;           // row stride of B in elements (>= n): ld, or the plan's re-pitched copy
   uint32_t n_tiles;       // column tiles per row
   int arg_col;            // arg = col_ind[p] instead of p
   int skip_tail;

@@ -187,7 +187,7 @@ __device__ __forceinline__ void warp_unit(const SpmmArgs& a, const Policies& pol
 #pragma unroll
   for (int c = 0; c < CF; ++c) all_cols = all_cols && colok[c];
   all_cols = __all_sync(kFull, all_cols);
-  const uint32_t stride = a.ld * 4u;  // bytes per B row (B < 4 GiB per row index * stride)
+  const uint32_t stride = a.ldb * 4u;  // bytes per B row (B < 4 GiB per row index * stride)
   const uint32_t* ci = a.col_ind + start;
   const float* vs = a.vals + start;
 
@@ -396,7 +396,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_cta(SpmmArgs a) {
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const uint32_t k = (kk + u < n_cur) ? kv[u].x : kv[0].x;
-        bv[u] = ld_keep<VEC>(bsafe + uint64_t(k) * a.ld, pol.keep);
+        bv[u] = ld_keep<VEC>(bsafe + uint64_t(k) * a.ldb, pol.keep);
       }
 #pragma unroll
       for (int u = 0; u < U; ++u) {
@@ -575,7 +575,7 @@ k_hub(SpmmArgs a) {
       const uint32_t* ci = a.col_ind + start;
       const float* vs = a.vals + start;
       const char* bsrc = reinterpret_cast<const char*>(a.b + col0);
-      const uint64_t stride = uint64_t(a.ld) * 4u;
+      const uint64_t stride = uint64_t(a.ldb) * 4u;
       uint32_t q = pw;
       uint32_t kn = 0;
       if (q < groups && q * G + lane < len && lane < uint32_t(G))
