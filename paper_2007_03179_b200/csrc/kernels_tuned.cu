@@ -59,7 +59,7 @@ constexpr int kWarpBlock = 4;  // warps per CTA: 72-register kernel -> 7 CTAs = 
 
 // max/min carry 2*CF*VEC accumulator registers (value + arg): 6 CTAs per SM
 // (85 registers; 4 at CF=4) instead of spilling under the 7-CTA cap.
-template <int OP, int CF>
+template <int OP, int CF, int LPR = 32>
 // CF=4 sum/mean shapes (low-degree rows, e.g. Pubmed): 6 CTAs per SM; 7 or 8
 // (<= 64 registers, spills) measured no faster on Pubmed N=128 (14.4 vs
 // 14.4/15.2/16.4 us median)
@@ -78,6 +78,9 @@ template <int OP, int CF>
 #define GESPMM_ARG_BLOCKS 6
 #endif
 constexpr int warp_min_blocks() {
+#ifdef GESPMM_NARROW_BLOCKS
+  if (LPR <= 16 && CF == 1 && !Reduce<OP>::kHasArg) return GESPMM_NARROW_BLOCKS;
+#endif
   return Reduce<OP>::kHasArg ? (CF >= 4 ? 4 : GESPMM_ARG_BLOCKS)
                              : (CF >= 4 ? GESPMM_CF4_BLOCKS
                                         : (CF == 1 ? GESPMM_CF1_BLOCKS : GESPMM_CF2_BLOCKS));
@@ -297,7 +300,7 @@ __device__ __forceinline__ void warp_unit(const SpmmArgs& a, const Policies& pol
 }
 
 template <int OP, bool FAST, int VEC, int LPR, int CF, bool HOT>
-__global__ void __launch_bounds__(32 * kWarpBlock, warp_min_blocks<OP, CF>()) k_warp(SpmmArgs a) {
+__global__ void __launch_bounds__(32 * kWarpBlock, warp_min_blocks<OP, CF, LPR>()) k_warp(SpmmArgs a) {
   // Staged sparse tile, double-buffered per warp: phase 1 writes E (col, val)
   // per lane, phase 2 reads them back with broadcast LDS of W entries — 2/W
   // shared-pipe wavefronts per nonzero instead of two shuffles.
