@@ -1,9 +1,10 @@
 // Tuned B200 SpMM-like kernels (the product path).
 //
 // k_warp — row per (sub)warp.  Coalesced Row Caching: the LPR lanes that own a
-//   row load the next LPR (col, val) pairs of the row with one coalesced load
-//   each (prefetched one chunk ahead) into a per-warp shared tile and read them
-//   back with broadcast LDS.128, so col_ind/vals are read once per row tile.  Lanes own VEC contiguous columns
+//   row load the next LPR*E (col, val) pairs of the row with E coalesced loads
+//   each (E = 2 for 4-lane rows, else 1; prefetched one chunk ahead) into a
+//   per-warp shared tile and read them back with broadcast LDS.128, so
+//   col_ind/vals are read once per row tile.  Lanes own VEC contiguous columns
 //   and gather B rows with 16-byte (float4) loads.  Coarse-grained Warp
 //   Merging: each lane owns CF column sub-tiles, so one staged nonzero feeds
 //   CF vector gathers.  U nonzeros are gathered before any is folded (memory-
@@ -55,7 +56,7 @@ struct Pack<4> {
   using F = float4;
 };
 
-constexpr int kWarpBlock = 4;  // warps per CTA: 72-register kernel -> 7 CTAs = 28 warps/SM
+constexpr int kWarpBlock = 4;  // warps per CTA (CF=1 sum: 64 registers, 8 CTAs = 32 warps/SM)
 
 // max/min carry 2*CF*VEC accumulator registers (value + arg): 6 CTAs per SM
 // (85 registers; 4 at CF=4) instead of spilling under the 7-CTA cap.
