@@ -174,13 +174,20 @@ __device__ __forceinline__ void warp_unit(const SpmmArgs& a, const Policies& pol
 
   const uint32_t col0 = tile * TW + sl * uint32_t(VEC);
   bool colok[CF];
-  const char* bbase[CF];  // byte base of the lane's sub-tile; masked ones read column 0
+  const char* bbase[CF];  // byte base of the lane's sub-tile (masked lanes: see below)
   float acc[CF][VEC];
   int32_t who[CF][VEC];
 #pragma unroll
   for (int c = 0; c < CF; ++c) {
     colok[c] = row_ok && (col0 + c * SUB) < a.n;
+#ifdef GESPMM_AB_MASK0
     bbase[c] = reinterpret_cast<const char*>(a.b + (colok[c] ? col0 + c * SUB : 0u));
+#else
+    // lanes past N re-read the row's last vector: it lies in a line the
+    // quarter-warp's active lanes touch anyway, where column 0 added a line
+    // (one more L1 wavefront per gathered row at N = 44)
+    bbase[c] = reinterpret_cast<const char*>(a.b + (colok[c] ? col0 + c * SUB : a.n - uint32_t(VEC)));
+#endif
 #pragma unroll
     for (int e = 0; e < VEC; ++e) {
       acc[c][e] = R::init();
