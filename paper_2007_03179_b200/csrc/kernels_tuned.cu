@@ -383,7 +383,8 @@ __global__ void __launch_bounds__(WARPS * 32) k_cta(SpmmArgs a) {
   __syncthreads();
 
   const float* bcol = a.b + col0;
-  const float* bsafe = colok ? bcol : a.b;
+  // lanes past N re-read the row's last vector (a line the active lanes touch)
+  const float* bsafe = colok ? bcol : a.b + (a.n - uint32_t(VEC));
   for (uint32_t off = 0, buf = 0; off < len; off += CHUNK, buf ^= 1u) {
     // issue the next chunk's sparse loads before consuming this one
     uint2 nxt[PER_T];
