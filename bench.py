@@ -47,6 +47,7 @@ CONFIGS = {
                    desc="Pubmed-shaped uniform CSR (19717 rows, 88648 nnz) x dense fp32 N=128, sum"),
 }
 GEN_SEED, VAL_SEED, B_SEED = 1, 2, 42
+DATA_DESC = "synthetic (seeded power-law / uniform generator, reference value and B generators)"
 
 
 def log(*a):
@@ -58,6 +59,8 @@ def log(*a):
 # ---------------------------------------------------------------------------
 
 def make_inputs(cfg):
+    """Our arm's inputs, from the product library's generators (bit-identical to
+    the oracle restatements the reference arm uses, tests/test_oracle.py)."""
     import paper_2007_03179_b200 as G
     t0 = time.perf_counter()
     if cfg["kind"] == "powerlaw":
@@ -69,6 +72,60 @@ def make_inputs(cfg):
     return a
 
 
+class HostCsr:
+    """Plain-array CSR for the reference arm (no product types)."""
+
+    def __init__(self, n_rows, n_cols, row_ptr, col_ind, vals):
+        self.n_rows, self.n_cols = int(n_rows), int(n_cols)
+        self.row_ptr, self.col_ind, self.vals = row_ptr, col_ind, vals
+
+    def nnz(self):
+        return int(len(self.col_ind))
+
+
+def make_inputs_reference(cfg):
+    """The reference arm's inputs, built WITHOUT the product library: the
+    reference's own gen_uniform_random (oracle/_ref) for the uniform shape, the
+    oracle's C restatement of the power-law generator otherwise, then the
+    value / B generators restated from the reference (oracle/powerlaw_oracle.c)."""
+    import oracle as O
+    t0 = time.perf_counter()
+    if cfg["kind"] == "powerlaw":
+        rp, ci, v = O.gen_powerlaw(cfg["rows"], cfg["nnz"], cfg["maxdeg"], cfg["exponent"],
+                                   GEN_SEED)
+    elif O.ref_available():
+        rp, ci, v = O.ref_gen_uniform(cfg["rows"], cfg["nnz"], GEN_SEED)
+    else:
+        raise SystemExit("bench.py --impl reference: oracle/_ref not built (uniform generator)")
+    v = np.ascontiguousarray(v, np.float32)
+    O.randomize_values(v, VAL_SEED)
+    a = HostCsr(cfg["rows"], cfg["rows"], rp, ci, v)
+    b = O.make_random_dense(a.n_cols, cfg["n"], B_SEED)
+    log(f"[bench] reference inputs {a.n_rows} rows / {a.nnz()} nnz in "
+        f"{time.perf_counter() - t0:.1f}s (oracle generators, no product library)")
+    return a, b
+
+
+def config_of(cfg, world, exact=True):
+    """The `config` object, identical in both arms for the same workload."""
+    return {"workload": cfg["desc"], "rows": cfg["rows"], "nnz": cfg["nnz"], "n": cfg["n"],
+            "op": cfg["op"], "arg": bool(cfg.get("arg")), "exact": bool(exact),
+            "parallelism": f"row-shard x{world}",
+            "l2": "flushed between steps (512 MB write)"}
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
+
+
 def algorithmic_bytes(a, n, arg):
     """4(M+1) + 8 nnz + 4 U N + 4 M N (+ 4 M N for arg), U = distinct columns."""
     u = int(np.count_nonzero(np.bincount(a.col_ind, minlength=a.n_cols))) if a.nnz() else 0
@@ -77,18 +134,18 @@ def algorithmic_bytes(a, n, arg):
 
 
 def sample_rows(a, frac, seed=0):
-    """Strided row sample (keeps the degree mix) as a standalone CSR."""
-    from paper_2007_03179_b200.dist import shard_csr  # noqa: F401
-    import paper_2007_03179_b200 as G
+    """Strided row sample (keeps the degree mix) as a standalone plain-array CSR."""
     m = a.n_rows
     step = max(1, int(round(1.0 / max(frac, 1e-9))))
+    if step == 1:
+        return HostCsr(a.n_rows, a.n_cols, a.row_ptr, a.col_ind, a.vals)
     rows = np.arange(seed % step, m, step, dtype=np.int64)
     rp = a.row_ptr.astype(np.int64)
     lens = rp[rows + 1] - rp[rows]
     idx = np.concatenate([np.arange(rp[r], rp[r + 1]) for r in rows]) if len(rows) else \
         np.zeros(0, np.int64)
-    return G.CsrMatrix(len(rows), a.n_cols, np.concatenate([[0], np.cumsum(lens)]).astype(np.uint32),
-                       a.col_ind[idx], a.vals[idx])
+    return HostCsr(len(rows), a.n_cols, np.concatenate([[0], np.cumsum(lens)]).astype(np.uint32),
+                   np.ascontiguousarray(a.col_ind[idx]), np.ascontiguousarray(a.vals[idx]))
 
 
 # ---------------------------------------------------------------------------
@@ -197,42 +254,56 @@ def ncu_traffic(config):
 # CPU baseline: the reference's own native_spmm (oracle/_ref) or the restatement
 # ---------------------------------------------------------------------------
 
-def cpu_sample_run(a, b, op, target_s=12.0):
+def _cpu_runner(sub, b, op, threads):
+    """One CPU SpMM step over `sub`: the reference's spmm::bench window
+    (oracle/_ref, RefSession, repeats=1) for the ops it has, else the oracle's
+    C restatement of the same fold (mean / min / arg have no reference code)."""
     import oracle as O
-    flops_per_nnz = 2 * b.shape[1]
-    use_ref = O.ref_available()
-    threads = O.ref_hardware_concurrency() if use_ref else (os.cpu_count() or 1)
+    use_ref = O.ref_available() and op in ("sum", "max")
     variant, cf = ("crc", 1) if b.shape[1] <= 32 else ("crc-cwm", 2)
+    if use_ref:
+        sess = O.RefSession(sub.n_rows, sub.n_cols, sub.row_ptr, sub.col_ind, sub.vals, b)
 
-    def run(sub):
-        t0 = time.perf_counter()
-        if use_ref and op in ("sum", "max"):
-            O.ref_native_spmm(sub.n_rows, sub.n_cols, sub.row_ptr, sub.col_ind, sub.vals, b, op,
-                              variant, cf, 0)
-        else:
+        def run():
+            return sess.bench(op, variant, cf, 0, 1)["median_s"]
+        what = f"spmm::bench(native_spmm {variant}{'' if variant == 'crc' else f'({cf})'}, " \
+               f"repeats=1) window, oracle/_ref"
+    else:
+        def run():
+            t0 = time.perf_counter()
             O.spmm(sub.n_rows, sub.n_cols, sub.row_ptr, sub.col_ind, sub.vals, b, op,
                    want_arg=op in ("max", "min"), threads=threads)
-        return time.perf_counter() - t0
+            return time.perf_counter() - t0
+        what = "oracle C restatement of the fold (no reference implementation of this op)"
+    return run, ("reference" if use_ref else "port"), what
 
+
+def cpu_sample_run(a, b, op, target_s=12.0):
+    """The reported cpu_baseline: the reference on this host's cores, over the
+    whole matrix when one pass fits `target_s`, else a strided row sample."""
+    import oracle as O
+    threads = O.ref_hardware_concurrency() if O.ref_available() else (os.cpu_count() or 1)
     frac = 1.0 / 512
-    sub = sample_rows(a, frac)
-    t = run(sub)
-    while t < 0.5 and frac < 1.0:
-        frac = min(1.0, frac * 4)
+    while True:
         sub = sample_rows(a, frac)
-        t = run(sub)
-    rate = sub.nnz() / max(t, 1e-9)
-    frac = min(1.0, frac * target_s / max(t, 1e-9)) if t < target_s else frac
-    sub = sample_rows(a, frac)
-    t = run(sub)
-    gflops = flops_per_nnz * sub.nnz() / t / 1e9
-    kind = "reference" if (use_ref and op in ("sum", "max")) else "port"
-    del rate
+        run, kind, what = _cpu_runner(sub, b, op, threads)
+        t = run()
+        if t >= 0.5 or frac >= 1.0:
+            break
+        frac = min(1.0, frac * 4)
+    if t < target_s and frac < 1.0:
+        frac = min(1.0, frac * target_s / max(t, 1e-9))
+        sub = sample_rows(a, frac)
+        run, kind, what = _cpu_runner(sub, b, op, threads)
+    reps = max(1, min(5, int(target_s / max(t, 1e-3))))
+    ts = sorted(run() for _ in range(reps))
+    t = ts[(len(ts) - 1) // 2]
+    gflops = 2 * b.shape[1] * sub.nnz() / t / 1e9
     return {"value": round(gflops, 4), "unit": "GFLOP/s", "cores": threads, "kind": kind,
+            "cpu_model": cpu_model(),
             "sample": f"every {int(round(1 / frac))}th row: {sub.n_rows} rows / {sub.nnz()} nnz "
-                      f"({100.0 * sub.nnz() / max(a.nnz(), 1):.2f}% of nnz), "
-                      f"{'spmm::native_spmm ' + variant if kind == 'reference' else 'oracle restatement'}"
-                      f", {t:.1f}s", "seconds": round(t, 2)}
+                      f"({100.0 * sub.nnz() / max(a.nnz(), 1):.2f}% of nnz); {what}; median of "
+                      f"{reps}", "seconds": round(t, 3)}
 
 
 # ---------------------------------------------------------------------------
@@ -257,6 +328,12 @@ def init_dist(world, local):
         import torch.distributed as dist
         backend = os.environ.get("GESPMM_DIST_BACKEND", "nccl")
         if backend == "nccl":
+            if world > torch.cuda.device_count():
+                raise SystemExit(f"bench.py: {world} NCCL ranks but {torch.cuda.device_count()} "
+                                 "GPU(s); GESPMM_DIST_BACKEND=gloo shares one device")
+            # communicator lines (nRanks, NVLS/NVLink transports) in each rank's stderr
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
             dist.init_process_group("nccl", device_id=dev)
         else:
             dist.init_process_group(backend)
@@ -264,54 +341,50 @@ def init_dist(world, local):
 
 
 def run_reference(args, cfg):
+    """The reference arm: the reference's own CPU native_spmm (oracle/_ref,
+    unmodified headers) on this host's cores, inside its own spmm::bench
+    timing window, on inputs built without the product library.  Rank 0
+    only; other ranks exit without work."""
     world, rank, _ = dist_env()
     if rank != 0:
         return 0
     import oracle as O
-    import paper_2007_03179_b200 as G
-    a = make_inputs(cfg)
-    b = G.make_random_dense(a.n_cols, cfg["n"], B_SEED).data
+    a, b = make_inputs_reference(cfg)
     op = cfg["op"]
-    use_ref = O.ref_available() and op in ("sum", "max")
     threads = O.ref_hardware_concurrency() if O.ref_available() else (os.cpu_count() or 1)
-    # size one step so (warmup + steps) samples take ~2 minutes in total
+    # one step over the whole matrix when (warmup + steps) of them take ~2 min,
+    # else a strided row sample sized to that budget
     per_step = max(0.2, 120.0 / max(1, args.steps + args.warmup))
-    probe = cpu_sample_run(a, b, op, target_s=min(per_step, 2.0))
-    rate_nnz = probe["value"] * 1e9 / (2 * cfg["n"])
-    frac = min(1.0, rate_nnz * per_step / a.nnz())
-    sub = sample_rows(a, frac, seed=1)
-    variant, cf = ("crc", 1) if cfg["n"] <= 32 else ("crc-cwm", 2)
-
-    def step():
-        if use_ref:
-            O.ref_native_spmm(sub.n_rows, sub.n_cols, sub.row_ptr, sub.col_ind, sub.vals, b, op,
-                              variant, cf, 0)
-        else:
-            O.spmm(sub.n_rows, sub.n_cols, sub.row_ptr, sub.col_ind, sub.vals, b, op,
-                   want_arg=op in ("max", "min"), threads=threads)
-
+    frac = 1.0
+    sub = a
+    run, kind, what = _cpu_runner(sub, b, op, threads)
+    t = run()
+    if t > per_step:
+        frac = max(1.0 / 4096, per_step / t)
+        sub = sample_rows(a, frac, seed=1)
+        run, kind, what = _cpu_runner(sub, b, op, threads)
     for _ in range(args.warmup):
-        step()
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        step()
-    total = time.perf_counter() - t0
+        run()
+    times = [run() for _ in range(args.steps)]
+    total = float(sum(times))
     flops = 2 * sub.nnz() * cfg["n"]
     value = flops * args.steps / total / 1e9
-    kind = "reference" if use_ref else "port"
+    sample = (f"{'whole matrix' if sub is a else f'every {int(round(1 / frac))}th row'}: "
+              f"{sub.n_rows} rows / {sub.nnz()} nnz per step; {what}"
+              + ("; max only (the reference has no argmax)" if cfg.get("arg") else ""))
     line = {
         "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": "GFLOP/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(1e3 * total / args.steps, 3), "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": cfg["desc"], "rows": a.n_rows, "nnz": a.nnz(), "n": cfg["n"],
-                   "op": op, "sample_rows": sub.n_rows, "sample_nnz": sub.nnz()},
+        "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+        "data": DATA_DESC,
+        "config": config_of(cfg, world),
         "cpu_baseline": {"value": round(value, 4), "unit": "GFLOP/s", "cores": threads,
-                         "kind": kind,
-                         "sample": f"every {int(round(1 / frac))}th row ({sub.nnz()} nnz) per "
-                                   f"step; {'spmm::native_spmm ' + variant + ' (oracle/_ref)' if use_ref else 'oracle restatement'}"},
+                         "kind": kind, "cpu_model": cpu_model(), "sample": sample},
         "e2e": {"value": round(value, 4), "unit": "GFLOP/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
+        "step_s": {"min": round(min(times), 4), "median": round(statistics.median(times), 4),
+                   "max": round(max(times), 4)},
     }
     print(json.dumps(line), flush=True)
     return 0
@@ -334,16 +407,29 @@ def run_ours(args, cfg):
     info = D.ShardInfo(rank, world, bounds)
     shard = D.shard_csr(a, info.lo, info.hi) if world > 1 else a
 
-    # B: generated on rank 0, replicated once over NCCL
+    # B: generated on rank 0, replicated once over NCCL (timed apart from the step)
     if rank == 0:
         b_host = G.make_random_dense(a.n_cols, n, B_SEED).data
         bt = torch.from_numpy(b_host).to(dev)
     else:
         b_host = None
         bt = torch.empty((a.n_cols, n), dtype=torch.float32, device=dev)
+    setup = None
     if world > 1:
-        D.broadcast_dense(bt, 0)
+        import torch.distributed as dist
+        dist.barrier()
         torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        D.broadcast_dense(bt, 0)
+        e1.record()
+        torch.cuda.synchronize()
+        bms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+        dist.all_reduce(bms, op=dist.ReduceOp.MAX)
+        setup = {"b_broadcast_ms": round(float(bms.item()), 3),
+                 "b_broadcast_bytes": int(bt.numel() * 4),
+                 "backend": dist.get_backend(),
+                 "note": "one-time replication of B (not in the step), max over ranks"}
     d = G.DeviceCsr.from_host(shard, dev)
     c = torch.empty((shard.n_rows, n), dtype=torch.float32, device=dev)
     arg = torch.empty((shard.n_rows, n), dtype=torch.int32, device=dev) if want_arg else None
@@ -528,13 +614,11 @@ def run_ours(args, cfg):
             "metric": METRIC, "value": round(value, 3), "unit": "GFLOP/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
-            "data": "synthetic (seeded power-law generator, reference value/B generators)",
-            "config": {"workload": cfg["desc"], "rows": a.n_rows, "nnz": a.nnz(), "n": n,
-                       "op": op, "arg": want_arg, "variant": args.variant,
-                       "exact": not args.fast, "shards": "nnz-balanced contiguous rows",
-                       "parallelism": f"row-shard x{world}",
-                       "l2": "flushed between steps (512 MB write); inputs 1.16 GB > L2",
-                       "plan": plan.description},
+            "data": DATA_DESC,
+            "config": config_of(cfg, world, exact=not args.fast),
+            "variant": args.variant, "plan": plan.description,
+            "shards": {"kind": "nnz-balanced contiguous rows", "bounds": [int(x) for x in bounds]},
+            "setup": setup,
             "hbm_gbs": round(achieved, 1),
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
                          "unit": "GB/s", "frac": round(achieved / peak, 4),
@@ -555,6 +639,14 @@ def run_ours(args, cfg):
             "cpu_baseline": cpu,
         }
         print(json.dumps(line), flush=True)
+    if args.dump_c:
+        # per-rank shard of C (and arg) for the parity tests; rank 0 adds the bounds
+        np.save(f"{args.dump_c}.rank{rank}.npy", c.cpu().numpy())
+        if arg is not None:
+            np.save(f"{args.dump_c}.arg.rank{rank}.npy", arg.cpu().numpy())
+        if rank == 0:
+            with open(f"{args.dump_c}.bounds.json", "w") as f:
+                json.dump({"bounds": [int(x) for x in bounds], "world": world}, f)
     plan.close()
     if world > 1:
         import torch.distributed as dist
@@ -586,6 +678,7 @@ def run_gcn(args):
     for _ in range(args.warmup):
         model.step(ht, yt, adj, info_arg, a.n_rows)
     torch.cuda.synchronize()
+    gcn.EXCHANGE_EVENTS = [] if world > 1 else None
     st = torch.cuda.current_stream()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     launches0 = G.launch_count()
@@ -604,6 +697,17 @@ def run_gcn(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     flops = gcn.spmm_flops_per_step(a.nnz(), gcfg)
+    exchange = None
+    if gcn.EXCHANGE_EVENTS:
+        ag = sum(s.elapsed_time(e) for s, e in gcn.EXCHANGE_EVENTS)
+        t = torch.tensor([ag], dtype=torch.float64, device=dev)
+        import torch.distributed as dist
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        exchange = {"allgather_ms_per_step": round(float(t.item()) / args.steps, 3),
+                    "allgathers_per_step": len(gcn.EXCHANGE_EVENTS) // args.steps,
+                    "note": "per-layer in-place ncclAllGather into the padded buffer (inside "
+                            "the step), max over ranks"}
+    gcn.EXCHANGE_EVENTS = None
     if rank == 0:
         print(json.dumps({
             "metric": "GCN 2-layer training step (Reddit shape, hidden 256): SpMM GFLOP/s "
@@ -615,6 +719,7 @@ def run_gcn(args):
             "config": {"workload": "two-layer GCN, Reddit-shaped power-law graph, features 602, "
                                    "hidden 256, classes 41, full batch, SGD",
                        "parallelism": f"row-shard x{world}, per-layer all-gather"},
+            "exchange": exchange,
             "loss": round(float(loss.item()), 6),
             "gpu_launches": G.launch_count() - launches0}), flush=True)
     adj.close()
@@ -622,6 +727,22 @@ def run_gcn(args):
         import torch.distributed as dist
         dist.destroy_process_group()
     return 0
+
+
+def relaunch(args):
+    """`bench.py --gpus N` outside torchrun: start N ranks (one process per GPU)
+    under torch.distributed.run on this node and return rank 0's exit code.
+    Rank 0 prints the JSON line."""
+    import socket
+    import subprocess
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1", f"--master-port={port}",
+           os.path.abspath(__file__)] + sys.argv[1:]
+    log(f"[bench] launching {args.gpus} ranks: {' '.join(cmd)}")
+    return subprocess.call(cmd)
 
 
 def main():
@@ -653,9 +774,17 @@ def main():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--no-ceiling", action="store_true", help="skip the live gather-ceiling probe")
+    p.add_argument("--dump-c", default="", help="save each rank's C shard to PATH.rank<r>.npy")
     p.add_argument("--cluster-hot", type=int, default=0,
                    help="N=128: hot B rows in cluster DSMEM, cluster size 2/4/8/16 (0 off)")
     args = p.parse_args()
+    if args.gpus < 1:
+        raise SystemExit("bench.py: --gpus must be >= 1")
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        return relaunch(args)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     if args.warmup < 3:
         log("[bench] warmup raised to 3 (timing rules)")
         args.warmup = 3

@@ -55,6 +55,13 @@ def _load_oracle():
                                     _f32p, C.c_void_p]
         lib.oracle_checksum.restype = C.c_uint64
         lib.oracle_checksum.argtypes = [C.c_uint32, C.c_uint32, C.c_void_p]
+        lib.oracle_gen_powerlaw.restype = C.c_int
+        lib.oracle_gen_powerlaw.argtypes = [C.c_uint32, C.c_uint64, C.c_uint32, C.c_double,
+                                            C.c_uint64, C.c_int, _u32p, C.c_void_p, C.c_void_p]
+        lib.oracle_make_random_dense.restype = None
+        lib.oracle_make_random_dense.argtypes = [C.c_uint32, C.c_uint32, C.c_uint64, C.c_void_p]
+        lib.oracle_randomize_values.restype = None
+        lib.oracle_randomize_values.argtypes = [C.c_void_p, C.c_uint64, C.c_uint64]
         lib.oracle_validate.restype = C.c_int
         lib.oracle_validate.argtypes = [C.c_uint32, C.c_uint32, _u32p, C.c_uint64, _u32p,
                                         C.c_uint64, C.c_uint64, C.c_char_p, C.c_uint32]
@@ -109,6 +116,13 @@ def _load_ref():
         lib.ref_load_matrix.restype = C.c_int
         lib.ref_load_matrix.argtypes = [cp, C.POINTER(cu), C.POINTER(cu), C.POINTER(cull),
                                         C.c_void_p, C.c_void_p, C.c_void_p, cp, cu]
+        lib.ref_session_new.restype = C.c_void_p
+        lib.ref_session_new.argtypes = [cu, cu, cull, _u32p, _u32p, _f32p, _f32p, cu, cp, cu]
+        lib.ref_session_bench.restype = C.c_int
+        lib.ref_session_bench.argtypes = [C.c_void_p, cp, C.c_int, cu, cu, cu, C.POINTER(cd),
+                                          C.POINTER(cd), C.POINTER(cd), C.POINTER(cull), cp, cu]
+        lib.ref_session_free.restype = None
+        lib.ref_session_free.argtypes = [C.c_void_p]
         lib.ref_hardware_concurrency.restype = cu
         lib.ref_hardware_concurrency.argtypes = []
         _ref = lib
@@ -142,6 +156,43 @@ def spmm(m, k, row_ptr, col_ind, vals, b, op="sum", want_arg=False, arg_kind=ARG
     if rc != 0:
         raise ValueError("oracle_spmm: bad arguments")
     return c, arg
+
+
+def gen_powerlaw(rows, nnz_target, max_degree, exponent=1.0, seed=1, threads=None):
+    """Restatement of the benchmark's power-law generator (powerlaw_oracle.c);
+    returns (row_ptr, col_ind, vals) — bit-identical to the product's
+    gen_powerlaw, built without loading the product library."""
+    lib = _load_oracle()
+    threads = threads or os.cpu_count() or 1
+    rp = np.zeros(rows + 1, np.uint32)
+    rc = lib.oracle_gen_powerlaw(rows, nnz_target, max_degree, exponent, seed, threads, rp,
+                                 None, None)
+    if rc:
+        raise ValueError(f"oracle_gen_powerlaw: rc {rc}")
+    nnz = int(rp[-1])
+    ci = np.empty(max(nnz, 1), np.uint32)
+    v = np.empty(max(nnz, 1), np.float32)
+    rc = lib.oracle_gen_powerlaw(rows, nnz_target, max_degree, exponent, seed, threads, rp,
+                                 ci.ctypes.data, v.ctypes.data)
+    if rc:
+        raise ValueError(f"oracle_gen_powerlaw: rc {rc}")
+    return rp, ci[:nnz], v[:nnz]
+
+
+def make_random_dense(rows, cols, seed):
+    """dense.hpp:51-59 restated (MT19937-64 in C)."""
+    out = np.empty((rows, cols), np.float32)
+    if out.size:
+        _load_oracle().oracle_make_random_dense(rows, cols, seed, out.ctypes.data)
+    return out
+
+
+def randomize_values(vals, seed):
+    """generate.hpp:73-80 restated; fills ``vals`` (float32, contiguous) in place."""
+    assert vals.dtype == np.float32 and vals.flags.c_contiguous
+    if vals.size:
+        _load_oracle().oracle_randomize_values(vals.ctypes.data, vals.size, seed)
+    return vals
 
 
 def checksum(c: np.ndarray) -> int:
@@ -210,6 +261,45 @@ def ref_bench(m, k, row_ptr, col_ind, vals, b, op="sum", variant="crc-cwm", cf=2
         raise RefError(e.value.decode())
     return {"median_s": med.value, "mean_s": mean.value, "gflops": gf.value,
             "checksum": cs.value}
+
+
+class RefSession:
+    """The reference's CsrMatrix + DenseMatrix built once; ``bench()`` runs
+    spmm::bench (native.hpp:156-180) on them, so only the reference's own
+    timing window is measured."""
+
+    def __init__(self, m, k, row_ptr, col_ind, vals, b):
+        lib = _load_ref()
+        b = np.ascontiguousarray(b, np.float32)
+        self.n = b.shape[1]
+        e = _err()
+        self._h = lib.ref_session_new(m, k, len(col_ind), _nz(row_ptr, np.uint32),
+                                      _nz(col_ind, np.uint32), _nz(vals, np.float32),
+                                      _nz(b.reshape(-1), np.float32), self.n, e, 1024)
+        if not self._h:
+            raise RefError(e.value.decode())
+
+    def bench(self, op="sum", variant="crc-cwm", cf=2, workers=0, repeats=1):
+        med, mean, gf = C.c_double(), C.c_double(), C.c_double()
+        cs = C.c_ulonglong()
+        e = _err()
+        if _load_ref().ref_session_bench(self._h, op.encode(), KIND[variant], cf, workers,
+                                         repeats, C.byref(med), C.byref(mean), C.byref(gf),
+                                         C.byref(cs), e, 1024):
+            raise RefError(e.value.decode())
+        return {"median_s": med.value, "mean_s": mean.value, "gflops": gf.value,
+                "checksum": cs.value}
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _load_ref().ref_session_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def ref_dense_reference(m, k, row_ptr, col_ind, vals, b, op="sum"):

@@ -9,7 +9,7 @@
 //
 // Reference entry points wrapped (file:line under /root/reference/proj):
 //   spmm::native_spmm        include/spmm/native.hpp:101-143
-//   spmm::bench              include/spmm/native.hpp:156-180
+//   spmm::bench              include/spmm/native.hpp:156-180 (also per session)
 //   spmm::dense_reference    include/spmm/oracle.hpp:42-57
 //   spmm::gen_uniform_random include/spmm/generate.hpp:39-69
 //   spmm::randomize_values   include/spmm/generate.hpp:73-80
@@ -292,6 +292,46 @@ int ref_load_matrix(const char* path, unsigned* m, unsigned* k, unsigned long lo
     return 1;
   }
 }
+
+// A bench session: the CsrMatrix and B built ONCE (outside any timed window),
+// then spmm::bench (native.hpp:156-180) per call — the reference's own timing
+// window around native_spmm.  bench.py's --impl reference arm times each step
+// with ref_session_bench(repeats = 1), so no shim copy is ever inside a step.
+struct RefSession {
+  CsrMatrix a;
+  DenseMatrix b;
+};
+
+void* ref_session_new(unsigned m, unsigned k, unsigned long long nnz, const unsigned* row_ptr,
+                      const unsigned* col_ind, const float* vals, const float* b, unsigned n,
+                      char* err, unsigned err_len) {
+  try {
+    return new RefSession{make_csr(m, k, nnz, row_ptr, col_ind, vals), make_dense(k, n, b)};
+  } catch (const std::exception& e) {
+    put_err(err, err_len, e.what());
+    return nullptr;
+  }
+}
+
+int ref_session_bench(void* h, const char* op_name, int kind, unsigned cf, unsigned workers,
+                      unsigned repeats, double* median_s, double* mean_s, double* gflops,
+                      unsigned long long* csum, char* err, unsigned err_len) {
+  try {
+    const RefSession* s = static_cast<const RefSession*>(h);
+    const ThroughputReport r =
+        bench(s->a, s->b, variant_of(kind, cf), reduce_op_by_name(op_name), workers, repeats);
+    *median_s = r.elapsed_s;
+    *mean_s = r.elapsed_mean_s;
+    *gflops = r.gflops;
+    *csum = r.output_checksum;
+    return 0;
+  } catch (const std::exception& e) {
+    put_err(err, err_len, e.what());
+    return 1;
+  }
+}
+
+void ref_session_free(void* h) { delete static_cast<RefSession*>(h); }
 
 unsigned ref_hardware_concurrency() { return std::max(1u, std::thread::hardware_concurrency()); }
 

@@ -23,10 +23,15 @@ uint64_t pack_cols_block(const uint32_t* row_ptr, const uint32_t* col_ind, uint3
   // with every core packing, the packing contends with the copy engine's reads
   // of host memory and with the CUDA driver threads (Reddit, 16 cores: 17.9 ms
   // at 16 threads, 16.3 ms at 12, 16.7-19.3 ms at 8; tools/e2e_threads.py)
+  // GESPMM_PACK_THREADS overrides; under torchrun (LOCAL_WORLD_SIZE set, which
+  // also forces OMP_NUM_THREADS=1) the host's threads are split between ranks
   static const int nt = [] {
-    if (std::getenv("OMP_NUM_THREADS")) return std::max(1, omp_get_max_threads());
+    if (const char* e = std::getenv("GESPMM_PACK_THREADS")) return std::max(1, std::atoi(e));
+    const char* lws = std::getenv("LOCAL_WORLD_SIZE");
+    if (std::getenv("OMP_NUM_THREADS") && !lws) return std::max(1, omp_get_max_threads());
     const int hw = int(std::thread::hardware_concurrency());
-    return std::max(1, hw > 4 ? hw * 3 / 4 : hw);
+    const int mine = std::max(1, hw > 4 ? hw * 3 / 4 : hw);
+    return lws ? std::max(1, mine / std::max(1, std::atoi(lws))) : mine;
   }();
   // rows split by nnz across threads
   std::vector<uint32_t> cut(size_t(nt) + 1, hi);

@@ -9,8 +9,10 @@ data:
 
 * ``broadcast_dense`` — the dense operand B, once per B (north_star: "replicated
   once via NCCL broadcast");
-* ``allgather_rows`` — variable-size C row blocks for the next layer
-  (padded to the largest shard, as ncclAllGather needs equal counts).
+* ``allgather_padded`` — variable-size C row blocks for the next layer, one
+  in-place ncclAllGather into a buffer padded to the largest shard (equal
+  counts); ``pad_columns`` re-indexes a shard's columns into that buffer so
+  the next SpMM reads it directly (``allgather_rows`` compacts it instead).
 
 The compute callable is injected, so the plumbing is tested on CPU (gloo)
 with the oracle as the per-shard compute, and runs the CUDA path on the box.
@@ -82,19 +84,52 @@ def broadcast_dense(tensor, src: int = 0, group=None):
     return tensor
 
 
-def allgather_rows(local, info: ShardInfo, group=None):
-    """Assemble the full M x N output from per-rank row blocks of unequal height.
-    Each block is padded to the largest shard, all-gathered, then unpadded."""
+def allgather_padded(local, info: ShardInfo, out=None, group=None):
+    """Per-layer exchange into ONE padded buffer: rank r's block lands at rows
+    [r*pad, r*pad + rows_r) of ``out`` (world*pad x N), pad = the largest shard.
+    One in-place all_gather_into_tensor (ncclAllGather), no per-rank buffers and
+    no concatenation.  ``local`` may already be ``out``'s own slot (zero-copy);
+    otherwise it is copied in.  Returns ``out``.  Pair it with
+    ``pad_columns`` so the next SpMM reads the padded buffer directly."""
     import torch
     import torch.distributed as dist
     n = local.shape[1]
     pad = info.max_rows
-    buf = torch.zeros((pad, n), dtype=local.dtype, device=local.device)
-    buf[: local.shape[0]].copy_(local)
-    gathered = [torch.empty_like(buf) for _ in range(info.world)]
-    dist.all_gather(gathered, buf, group=group)
-    parts = [gathered[r][: info.bounds[r + 1] - info.bounds[r]] for r in range(info.world)]
-    return torch.cat(parts, dim=0)
+    if out is None:
+        out = torch.zeros((info.world * pad, n), dtype=local.dtype, device=local.device)
+    slot = out[info.rank * pad:(info.rank + 1) * pad]
+    if local.data_ptr() != slot.data_ptr():
+        slot[: local.shape[0]].copy_(local)
+    dist.all_gather_into_tensor(out, slot, group=group)
+    return out
+
+
+def padded_row(info: ShardInfo, rows):
+    """Global row ids -> their rows in the padded all-gather buffer."""
+    b = np.asarray(info.bounds, np.int64)
+    rows = np.asarray(rows, np.int64)
+    owner = np.searchsorted(b, rows, side="right") - 1
+    return owner * info.max_rows + (rows - b[owner])
+
+
+def pad_columns(a: CsrMatrix, info: ShardInfo) -> CsrMatrix:
+    """A copy of ``a`` whose column ids index the padded all-gather buffer
+    (column c -> padded_row(c)).  The map is increasing, so rows stay sorted
+    and the fold order (ascending CSR position) is unchanged: results are
+    bit-identical to the SpMM on the compact operand."""
+    ci = padded_row(info, a.col_ind).astype(np.uint32)
+    return CsrMatrix(a.n_rows, info.world * info.max_rows, a.row_ptr.copy(), ci, a.vals.copy())
+
+
+def allgather_rows(local, info: ShardInfo, group=None):
+    """Assemble the full M x N output (compact rows) from per-rank row blocks
+    of unequal height: allgather_padded, then one gather of the valid rows."""
+    import torch
+    buf = allgather_padded(local, info, group=group)
+    if info.max_rows * info.world == info.bounds[-1]:
+        return buf
+    idx = torch.from_numpy(padded_row(info, np.arange(info.bounds[-1]))).to(buf.device)
+    return buf.index_select(0, idx)
 
 
 def distributed_spmm(a: CsrMatrix, b, rank: int, world: int,
@@ -293,20 +328,40 @@ def fused_propagate(a: CsrMatrix, x0, hops: int, info: ShardInfo, device, op: st
 
 def nccl_propagate(a: CsrMatrix, x0, hops: int, info: ShardInfo, device, op: str = "sum",
                    group=None, exec=None):
-    """The same propagation with the unfused exchange: local SpMM, then
-    allgather_rows (padded ncclAllGather).  The baseline fused_propagate replaces."""
+    """The same propagation with the unfused exchange: local SpMM into this
+    rank's slot of a padded buffer, then one in-place ncclAllGather
+    (allgather_padded); the local block's columns index that buffer
+    (pad_columns).  The baseline fused_propagate replaces."""
     from .api import DeviceCsr, ExecOptions, Plan
     import torch
     n = int(x0.shape[1])
-    local = DeviceCsr.from_host(shard_csr(a, info.lo, info.hi), device)
-    plan = Plan(local, n, op, exec=exec or ExecOptions())
-    h = x0.contiguous()
-    try:
-        for _ in range(hops):
-            y = torch.empty((info.rows, n), dtype=torch.float32, device=device)
-            if info.rows:
+    m = a.n_rows
+    if info.world == 1:
+        local = DeviceCsr.from_host(a, device)
+        plan = Plan(local, n, op, exec=exec or ExecOptions())
+        h = x0.contiguous()
+        try:
+            for _ in range(hops):
+                y = torch.empty((m, n), dtype=torch.float32, device=device)
                 plan.execute(h, y)
-            h = allgather_rows(y, info, group) if info.world > 1 else y
-        return h
+                h = y
+            return h
+        finally:
+            plan.close()
+    pad = info.max_rows
+    local = DeviceCsr.from_host(pad_columns(shard_csr(a, info.lo, info.hi), info), device)
+    plan = Plan(local, n, op, exec=exec or ExecOptions())
+    idx = torch.from_numpy(padded_row(info, np.arange(m))).to(device)
+    bufs = [torch.zeros((info.world * pad, n), dtype=torch.float32, device=device)
+            for _ in range(2)]
+    bufs[0].index_copy_(0, idx, x0.contiguous())
+    try:
+        for t in range(hops):
+            src, dst = bufs[t % 2], bufs[(t + 1) % 2]
+            slot = dst[info.rank * pad:(info.rank + 1) * pad]
+            if info.rows:
+                plan.execute(src, slot[:info.rows])
+            allgather_padded(slot, info, out=dst, group=group)
+        return bufs[hops % 2].index_select(0, idx)
     finally:
         plan.close()

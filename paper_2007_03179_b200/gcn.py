@@ -12,7 +12,9 @@ Multi-GPU (one process per GPU): nodes are row-sharded by nnz
 (dist.partition_rows); rank r holds rows [lo, hi) of A and of A^T.  Each layer
 all-gathers the transformed features before aggregating (forward) and the
 incoming gradient before the A^T aggregation (backward) — the per-layer NCCL
-all-gather of the north_star; weight gradients are all-reduced.
+all-gather of the north_star, one in-place ncclAllGather into a padded buffer
+that the local blocks' column ids index directly (dist.pad_columns: no
+concatenation); weight gradients are all-reduced.
 """
 from __future__ import annotations
 
@@ -59,17 +61,37 @@ def build_adjacency(a: CsrMatrix, device, rank: int = 0, world: int = 1,
     torch.cuda.synchronize(device)
     if world == 1:
         return Adjacency(full, at_full, exec), info
-    a_loc = DeviceCsr.from_host(D.shard_csr(a, info.lo, info.hi), device)
+    # column ids of the local blocks index the padded all-gather buffer
+    # (dist.pad_columns), so each layer's exchange feeds the SpMM directly
+    a_loc = DeviceCsr.from_host(D.pad_columns(D.shard_csr(a, info.lo, info.hi), info), device)
     at_host = at_full.to_host()
-    at_loc = DeviceCsr.from_host(D.shard_csr(at_host, info.lo, info.hi), device)
+    at_loc = DeviceCsr.from_host(D.pad_columns(D.shard_csr(at_host, info.lo, info.hi), info),
+                                 device)
     del full, at_full
     return Adjacency(a_loc, at_loc, exec), info
 
 
+# When a list, every per-layer exchange appends its (start, end) CUDA events,
+# so bench.py can report the all-gather time apart from the step.
+EXCHANGE_EVENTS = None
+
+
 def _gather(x, info: Optional[D.ShardInfo]):
+    """The per-layer exchange: one in-place ncclAllGather into the padded buffer
+    the local A / A^T blocks are column-indexed by (build_adjacency)."""
     if info is None or info.world == 1:
         return x
-    return D.allgather_rows(x.contiguous(), info)
+    import torch
+    ev = None
+    if EXCHANGE_EVENTS is not None:
+        ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+        ev[0].record()
+    out = torch.empty((info.world * info.max_rows, x.shape[1]), dtype=x.dtype, device=x.device)
+    D.allgather_padded(x.contiguous(), info, out=out)
+    if ev is not None:
+        ev[1].record()
+        EXCHANGE_EVENTS.append(ev)
+    return out
 
 
 class _Aggregate:

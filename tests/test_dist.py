@@ -87,6 +87,59 @@ def test_two_rank_gloo_spmm_equals_single_process(tmp_path, op):
         assert np.array_equal(np.load(tmp_path / f"b{r}.npy"), b.data)  # broadcast reached rank 1
 
 
+def _padded_worker(rank, world, port, result_dir):
+    """Two stacked layers on shards whose columns index the padded all-gather
+    buffer (dist.pad_columns + allgather_padded), oracle as the compute."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    a = G.gen_powerlaw(2500, 60000, 1200, 1.0, 31)
+    G.randomize_values(a, 32)
+    x0 = G.make_random_dense(2500, 12, 33).data
+    info = D.ShardInfo(rank, world, D.partition_rows(a.row_ptr, world))
+    local = D.pad_columns(D.shard_csr(a, info.lo, info.hi), info)
+    pad = info.max_rows
+    buf = torch.zeros((world * pad, 12))
+    buf[torch.from_numpy(D.padded_row(info, np.arange(2500)))] = torch.from_numpy(x0)
+    for _ in range(2):
+        y, _ = O.spmm(local.n_rows, local.n_cols, local.row_ptr, local.col_ind, local.vals,
+                      buf.numpy(), "sum")
+        nxt = torch.zeros_like(buf)
+        D.allgather_padded(torch.from_numpy(y), info, out=nxt)
+        buf = nxt
+    full = D.allgather_rows(torch.from_numpy(y), info)  # the compacting form
+    np.save(os.path.join(result_dir, f"pad_rank{rank}.npy"),
+            buf[torch.from_numpy(D.padded_row(info, np.arange(2500)))].numpy())
+    np.save(os.path.join(result_dir, f"compact_rank{rank}.npy"), full.numpy())
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_padded_allgather_two_layers_gloo(tmp_path, world):
+    mp.spawn(_padded_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    a = G.gen_powerlaw(2500, 60000, 1200, 1.0, 31)
+    G.randomize_values(a, 32)
+    x = G.make_random_dense(2500, 12, 33).data
+    for _ in range(2):
+        x, _ = O.spmm(a.n_rows, a.n_cols, a.row_ptr, a.col_ind, a.vals, x, "sum")
+    for r in range(world):
+        for name in ("pad", "compact"):
+            got = np.load(tmp_path / f"{name}_rank{r}.npy")
+            assert np.array_equal(got.view(np.uint32), x.view(np.uint32)), (name, r)
+
+
+def test_pad_columns_keeps_rows_sorted():
+    a = G.gen_powerlaw(4000, 100000, 2000, 1.0, 5)
+    info = D.ShardInfo(0, 3, D.partition_rows(a.row_ptr, 3))
+    p = D.pad_columns(a, info)
+    assert p.n_cols == 3 * info.max_rows
+    rp = p.row_ptr.astype(np.int64)
+    d = np.diff(p.col_ind.astype(np.int64))
+    inner = np.ones(p.nnz(), bool)
+    inner[rp[:-1][rp[:-1] < rp[1:]]] = False  # row starts
+    assert np.all(d[inner[1:]] > 0)
+    assert np.array_equal(D.padded_row(info, a.col_ind), p.col_ind)
+
+
 def _cuda_worker(rank, world, port, op, result_dir):
     """Two ranks sharing cuda:0 over gloo: the library's CUDA kernels as the
     per-shard compute, B broadcast and C all-gathered as CUDA tensors."""
