@@ -5,8 +5,13 @@
  * (arXiv 2007.03179 reference, /root/reference/proj/include/spmm/).  Plain
  * pointers and sizes only; no C++ or torch types cross it, no exception
  * crosses it.  Every entry point names the reference interface it replaces.
- * The C++ drop-in (namespace spmm, include/gespmm/spmm.hpp) and the Python
- * host mirror (paper_2007_03179_b200/) are thin layers over these calls.
+ * The C++ drop-in (namespace spmm, include/gespmm/native_spmm.hpp) and the
+ * Python host mirror (paper_2007_03179_b200/) are thin layers over these calls.
+ *
+ * Experimental options (l2_persist, l2_hot_mb > 0, col_slices > 1,
+ * cluster_hot) were measured slower on B200 and are compiled only into the
+ * GESPMM_EXPERIMENTAL build (gespmm_build_flags() & GESPMM_BUILD_EXPERIMENTAL);
+ * the default library rejects them with GESPMM_EUNSUPPORTED.
  *
  * Semantics (bit-exact contract):
  *   C[i][j] = fold_{p in row i, ascending} combine(acc, vals[p] * B[col_ind[p]][j])
@@ -109,7 +114,9 @@ typedef struct {
   int32_t cluster_hot; /* TUNED plans, N = 128: keep the most-gathered B rows in the distributed
                          shared memory of thread-block clusters of this many CTAs (2, 4, 8 or
                          16; one CTA per SM, 416 rows each) and gather them over DSMEM; the plan
-                         keeps a remapped copy of col_ind.  0 = off (default) */
+                         keeps a remapped copy of col_ind (a SNAPSHOT: an explicit plan must be
+                         rebuilt if col_ind changes; gespmm_spmm_device never caches such a
+                         plan).  0 = off (default) */
   int32_t h2d_pack;   /* gespmm_spmm_host: send col_ind as 16-bit row-gap codes (lossless, escapes
                          for large gaps) and rebuild it on the device: 0 = auto (>= 8M nonzeros),
                          1 = on, -1 = off */
@@ -295,6 +302,8 @@ gespmm_status_t gespmm_gen_powerlaw(uint32_t rows, uint64_t nnz_target, uint32_t
 
 /* Library / device facts for reports. */
 int32_t gespmm_abi_version(void);
+#define GESPMM_BUILD_EXPERIMENTAL 1
+int32_t gespmm_build_flags(void); /* GESPMM_BUILD_* bits this library was compiled with */
 gespmm_status_t gespmm_device_info(int32_t* sm_count, int64_t* l2_bytes,
                                    int64_t* persisting_l2_max, int32_t* cc_major,
                                    int32_t* cc_minor);

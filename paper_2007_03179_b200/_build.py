@@ -29,7 +29,11 @@ CXX_FLAGS = ["-O3", "-std=c++17", "-fPIC", "-ffp-contract=off", "-Wall", "-Wextr
              "-I", INCLUDE, "-I", CSRC, "-I", "/usr/local/cuda/include"]
 
 CU_SOURCES = ["api.cu", "validate.cu", "kernels_faithful.cu", "kernels_tuned.cu", "diag.cu",
-              "transpose.cu", "hotcols.cu", "peer.cu", "cluster.cu", "h2dpack.cu"]
+              "transpose.cu", "peer.cu", "h2dpack.cu"]
+# measured slower on B200: only in the GESPMM_EXPERIMENTAL build
+EXPERIMENTAL_CU = ["hotcols.cu", "cluster.cu"]
+LIB_EXP = os.path.join(PKG, "libgespmm_exp.so")
+BUILD_EXP = os.path.join(ROOT, "build", "gespmm_exp")
 CXX_SOURCES = ["gen.cpp", "io.cpp", "h2dpack_host.cpp"]
 HEADERS = ["common.cuh", "launch.h"]
 
@@ -49,15 +53,23 @@ def _run(cmd):
 
 
 def build(verbose: bool = False, force: bool = False, defines=(), build_dir=None,
-          lib=None) -> str:
+          lib=None, experimental: bool = False) -> str:
     """defines/build_dir/lib: an experimental variant (-D flags) built into its
-    own object dir and library path (tools/variant_build.py)."""
+    own object dir and library path (tools/variant_build.py).
+    experimental: also compile the measured-slower options (cluster DSMEM hot
+    rows, hot-column L2 map, column slices, L2 persistence) into
+    libgespmm_exp.so (selected at run time with GESPMM_EXPERIMENTAL=1)."""
+    if experimental:
+        defines = tuple(defines) + ("GESPMM_EXPERIMENTAL",)
+        build_dir = build_dir or BUILD_EXP
+        lib = lib or LIB_EXP
     BUILD = build_dir or globals()["BUILD"]
     LIB = lib or globals()["LIB"]
+    cu_sources = CU_SOURCES + (EXPERIMENTAL_CU if "GESPMM_EXPERIMENTAL" in defines else [])
     os.makedirs(BUILD, exist_ok=True)
     hdrs = [os.path.join(CSRC, h) for h in HEADERS] + [os.path.join(INCLUDE, "gespmm", "gespmm.h")]
     jobs, objs = [], []
-    for src in CU_SOURCES + CXX_SOURCES:
+    for src in cu_sources + CXX_SOURCES:
         path = os.path.join(CSRC, src)
         obj = os.path.join(BUILD, src + ".o")
         objs.append(obj)
@@ -87,5 +99,6 @@ def build(verbose: bool = False, force: bool = False, defines=(), build_dir=None
 
 
 if __name__ == "__main__":
-    build(verbose="-v" in sys.argv, force="-f" in sys.argv)
-    print(LIB)
+    exp = "--experimental" in sys.argv or os.environ.get("GESPMM_EXPERIMENTAL") == "1"
+    build(verbose="-v" in sys.argv, force="-f" in sys.argv, experimental=exp)
+    print(LIB_EXP if exp else LIB)

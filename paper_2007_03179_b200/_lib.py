@@ -15,7 +15,10 @@ import threading
 _HERE = os.path.dirname(os.path.abspath(__file__))
 # GESPMM_LIB: an alternative build of the same library (A/B kernel experiments,
 # tools/variant_build.py); the default is the in-tree build.
-LIB_PATH = os.environ.get("GESPMM_LIB") or os.path.join(_HERE, "libgespmm.so")
+# GESPMM_EXPERIMENTAL=1 selects the build with the measured-slower options
+# (libgespmm_exp.so, _build.build(experimental=True)).
+LIB_PATH = os.environ.get("GESPMM_LIB") or os.path.join(
+    _HERE, "libgespmm_exp.so" if os.environ.get("GESPMM_EXPERIMENTAL") == "1" else "libgespmm.so")
 
 # gespmm_status_t
 OK, EINVAL, EDIM, ENONCANON, ECUDA, ENOMEM, EUNSUPPORTED = range(7)
@@ -41,8 +44,9 @@ EXPORTS = [
     "gespmm_diag_gather_hub", "gespmm_diag_gather_mode", "gespmm_plan_execute_gather",
     "gespmm_peer_barrier", "gespmm_peer_alloc", "gespmm_peer_free", "gespmm_ipc_get_handle",
     "gespmm_ipc_open_handle", "gespmm_ipc_close", "gespmm_multicast_alloc",
-    "gespmm_multicast_free",
+    "gespmm_multicast_free", "gespmm_build_flags",
 ]
+BUILD_EXPERIMENTAL = 1
 MAX_GATHER_DSTS = 8
 
 
@@ -133,6 +137,8 @@ def lib():
         L.gespmm_gen_powerlaw.restype = C.c_int
         L.gespmm_abi_version.argtypes = []
         L.gespmm_abi_version.restype = i32
+        L.gespmm_build_flags.argtypes = []
+        L.gespmm_build_flags.restype = i32
         L.gespmm_device_info.argtypes = [C.POINTER(i32), C.POINTER(C.c_int64),
                                          C.POINTER(C.c_int64), C.POINTER(i32), C.POINTER(i32)]
         L.gespmm_device_info.restype = C.c_int
@@ -189,6 +195,12 @@ def default_options(**kw) -> Options:
             raise TypeError(f"unknown option {k}")
         setattr(o, k, int(v))
     return o
+
+
+def experimental_built() -> bool:
+    """True when the loaded library carries the experimental (measured-slower)
+    options: GESPMM_EXPERIMENTAL=1 build, or GESPMM_LIB pointing at one."""
+    return bool(lib().gespmm_build_flags() & BUILD_EXPERIMENTAL)
 
 
 def launch_count() -> int:

@@ -565,6 +565,21 @@ class DeviceCsr:
                    self.vals.data_ptr() if self.nnz() else None)
 
 
+def _require_dense(t, rows: int, cols: int, dtype, device, what: str):
+    """Raw device pointers go to the kernels: refuse anything that is not a
+    contiguous 2-D tensor of exactly the plan's shape, dtype and device."""
+    import torch
+    ok = (isinstance(t, torch.Tensor) and t.dim() == 2 and t.dtype == dtype and t.is_cuda
+          and t.is_contiguous() and tuple(t.shape) == (rows, cols)
+          and (device is None or t.device == device))
+    if not ok:
+        got = (f"{tuple(t.shape)} {t.dtype} on {t.device}"
+               f"{'' if t.is_contiguous() else ' (non-contiguous)'}"
+               if isinstance(t, torch.Tensor) else type(t).__name__)
+        raise Error(f"{what}: expected a contiguous {rows}x{cols} {dtype} CUDA tensor"
+                    f"{'' if device is None else f' on {device}'}, got {got}", _lib.EDIM)
+
+
 def _stream_ptr(stream=None) -> Optional[int]:
     import torch
     s = stream if stream is not None else torch.cuda.current_stream()
@@ -573,8 +588,10 @@ def _stream_ptr(stream=None) -> Optional[int]:
 
 def spmm(a: DeviceCsr, b, op: ReduceOp | str = "sum", want_arg: bool = False,
          variant: KernelVariant = KernelVariant.tuned(), exec: ExecOptions = ExecOptions(),
-         validate: bool = False, out=None, stream=None):
-    """C = A (x) B on the device; returns (C, arg or None) as torch tensors."""
+         validate: bool = True, out=None, stream=None):
+    """C = A (x) B on the device; returns (C, arg or None) as torch tensors.
+    ``validate`` (default on, like the reference's native_spmm) runs the
+    canonical-CSR check on the device first."""
     import torch
     if isinstance(op, str):
         op = reduce_op_by_name(op)
@@ -585,6 +602,10 @@ def spmm(a: DeviceCsr, b, op: ReduceOp | str = "sum", want_arg: bool = False,
         raise Error(f"spmm: dimension mismatch: A is {a.n_rows}x{a.n_cols} but B has "
                     f"{b.shape[0]} rows", _lib.EDIM)
     n = b.shape[1]
+    if a.row_ptr.device != b.device:
+        raise Error(f"spmm: A is on {a.row_ptr.device} but B is on {b.device}", _lib.EDIM)
+    if out is not None:
+        _require_dense(out, a.n_rows, n, torch.float32, b.device, "spmm: out")
     c = out if out is not None else torch.empty((a.n_rows, n), dtype=torch.float32, device=b.device)
     arg = torch.empty((a.n_rows, n), dtype=torch.int32, device=b.device) if want_arg else None
     csr = a.c_struct()
@@ -620,7 +641,17 @@ class Plan:
     def launches(self) -> int:
         return int(lib().gespmm_plan_launches(self._h))
 
+    def _check_operands(self, b, c=None, arg=None):
+        import torch
+        dev = self.a.row_ptr.device
+        _require_dense(b, self.a.n_cols, self.n, torch.float32, dev, "Plan: B")
+        if c is not None:
+            _require_dense(c, self.a.n_rows, self.n, torch.float32, dev, "Plan: C")
+        if arg is not None:
+            _require_dense(arg, self.a.n_rows, self.n, torch.int32, dev, "Plan: arg")
+
     def execute(self, b, c, arg=None, stream=None):
+        self._check_operands(b, c, arg)
         _check(lib().gespmm_plan_execute(self._h, b.data_ptr(), c.data_ptr(),
                                          arg.data_ptr() if arg is not None else None,
                                          _stream_ptr(stream)))
@@ -632,6 +663,7 @@ class Plan:
         stored into replicas (fused all-gather epilogue).  ``c_dsts`` are raw
         device addresses (ints) of where this shard's row 0 lands, local first;
         ``arg_dsts`` likewise for max/min arg (or None)."""
+        self._check_operands(b)
         k = len(c_dsts)
         cd = (C.c_void_p * k)(*[int(x) for x in c_dsts])
         ad = None

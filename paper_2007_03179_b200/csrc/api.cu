@@ -85,6 +85,18 @@ gespmm_status_t validation_status(const ValidateResult& r, uint32_t m, uint32_t 
 }
 
 gespmm_status_t check_opts(const gespmm_options_t& o) {
+#ifndef GESPMM_EXPERIMENTAL
+  // options that were measured slower on B200 ship only in the
+  // experimental build (GESPMM_EXPERIMENTAL=1 python -m paper_2007_03179_b200._build)
+  const char* exp_opt = o.cluster_hot ? "cluster_hot"
+                        : o.l2_hot_mb > 0 ? "l2_hot_mb"
+                        : o.col_slices > 1 ? "col_slices"
+                        : o.l2_persist ? "l2_persist" : nullptr;
+  if (exp_opt)
+    return fail(GESPMM_EUNSUPPORTED, std::string(exp_opt) +
+                                         " is an experimental option (measured slower, DESIGN.md "
+                                         "§2); this library was built without GESPMM_EXPERIMENTAL");
+#endif
   if (o.cluster_hot != 0 && o.cluster_hot != 2 && o.cluster_hot != 4 && o.cluster_hot != 8 &&
       o.cluster_hot != 16)
     return fail(GESPMM_EINVAL, "cluster_hot must be 0, 2, 4, 8 or 16");
@@ -150,6 +162,7 @@ struct Plan {
   uint32_t hub_threshold = 0;
   bool hub_pdl = false;      // hub rows carry >= kHubPdlShare of the nonzeros
   uint32_t* d_order = nullptr;
+  uint32_t* d_work = nullptr;  // hub kernel unit counters, one per column slice (plan-owned)
   uint32_t* d_hot = nullptr;  // hot-column bitmap (frequency-aware L2 policy), nullable
   HotStats hot{};
   cudaStream_t side = nullptr;
@@ -160,8 +173,11 @@ struct Plan {
   ClusterHot ch;             // cluster-DSMEM hot-row cache (o.cluster_hot), col_ind copy
 
   ~Plan() {
+#ifdef GESPMM_EXPERIMENTAL
     free_cluster_hot(&ch);
+#endif
     if (d_order) cudaFree(d_order);
+    if (d_work) cudaFree(d_work);
     if (d_hot) cudaFree(d_hot);
     if (ev_fork) cudaEventDestroy(ev_fork);
     if (ev_join) cudaEventDestroy(ev_join);
@@ -292,7 +308,7 @@ gespmm_status_t launch_tuned_rows(const TunedShapes& t, int op, bool fast, const
                                   const uint32_t* order, uint32_t n_hub, uint32_t n_rest,
                                   cudaStream_t st, cudaStream_t side, cudaEvent_t fork,
                                   cudaEvent_t join, const cudaAccessPolicyWindow* winp,
-                                  bool hub_pdl) {
+                                  bool hub_pdl, uint32_t* work) {
   SpmmArgs a = a0;
   GESPMM_CUDA(resolve_policies(&a, st), "spmm");
   const bool v_ok = aligned(a.b, 16) && aligned(a.c, 16) && (!a.arg || aligned(a.arg, 16));
@@ -327,6 +343,7 @@ gespmm_status_t launch_tuned_rows(const TunedShapes& t, int op, bool fast, const
       SpmmArgs h = sa;
       h.order = order;
       h.n_sched = n_hub;
+      h.work = work ? work + j : nullptr;  // caller-owned counter of this launch site
       // TMA-ring hub kernel when bulk copies can address the B slices (16-byte
       // units: N % 4 == 0, ld % 4 == 0, 16-byte aligned B/C/arg at this offset)
       static const bool force_cta = [] {  // GESPMM_HUB_KCTA=1: A/B against the LDG CTA kernel
@@ -425,7 +442,10 @@ gespmm_status_t build_tuned(Plan& p, const uint32_t* host_rp, cudaStream_t st) {
     GESPMM_CUDA(cudaStreamCreateWithPriority(&p.side, cudaStreamNonBlocking, hi_prio), "plan_create");
     GESPMM_CUDA(cudaEventCreateWithFlags(&p.ev_fork, cudaEventDisableTiming), "plan_create");
     GESPMM_CUDA(cudaEventCreateWithFlags(&p.ev_join, cudaEventDisableTiming), "plan_create");
+    GESPMM_CUDA(cudaMalloc(reinterpret_cast<void**>(&p.d_work), sizeof(uint32_t) * p.sh.slices),
+                "plan_create");
   }
+#ifdef GESPMM_EXPERIMENTAL
   if (p.o.cluster_hot > 0 && p.n == 128 && p.a.nnz) {
     // every row goes through the cluster kernel (LPT order, persistent warps)
     if (!p.d_order && m) {
@@ -444,6 +464,7 @@ gespmm_status_t build_tuned(Plan& p, const uint32_t* host_rp, cudaStream_t st) {
                                  &p.hot),
                 "plan_create");
   }
+#endif
   char buf[400];
   int len = std::snprintf(buf, sizeof buf,
                 "tuned: warp(vec=%d,lpr=%d,cf=%d) rows=%u; cta(vec=%d,warps=%d) hub_rows=%u "
@@ -454,7 +475,7 @@ gespmm_status_t build_tuned(Plan& p, const uint32_t* host_rp, cudaStream_t st) {
   if (p.d_hot && len > 0 && size_t(len) < sizeof buf)
     std::snprintf(buf + len, sizeof buf - size_t(len),
                   "; l2 hot map %.0f MB: %llu cols (gathered>=%u) = %.1f%% of gathers",
-                  double(hot_budget) / 1e6, (unsigned long long)p.hot.hot_cols, p.hot.threshold,
+                  double(p.o.l2_hot_mb) * 1.048576, (unsigned long long)p.hot.hot_cols, p.hot.threshold,
                   100.0 * p.hot.hot_nnz_frac);
   len = int(std::strlen(buf));
   if (size_t(len) < sizeof buf)
@@ -576,6 +597,7 @@ gespmm_status_t plan_execute_impl(Plan& p, const float* b, float* c, int32_t* ar
     return GESPMM_OK;
   }
   args.ld = args.ldb = p.n;
+#ifdef GESPMM_EXPERIMENTAL
   if (p.ch.col_ind && aligned(b, 16) && aligned(c, 16) && (!arg || aligned(arg, 16))) {
     args.order = p.d_order;
     args.n_sched = p.a.n_rows;
@@ -585,6 +607,7 @@ gespmm_status_t plan_execute_impl(Plan& p, const float* b, float* c, int32_t* ar
     GESPMM_CUDA(launch_cluster_warp(p.ch, p.op, fast, args, st, &clusters), "spmm");
     return GESPMM_OK;
   }
+#endif
   cudaAccessPolicyWindow win{};
   const cudaAccessPolicyWindow* winp = nullptr;
   if (p.o.l2_persist == 2) persist_limits(p.device);  // set-aside only, no window
@@ -601,12 +624,15 @@ gespmm_status_t plan_execute_impl(Plan& p, const float* b, float* c, int32_t* ar
     }
   }
   return launch_tuned_rows(p.sh, p.op, fast, args, p.d_order, p.n_hub, p.a.n_rows - p.n_hub, st,
-                           p.side, p.ev_fork, p.ev_join, winp, p.hub_pdl);
+                           p.side, p.ev_fork, p.ev_join, winp, p.hub_pdl, p.d_work);
 }
 
 // Small LRU of plans for the plan-less device entry point: keyed by the CSR
-// arrays, shape, op and options.  A stale entry (arrays mutated in place)
-// can only cost speed: every schedule covers every row exactly once.
+// arrays, shape, op and options.  A cached plan keeps only a row schedule
+// derived from row_ptr, and every schedule covers every row exactly once, so
+// a stale entry (row_ptr mutated in place, or a new CSR at a recycled address)
+// can only cost speed.  Plans that snapshot col_ind (cluster_hot's remapped
+// copy) are never cached: the call builds and drops one each time.
 struct CacheEntry {
   gespmm_csr_t a;
   uint32_t n;
@@ -651,9 +677,9 @@ struct Workspace {
   cudaEvent_t ev_b = nullptr, ev_in[kMaxChunks] = {}, ev_done[kMaxChunks] = {};
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   // device: row_ptr, col_ind, vals, B, C, arg, order, validation scratch +
-  // row-start bitmap, packed codes, packed exceptions, scan temp
-  void* buf[11] = {};
-  size_t cap[11] = {};
+  // row-start bitmap, packed codes, packed exceptions, scan temp, hub counters
+  void* buf[12] = {};
+  size_t cap[12] = {};
   // pinned host staging: packed codes, packed exceptions, row schedule
   void* hbuf[3] = {};
   size_t hcap[3] = {};
@@ -787,6 +813,14 @@ const char* gespmm_last_error(void) { return t_err.c_str(); }
 
 int32_t gespmm_abi_version(void) { return GESPMM_ABI_VERSION; }
 
+int32_t gespmm_build_flags(void) {
+#ifdef GESPMM_EXPERIMENTAL
+  return GESPMM_BUILD_EXPERIMENTAL;
+#else
+  return 0;
+#endif
+}
+
 uint64_t gespmm_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
 
 gespmm_status_t gespmm_validate_device(const gespmm_csr_t* a, void* stream) {
@@ -862,7 +896,11 @@ int32_t gespmm_plan_launches(gespmm_plan_t plan) {
   const Plan* p = reinterpret_cast<Plan*>(plan);
   if (p->a.n_rows == 0) return 0;
   if (p->o.variant != GESPMM_VARIANT_TUNED) return 1;
-  return (p->n_hub ? 1 : 0) + (p->a.n_rows > p->n_hub ? 1 : 0);
+  // the same branches as plan_execute_impl / launch_tuned_rows: one cluster
+  // launch, or per column slice a hub launch and a warp launch
+  if (p->ch.col_ind) return 1;
+  const int32_t per_slice = (p->n_hub ? 1 : 0) + (p->a.n_rows > p->n_hub ? 1 : 0);
+  return per_slice * int32_t(p->sh.slices);
 }
 
 void gespmm_plan_destroy(gespmm_plan_t plan) { delete reinterpret_cast<Plan*>(plan); }
@@ -885,6 +923,15 @@ gespmm_status_t gespmm_spmm_device(const gespmm_csr_t* a, const float* b, uint32
   if (a->n_rows == 0) return GESPMM_OK;
   if (n == 0) return fail(GESPMM_EINVAL, "native_spmm: N must be >= 1");
   o.validate = 0;  // not part of the plan identity
+  if (o.cluster_hot > 0) {  // snapshots col_ind: a fresh plan per call, never cached
+    Plan* fresh = nullptr;
+    s = plan_create_impl(a, n, op, &o, st, nullptr, &fresh);
+    if (s != GESPMM_OK) return s;
+    std::unique_ptr<Plan> own(fresh);
+    s = plan_execute_impl(*own, b, c, arg, st);
+    if (s == GESPMM_OK) GESPMM_CUDA(cudaStreamSynchronize(st), "spmm");  // before the free
+    return s;
+  }
   Plan* p = cached_plan(a, n, op, o, st, nullptr, &s);
   if (!p) return s;
   return plan_execute_impl(*p, b, c, arg, st);
@@ -1005,10 +1052,13 @@ gespmm_status_t gespmm_spmm_host(const gespmm_csr_t* a, const float* b, uint32_t
   uint32_t hub_count[kMaxChunks] = {};
   uint64_t hub_nnz[kMaxChunks] = {};
   TunedShapes shapes;
+  uint32_t* d_work = nullptr;  // hub kernel counters: one per (block, column slice)
   if (tuned) {
     int dev = 0;
     GESPMM_CUDA(cudaGetDevice(&dev), "spmm");
     shapes = make_shapes(o, a->n_cols, n, dev, m ? double(nnz) / double(m) : 0.0);
+    GESPMM_CUDA(ws->reserve(11, sizeof(uint32_t) * size_t(kMaxChunks) * shapes.slices), "spmm");
+    d_work = static_cast<uint32_t*>(ws->buf[11]);
     const int32_t ht = o.hub_threshold;
     uint32_t maxd = 0;
     for (uint64_t r = 0; r < m; ++r) maxd = std::max(maxd, a->row_ptr[r + 1] - a->row_ptr[r]);
@@ -1153,7 +1203,8 @@ gespmm_status_t gespmm_spmm_host(const gespmm_csr_t* a, const float* b, uint32_t
         const uint32_t nh = hub_count[ch];
         const bool pdl = double(hub_nnz[ch]) >= kHubPdlShare * double(pe - ps);
         s = launch_tuned_rows(shapes, op, fast, args, d_order + lo, nh, hi - lo - nh, ws->stream,
-                              ws->side, ws->ev_fork, ws->ev_join, nullptr, pdl);
+                              ws->side, ws->ev_fork, ws->ev_join, nullptr, pdl,
+                              d_work + size_t(ch) * shapes.slices);
         if (s != GESPMM_OK) return s;
       }
     }

@@ -402,7 +402,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_cta(SpmmArgs a) {
 #pragma unroll
       for (int u = 0; u < U; ++u) kv[u] = s_kv[buf][kk + u];
       // unpredicated gathers (slots past the chunk re-read the batch's first
-      // row, lanes past N read column 0): predicated loads let ptxas interleave
+      // row, lanes past N re-read the row's last vector, bsafe): predicated loads let ptxas interleave
       // them with the folds, and the U loads in flight collapse to ~1
       Vec<VEC> bv[U];
 #pragma unroll
@@ -781,16 +781,18 @@ cudaError_t cta_dispatch(const CtaShape& s, const SpmmArgs& a, cudaStream_t st) 
   return cudaErrorInvalidValue;
 }
 
-// Persistent hub launches pull units from a per-launch counter: a ring of
-// counters per device, zeroed on the launch's stream right before it.
+// Persistent hub launches pull units from a counter zeroed on the launch's
+// stream right before it.  Plans and the host entry's workspace own their
+// counters (SpmmArgs::work, one per launch site), so a captured graph or a
+// second stream never shares one; only a caller without one (none in the
+// library today) falls back to this per-device ring.
 struct HubCounters {
   uint32_t* d = nullptr;
   std::atomic<uint32_t> next{0};
-  int sms = 0;
 };
 constexpr uint32_t kHubCounterRing = 256;
 
-cudaError_t hub_counter(uint32_t** out, int* sms, cudaStream_t st) {
+cudaError_t hub_counter(uint32_t** out, cudaStream_t st) {
   static std::mutex mu;
   static HubCounters per_dev[64];
   int dev = 0;
@@ -800,16 +802,40 @@ cudaError_t hub_counter(uint32_t** out, int* sms, cudaStream_t st) {
   HubCounters& h = per_dev[dev];
   {
     std::lock_guard<std::mutex> lk(mu);
-    if (!h.d) {
-      if ((e = cudaMalloc(reinterpret_cast<void**>(&h.d), sizeof(uint32_t) * kHubCounterRing)) != cudaSuccess)
-        return e;
-      cudaDeviceGetAttribute(&h.sms, cudaDevAttrMultiProcessorCount, dev);
-    }
+    if (!h.d &&
+        (e = cudaMalloc(reinterpret_cast<void**>(&h.d), sizeof(uint32_t) * kHubCounterRing)) !=
+            cudaSuccess)
+      return e;
   }
   uint32_t* c = h.d + (h.next.fetch_add(1) % kHubCounterRing);
-  *sms = h.sms;
   *out = c;
   return cudaMemsetAsync(c, 0, sizeof(uint32_t), st);
+}
+
+int sm_count_of_current_device() {
+  static std::mutex mu;
+  static int sms[64] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 148;
+  std::lock_guard<std::mutex> lk(mu);
+  if (!sms[dev]) cudaDeviceGetAttribute(&sms[dev], cudaDevAttrMultiProcessorCount, dev);
+  return sms[dev] > 0 ? sms[dev] : 148;
+}
+
+// cudaFuncSetAttribute once per (kernel instance, device); not stream-ordered,
+// so concurrent first calls from two host threads are serialised.
+template <typename K>
+cudaError_t set_smem_once(K kernel, size_t bytes, bool* done) {
+  static std::mutex mu;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+  std::lock_guard<std::mutex> lk(mu);
+  if (done[dev]) return cudaSuccess;
+  e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes));
+  if (e == cudaSuccess) done[dev] = true;
+  return e;
 }
 
 template <int OP, bool FAST>
@@ -825,25 +851,20 @@ cudaError_t hub_dispatch(int vec, int cons, bool big, const SpmmArgs& a0, cudaSt
     return e ? std::atoi(e) : 2;
   }();
   uint64_t blocks = units;
-  a.work = nullptr;
   if (per_sm > 0) {
-    int sms = 0;
-    const cudaError_t ec = hub_counter(&a.work, &sms, st);
+    const cudaError_t ec = a0.work ? cudaMemsetAsync(a.work, 0, sizeof(uint32_t), st)
+                                   : hub_counter(&a.work, st);
     if (ec != cudaSuccess) return ec;
-    blocks = std::min<uint64_t>(units, uint64_t(per_sm) * uint64_t(sms > 0 ? sms : 148));
+    blocks = std::min<uint64_t>(units, uint64_t(per_sm) * uint64_t(sm_count_of_current_device()));
+  } else {
+    a.work = nullptr;
   }
 #define GESPMM_H(V, BIG, C)                                                                \
   if (vec == V && big == BIG && cons == C) {                                               \
     const size_t sm = hub_smem_bytes<V, BIG, C>();                                         \
-    static bool attr_done[64] = {}; /* once per device: the call is not stream-ordered */   \
-    int dev_ = 0;                                                                          \
-    cudaGetDevice(&dev_);                                                                  \
-    if (dev_ < 0 || dev_ >= 64 || !attr_done[dev_]) {                                      \
-      const cudaError_t e0 = cudaFuncSetAttribute(                                         \
-          k_hub<OP, FAST, V, BIG, C>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)); \
-      if (e0 != cudaSuccess) return e0;                                                    \
-      if (dev_ >= 0 && dev_ < 64) attr_done[dev_] = true;                                  \
-    }                                                                                      \
+    static bool attr_done[64] = {};                                                        \
+    const cudaError_t e0 = set_smem_once(k_hub<OP, FAST, V, BIG, C>, sm, attr_done);       \
+    if (e0 != cudaSuccess) return e0;                                                      \
     k_hub<OP, FAST, V, BIG, C><<<dim3(uint32_t(blocks)), dim3(32 * (C + kHubProducers)), sm, st>>>(a); \
     note_launch();                                                                         \
     return cudaGetLastError();                                                             \

@@ -15,6 +15,21 @@ GOLDEN_DIR = os.path.join(ROOT, "tests", "golden")
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA device (B200); run with -m gpu")
     config.addinivalue_line("markers", "slow: long-running (large shapes)")
+    config.addinivalue_line("markers", "experimental: exercises the GESPMM_EXPERIMENTAL build's "
+                                       "options (skipped on the default library)")
+
+
+def experimental_built() -> bool:
+    import paper_2007_03179_b200._lib as L
+    return L.experimental_built()
+
+
+def requires_experimental(fn):
+    """Tests of options compiled only into libgespmm_exp.so; the default
+    suite runs them through test_gpu_parity::test_experimental_build_suite."""
+    fn = pytest.mark.experimental(fn)
+    return pytest.mark.skipif("not __import__('conftest').experimental_built()",
+                              reason="default build: experimental options not compiled")(fn)
 
 
 @pytest.fixture(scope="session")

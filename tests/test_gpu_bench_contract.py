@@ -52,3 +52,35 @@ def test_reference_arm_line_contract():
     assert d["impl"] == "reference" and d["value"] > 0
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
     assert d["cpu_baseline"]["kind"] in ("reference", "port")
+
+
+def test_bench_gpus2_launches_two_ranks_and_matches_oracle(tmp_path):
+    """`bench.py --gpus 2` outside torchrun starts two ranks itself (gloo here:
+    the box has one GPU, both ranks share it); the line reports n_gpus 2, the
+    one-time B broadcast apart from the step, and the two C shards together
+    are bit-identical to the oracle on the whole matrix."""
+    import numpy as np
+    import oracle as O
+    env = dict(os.environ, GESPMM_DIST_BACKEND="gloo")
+    env.pop("WORLD_SIZE", None)
+    dump = str(tmp_path / "c")
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2",
+                          "--config", "pubmed", "--steps", "3", "--warmup", "3", "--no-cpu",
+                          "--dump-c", dump], cwd=ROOT, capture_output=True, text=True,
+                         timeout=900, env=env)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.strip().startswith("{")]
+    assert len(lines) == 1, out.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["config"]["parallelism"] == "row-shard x2"
+    assert d["setup"]["b_broadcast_bytes"] == 19717 * 128 * 4 and d["setup"]["backend"] == "gloo"
+    bounds = json.load(open(dump + ".bounds.json"))["bounds"]
+    assert len(bounds) == 3 and bounds[0] == 0 and bounds[-1] == 19717
+    got = np.concatenate([np.load(f"{dump}.rank{r}.npy") for r in range(2)])
+    rp, ci, v = O.ref_gen_uniform(19717, 88648, 1)
+    v = np.ascontiguousarray(v, np.float32)
+    O.randomize_values(v, 2)
+    b = O.make_random_dense(19717, 128, 42)
+    want, _ = O.spmm(19717, 19717, rp, ci, v, b, "sum")
+    assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
+

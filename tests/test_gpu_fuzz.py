@@ -12,9 +12,12 @@ from hypothesis import strategies as st
 
 import oracle as O
 import paper_2007_03179_b200 as G
-from conftest import first_divergence
+from conftest import experimental_built, first_divergence
 
 pytestmark = pytest.mark.gpu
+# the option fuzzers also run against libgespmm_exp.so
+# (test_gpu_parity::test_experimental_build_suite), drawing its options there
+EXPERIMENTAL = experimental_built()
 
 
 def _matrix(rng, m, k, density, long_row):
@@ -37,6 +40,7 @@ VARIANTS = [G.KernelVariant.tuned(), G.KernelVariant.naive(), G.KernelVariant.cr
             G.KernelVariant.crc_cwm(2), G.KernelVariant.crc_cwm(4), G.KernelVariant.crc_cwm(8)]
 
 
+@pytest.mark.experimental
 @seed(20261017)
 @settings(max_examples=int(os.environ.get("FUZZ_EXAMPLES", "60")), deadline=None, suppress_health_check=[HealthCheck.too_slow])
 @given(m=st.integers(0, 300), k=st.integers(1, 400), density=st.floats(0.0, 0.3),
@@ -47,6 +51,8 @@ VARIANTS = [G.KernelVariant.tuned(), G.KernelVariant.naive(), G.KernelVariant.cr
        data=st.integers(0, 1 << 30))
 def test_random_shapes_every_path_bit_exact(m, k, density, long_row, n, op, column_arg, vi, hub,
                                             rpw, slices, pack, data):
+    if not EXPERIMENTAL:
+        slices = min(slices, 1)
     if os.environ.get("FUZZ_LOG"):  # a CUDA fault poisons the context: log before running
         with open(os.environ["FUZZ_LOG"], "a") as f:
             f.write(repr(dict(m=m, k=k, density=density, long_row=long_row, n=n, op=op,
@@ -74,6 +80,7 @@ def test_random_shapes_every_path_bit_exact(m, k, density, long_row, n, op, colu
         assert np.array_equal(arg, warg)
 
 
+@pytest.mark.experimental
 @seed(20261018)
 @settings(max_examples=int(os.environ.get("FUZZ_EXAMPLES", "60")), deadline=None,
           suppress_health_check=[HealthCheck.too_slow])
@@ -92,6 +99,8 @@ def test_random_device_plans_bit_exact(m, k, density, long_row, n, op, column_ar
     off 16-byte alignment (scalar fallbacks); the cluster-DSMEM cache at N=128;
     fast mode (FFMA) for sum/mean within the documented tolerance."""
     import torch
+    if not EXPERIMENTAL:
+        slices, hot, cluster = min(slices, 1), 0, 0
     if cluster and n != 128:
         n = 128
     if os.environ.get("FUZZ_LOG"):

@@ -9,7 +9,7 @@ import pytest
 
 import oracle as O
 import paper_2007_03179_b200 as G
-from conftest import bits, first_divergence
+from conftest import bits, first_divergence, requires_experimental
 
 pytestmark = pytest.mark.gpu
 
@@ -303,6 +303,7 @@ def test_device_api_plans_and_unaligned_views(cuda):
     assert first_divergence(c.cpu().numpy(), want) is None
 
 
+@requires_experimental
 @pytest.mark.parametrize("n", [64, 128, 256])
 def test_hot_column_map_keeps_bits(n, cuda):
     """The frequency-aware L2 map only changes cache hints: forced on (tiny
@@ -400,6 +401,7 @@ def test_products_scale_max_arg_sampled_rows(cuda):
     assert np.array_equal(got_arg, mapped)
 
 
+@requires_experimental
 @pytest.mark.parametrize("slices", [2, 3, 8])
 @pytest.mark.parametrize("n", [64, 100, 256])
 def test_column_slices_keep_bits(slices, n, cuda):
@@ -493,6 +495,7 @@ def test_fault_injection_through_hub_kernels(n, cuda):
     assert first_divergence(c.data, faulty) is None
 
 
+@requires_experimental
 @pytest.mark.parametrize("cs", [2, 8, 16])
 @pytest.mark.parametrize("op", OPS)
 def test_cluster_dsmem_hot_rows_keep_bits(cs, op, cuda):
@@ -694,3 +697,54 @@ def test_reddit_scale_hub_threshold_by_width(cuda):
         for p in range(lo, hi):  # ordered fold v*b then add, as the reference
             want = (want + np.float32(a.vals[p]) * b.data[a.col_ind[p]]).astype(np.float32)
         assert np.array_equal(got[r], want), int(r)
+
+
+def test_plan_and_spmm_refuse_bad_operands(cuda):
+    """Raw pointers reach the kernels only for tensors of exactly the plan's
+    shape, dtype, device and layout (no silent out-of-bounds writes)."""
+    import torch
+    a = G.gen_powerlaw(500, 8000, 400, 1.0, 3)
+    G.randomize_values(a, 4)
+    d = G.DeviceCsr.from_host(a, cuda)
+    p = G.Plan(d, 64, "max")
+    b = torch.zeros((500, 64), device=cuda)
+    c = torch.empty((500, 64), device=cuda)
+    arg = torch.empty((500, 64), dtype=torch.int32, device=cuda)
+    p.execute(b, c, arg)
+    bad = [
+        (torch.zeros((500, 128), device=cuda)[:, :64], c, arg),      # non-contiguous B
+        (torch.zeros((499, 64), device=cuda), c, arg),              # short B
+        (b, torch.empty((499, 64), device=cuda), arg),              # short C
+        (b, torch.empty((500, 64), dtype=torch.float64, device=cuda), arg),
+        (b, c, torch.empty((500, 64), dtype=torch.int64, device=cuda)),
+        (b.cpu(), c, arg),
+    ]
+    for bb, cc, aa in bad:
+        with pytest.raises(G.Error):
+            p.execute(bb, cc, aa)
+    with pytest.raises(G.Error):
+        G.spmm(d, b, "sum", out=torch.empty((10, 64), device=cuda))
+    p.close()
+
+
+@pytest.mark.slow
+def test_experimental_build_suite(cuda):
+    """The measured-slower options ship only in libgespmm_exp.so: run their
+    parity tests (and the option fuzzers) against that build in a subprocess."""
+    import os
+    import subprocess
+    import sys
+    import paper_2007_03179_b200._lib as L
+    exp = os.path.join(os.path.dirname(L.__file__), "libgespmm_exp.so")
+    if L.experimental_built():
+        pytest.skip("this process already runs the experimental build")
+    if not os.path.exists(exp):
+        pytest.skip("libgespmm_exp.so not built")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, GESPMM_EXPERIMENTAL="1", FUZZ_EXAMPLES="25")
+    out = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m",
+                          "gpu and experimental", "tests/test_gpu_parity.py",
+                          "tests/test_gpu_fuzz.py", "tests/test_gpu_peer.py"],
+                         cwd=root, env=env, capture_output=True, text=True, timeout=1500)
+    assert out.returncode == 0, out.stdout[-3000:] + out.stderr[-2000:]
+    assert " passed" in out.stdout

@@ -184,3 +184,29 @@ def test_powerlaw_sample_against_dense_oracle():
             acc = (acc + (a.vals[p] * b.data[a.col_ind[p]]).astype(np.float32)).astype(np.float32)
         want[i] = acc
     assert first_divergence(got, want) is None
+
+
+@pytest.mark.parametrize("shape", [(2000, 60000, 1500, 7), (50000, 2_000_000, 5000, 1),
+                                   (2449, 123_718, 1748, 1), (3, 4, 2, 5)])
+def test_powerlaw_restatement_matches_product(shape):
+    """The oracle's C restatement of the power-law generator (the reference arm's
+    input builder) is bit-identical to the product's gespmm_gen_powerlaw."""
+    rows, nnz, maxdeg, seed = shape
+    rp, ci, v = O.gen_powerlaw(rows, nnz, maxdeg, 1.0, seed)
+    a = G.gen_powerlaw(rows, nnz, maxdeg, 1.0, seed)
+    assert np.array_equal(rp, a.row_ptr) and np.array_equal(ci, a.col_ind)
+    assert np.array_equal(v, a.vals)
+    assert int(rp[-1]) == nnz
+
+
+def test_value_and_dense_restatements_match_reference():
+    if not O.ref_available():
+        pytest.skip("oracle/_ref not built")
+    for n, seed in ((0, 1), (1, 2), (1000, 2), (99991, 123456789)):
+        v = np.zeros(n, np.float32)
+        O.randomize_values(v, seed)
+        assert np.array_equal(v.view(np.uint32), O.ref_randomize_values(np.zeros(n), seed)
+                              .view(np.uint32))
+    for r, c, seed in ((1, 1, 42), (300, 17, 42), (64, 128, 7)):
+        assert np.array_equal(O.make_random_dense(r, c, seed).view(np.uint32),
+                              O.ref_make_random_dense(r, c, seed).view(np.uint32))
