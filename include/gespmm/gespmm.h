@@ -256,6 +256,35 @@ gespmm_status_t gespmm_csr1_load_device(const char* path, uint32_t* d_row_ptr,
                                         uint32_t* d_col_ind, float* d_vals, int32_t validate,
                                         void* stream);
 
+/* ---- host data model: COO ingestion, full canonical report, Matrix Market -- */
+
+/* from_coo (csr.hpp:37-93): (row, col)-ordered canonical CSR from COO triples;
+ * duplicates collapse in input order — SUM: v = v + next, LAST: the final one.
+ * row_ptr has n_rows + 1 entries; col_ind / out_vals have room for `count`;
+ * *nnz receives the canonical length.  EINVAL with the reference's text
+ * ("coo entry (r, c, v) outside declared RxC bounds") on a bad triple. */
+typedef enum { GESPMM_DEDUP_SUM = 0, GESPMM_DEDUP_LAST = 1 } gespmm_dedup_t;
+gespmm_status_t gespmm_from_coo(uint32_t n_rows, uint32_t n_cols, uint64_t count,
+                                const uint32_t* rows, const uint32_t* cols, const float* vals,
+                                int32_t policy, uint32_t* row_ptr, uint32_t* col_ind,
+                                float* out_vals, uint64_t* nnz);
+
+/* validate (csr.hpp:107-153) on host arrays of the given lengths: returns the
+ * number of violations and writes their messages, '\n'-separated, in the
+ * reference's order and wording into msgs (truncated to msgs_cap; the full
+ * size incl. the terminator in *msgs_needed). */
+uint64_t gespmm_validate_host(const gespmm_csr_t* a, uint64_t row_ptr_len, uint64_t col_ind_len,
+                              uint64_t vals_len, char* msgs, uint64_t msgs_cap,
+                              uint64_t* msgs_needed);
+
+/* parse_matrix_market (matrix_market.hpp:60-160): coordinate real / integer /
+ * pattern, general / symmetric (mirrored off the diagonal), 1-based indices.
+ * Two calls: rows == NULL sizes (*n_entries = stored triples), then with
+ * arrays of *n_entries.  EINVAL with "matrix market: line L: ..." on error. */
+gespmm_status_t gespmm_mtx_parse(const char* text, uint64_t len, uint32_t* n_rows,
+                                 uint32_t* n_cols, uint64_t* n_entries, uint32_t* rows,
+                                 uint32_t* cols, float* vals);
+
 /* ---- checks and helpers -------------------------------------------------- */
 
 /* Device canonical-CSR check (csr.hpp:112-153); status ENONCANON with the

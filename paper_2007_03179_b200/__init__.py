@@ -10,8 +10,9 @@ from .api import (  # noqa: F401
     check_config, check_dense_valid, checksum, device_info, from_coo, gen_powerlaw,
     gen_uniform_random, make_random_dense, native_spmm, native_spmm_arg, ops,
     randomize_values, reduce_op_by_name, select_variant, spmm, variant_by_name,
-    save_csr_cache, read_csr_cache, load_matrix,
+    save_csr_cache, read_csr_cache, load_matrix, to_coo, ValidationReport, validate,
+    require_canonical, parse_matrix_market,
 )
-from ._lib import LIB_PATH, launch_count  # noqa: F401
+from ._lib import LIB_PATH, experimental_built, launch_count  # noqa: F401
 
 __version__ = "0.1.0"

@@ -34,7 +34,7 @@ CU_SOURCES = ["api.cu", "validate.cu", "kernels_faithful.cu", "kernels_tuned.cu"
 EXPERIMENTAL_CU = ["hotcols.cu", "cluster.cu"]
 LIB_EXP = os.path.join(PKG, "libgespmm_exp.so")
 BUILD_EXP = os.path.join(ROOT, "build", "gespmm_exp")
-CXX_SOURCES = ["gen.cpp", "io.cpp", "h2dpack_host.cpp"]
+CXX_SOURCES = ["gen.cpp", "io.cpp", "h2dpack_host.cpp", "host_api.cpp"]
 HEADERS = ["common.cuh", "launch.h"]
 
 

@@ -44,7 +44,8 @@ EXPORTS = [
     "gespmm_diag_gather_hub", "gespmm_diag_gather_mode", "gespmm_plan_execute_gather",
     "gespmm_peer_barrier", "gespmm_peer_alloc", "gespmm_peer_free", "gespmm_ipc_get_handle",
     "gespmm_ipc_open_handle", "gespmm_ipc_close", "gespmm_multicast_alloc",
-    "gespmm_multicast_free", "gespmm_build_flags",
+    "gespmm_multicast_free", "gespmm_build_flags", "gespmm_from_coo", "gespmm_validate_host",
+    "gespmm_mtx_parse",
 ]
 BUILD_EXPERIMENTAL = 1
 MAX_GATHER_DSTS = 8
@@ -137,6 +138,15 @@ def lib():
         L.gespmm_gen_powerlaw.restype = C.c_int
         L.gespmm_abi_version.argtypes = []
         L.gespmm_abi_version.restype = i32
+        L.gespmm_from_coo.argtypes = [u32, u32, u64, vp, vp, vp, i32, vp, vp, vp,
+                                      C.POINTER(u64)]
+        L.gespmm_from_coo.restype = C.c_int
+        L.gespmm_validate_host.argtypes = [C.POINTER(Csr), u64, u64, u64, C.c_char_p, u64,
+                                           C.POINTER(u64)]
+        L.gespmm_validate_host.restype = u64
+        L.gespmm_mtx_parse.argtypes = [C.c_char_p, u64, C.POINTER(u32), C.POINTER(u32),
+                                       C.POINTER(u64), vp, vp, vp]
+        L.gespmm_mtx_parse.restype = C.c_int
         L.gespmm_build_flags.argtypes = []
         L.gespmm_build_flags.restype = i32
         L.gespmm_device_info.argtypes = [C.POINTER(i32), C.POINTER(C.c_int64),

@@ -29,7 +29,7 @@ import ctypes as C
 import dataclasses
 import enum
 import time
-from typing import Optional, Tuple
+from typing import List, Optional, Tuple
 
 import numpy as np
 
@@ -127,30 +127,95 @@ def check_dense_valid(m: DenseMatrix):
 
 
 def from_coo(n_rows: int, n_cols: int, entries, policy: str = "sum") -> CsrMatrix:
-    """COO triples -> canonical CSR (csr.hpp:58-93): stable sort by (row, col),
-    duplicates collapse by policy ``sum`` (input order) or ``last``."""
-    rows = np.array([e[0] for e in entries], np.int64)
-    cols = np.array([e[1] for e in entries], np.int64)
-    vals = np.array([e[2] for e in entries], np.float32)
-    for r, c, v in zip(rows, cols, vals):
-        if r >= n_rows or c >= n_cols or r < 0 or c < 0:
-            raise Error(f"coo entry ({r}, {c}, {float(v):g}) outside declared "
-                        f"{n_rows}x{n_cols} bounds")
-    order = np.lexsort((cols, rows)) if len(rows) else np.zeros(0, np.int64)
+    """COO triples -> canonical CSR (csr.hpp:58-93) through gespmm_from_coo:
+    ordered by (row, col), duplicates collapse in input order by policy
+    ``sum`` or ``last``."""
+    if policy not in ("sum", "last"):
+        raise Error(f"from_coo: unknown dedup policy '{policy}' (sum, last)")
+    if isinstance(entries, tuple) and len(entries) == 3 and hasattr(entries[0], "__len__") \
+            and not np.isscalar(entries[0]):
+        rows, cols, vals = entries
+    else:
+        ent = list(entries)
+        rows = [e[0] for e in ent]
+        cols = [e[1] for e in ent]
+        vals = [e[2] for e in ent]
+    r = np.asarray(rows, np.int64)
+    c = np.asarray(cols, np.int64)
+    if r.size and (r.min() < 0 or c.min() < 0 or r.max() > 0xffffffff or c.max() > 0xffffffff):
+        i = int(np.nonzero((r < 0) | (c < 0) | (r > 0xffffffff) | (c > 0xffffffff))[0][0])
+        raise Error(f"coo entry ({r[i]}, {c[i]}, {float(np.float32(vals[i])):g}) outside declared "
+                    f"{n_rows}x{n_cols} bounds")
+    r = np.ascontiguousarray(r, np.uint32)
+    c = np.ascontiguousarray(c, np.uint32)
+    v = np.ascontiguousarray(vals, np.float32)
+    cnt = len(r)
     rp = np.zeros(n_rows + 1, np.uint32)
-    out_c, out_v = [], []
-    i = 0
-    while i < len(order):
-        r, c, v = rows[order[i]], cols[order[i]], vals[order[i]]
-        i += 1
-        while i < len(order) and rows[order[i]] == r and cols[order[i]] == c:
-            v = np.float32(v + vals[order[i]]) if policy == "sum" else vals[order[i]]
-            i += 1
-        out_c.append(c)
-        out_v.append(v)
-        rp[r + 1] += 1
-    rp = np.cumsum(rp, dtype=np.uint64).astype(np.uint32)
-    return CsrMatrix(n_rows, n_cols, rp, np.array(out_c, np.uint32), np.array(out_v, np.float32))
+    ci = np.empty(max(cnt, 1), np.uint32)
+    vv = np.empty(max(cnt, 1), np.float32)
+    nnz = C.c_uint64()
+    _check(lib().gespmm_from_coo(n_rows, n_cols, cnt, r.ctypes.data if cnt else None,
+                                 c.ctypes.data if cnt else None, v.ctypes.data if cnt else None,
+                                 0 if policy == "sum" else 1, rp.ctypes.data, ci.ctypes.data,
+                                 vv.ctypes.data, C.byref(nnz)))
+    z = nnz.value
+    return CsrMatrix(n_rows, n_cols, rp, ci[:z].copy(), vv[:z].copy())
+
+
+def to_coo(m: CsrMatrix):
+    """CSR -> (n_rows, n_cols, [(row, col, val), ...]) in row-major order (csr.hpp:95-104)."""
+    rows = np.repeat(np.arange(m.n_rows, dtype=np.uint32), np.diff(m.row_ptr.astype(np.int64)))
+    return m.n_rows, m.n_cols, list(zip(rows.tolist(), m.col_ind.tolist(),
+                                        m.vals.astype(np.float32).tolist()))
+
+
+@dataclasses.dataclass
+class ValidationReport:
+    """csr.hpp:107-110: one message per violation, empty iff canonical."""
+    violations: List[str]
+
+    def ok(self) -> bool:
+        return not self.violations
+
+
+def validate(m: CsrMatrix) -> ValidationReport:
+    """Every canonical-CSR violation, in the reference's order and wording
+    (csr.hpp:112-153), through gespmm_validate_host."""
+    rp = np.ascontiguousarray(m.row_ptr, np.uint32)
+    ci = np.ascontiguousarray(m.col_ind, np.uint32)
+    s = Csr(m.n_rows, m.n_cols, len(ci), rp.ctypes.data if rp.size else None,
+            ci.ctypes.data if ci.size else None, None)
+    need = C.c_uint64()
+    n = lib().gespmm_validate_host(C.byref(s), rp.size, ci.size, len(m.vals), None, 0,
+                                   C.byref(need))
+    if n == 0:
+        return ValidationReport([])
+    buf = C.create_string_buffer(need.value)
+    lib().gespmm_validate_host(C.byref(s), rp.size, ci.size, len(m.vals), buf, need.value,
+                               C.byref(need))
+    return ValidationReport(buf.value.decode().split("\n"))
+
+
+def require_canonical(m: CsrMatrix, who: str) -> None:
+    """csr.hpp:155-158."""
+    rep = validate(m)
+    if not rep.ok():
+        raise Error(f"{who}: matrix is not canonical CSR: {rep.violations[0]}", _lib.ENONCANON)
+
+
+def parse_matrix_market(text) -> Tuple[int, int, list]:
+    """matrix_market.hpp:60-160 (gespmm_mtx_parse): (n_rows, n_cols, triples)."""
+    data = text.encode() if isinstance(text, str) else bytes(text)
+    rows, cols, k = C.c_uint32(), C.c_uint32(), C.c_uint64()
+    _check(lib().gespmm_mtx_parse(data, len(data), C.byref(rows), C.byref(cols), C.byref(k),
+                                  None, None, None))
+    r = np.empty(max(k.value, 1), np.uint32)
+    c = np.empty(max(k.value, 1), np.uint32)
+    v = np.empty(max(k.value, 1), np.float32)
+    _check(lib().gespmm_mtx_parse(data, len(data), C.byref(rows), C.byref(cols), C.byref(k),
+                                  r.ctypes.data, c.ctypes.data, v.ctypes.data))
+    z = k.value
+    return rows.value, cols.value, (r[:z], c[:z], v[:z])
 
 
 # ---------------------------------------------------------------------------
@@ -479,18 +544,27 @@ def read_csr_cache(path) -> CsrMatrix:
 
 
 def load_matrix(path) -> CsrMatrix:
-    """load_matrix (io.hpp:100-115) for the .csr cache: read, then the canonical
-    check with the reference's "load_matrix: matrix is not canonical CSR: ..."
-    text.  Matrix Market (.mtx) parsing is out of scope here (SURVEY.md §2 #11)."""
+    """load_matrix (io.hpp:100-115): .mtx parses Matrix Market and canonicalises
+    with duplicate summation, .csr reads the binary cache; both then get the
+    canonical check with the reference's "load_matrix: matrix is not canonical
+    CSR: ..." text."""
     import os
     ext = os.path.splitext(os.fspath(path))[1]
-    if ext == ".mtx":
-        raise Error("load_matrix: Matrix Market input is not supported by this build "
-                    "(convert to the .csr cache)", _lib.EUNSUPPORTED)
-    if ext != ".csr":
+    if ext not in (".mtx", ".csr"):
+        if not os.path.exists(path):
+            raise Error(f"cannot open '{os.fspath(path)}'")
         raise Error(f"unknown matrix extension '{ext}' (expected .mtx or .csr)")
-    m = read_csr_cache(path)
-    _host_validate(m, "load_matrix")
+    if ext == ".mtx":
+        try:
+            with open(path, "rb") as f:
+                text = f.read()
+        except OSError:
+            raise Error(f"cannot open '{os.fspath(path)}'") from None
+        rows, cols, triples = parse_matrix_market(text)
+        m = from_coo(rows, cols, triples, "sum")
+    else:
+        m = read_csr_cache(path)
+    require_canonical(m, "load_matrix")
     return m
 
 

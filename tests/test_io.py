@@ -97,6 +97,10 @@ def test_csr_cache_rejects_bad_magic_and_truncation(tmp_path):
 def test_missing_file_and_extension_dispatch(tmp_path):
     with pytest.raises(G.Error, match="cannot open"):
         G.read_csr_cache(tmp_path / "nope.csr")
+    # the reference opens the file before dispatching on the extension (io.hpp:100-113)
+    with pytest.raises(G.Error, match="cannot open"):
+        G.load_matrix(tmp_path / "x.bin")
+    (tmp_path / "x.bin").write_bytes(b"x")
     with pytest.raises(G.Error, match=r"unknown matrix extension '\.bin' \(expected \.mtx or \.csr\)"):
         G.load_matrix(tmp_path / "x.bin")
 
