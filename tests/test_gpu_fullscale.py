@@ -118,3 +118,20 @@ def test_gcn_widths_a_and_at_equal_reference(cuda, n):
         want = O.ref_native_spmm(m.n_rows, m.n_cols, m.row_ptr, m.col_ind, m.vals, x, "sum",
                                  variant, cf, 0)
         _assert_bits(got, want, f"GCN {name} N={n}")
+
+
+@needs_ref
+@pytest.mark.parametrize("op", ["sum", "max"])
+def test_cora_equals_reference_dense_oracle(cuda, op):
+    """BASELINE config 0 (Cora shape, N=16) against the reference's
+    independent brute-force oracle dense_reference (oracle.hpp:42-57: the
+    densified A folded in ascending k), every kernel variant."""
+    rp, ci, v = O.ref_gen_uniform(2708, 10556, 1)
+    a = G.CsrMatrix(2708, 2708, rp, ci, np.ascontiguousarray(v, np.float32))
+    G.randomize_values(a, 2)
+    b = G.make_random_dense(2708, 16, 42).data
+    want = O.ref_dense_reference(a.n_rows, a.n_cols, a.row_ptr, a.col_ind, a.vals, b, op)
+    for variant in (G.KernelVariant.tuned(), G.KernelVariant.naive(), G.KernelVariant.crc(),
+                    G.KernelVariant.crc_cwm(2), G.KernelVariant.crc_cwm(8)):
+        c = G.native_spmm(a, G.DenseMatrix.of(b), variant, G.reduce_op_by_name(op))
+        _assert_bits(c.data, want, f"Cora N=16 {op} {variant}")
