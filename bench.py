@@ -241,13 +241,15 @@ def hbm_peak():
 
 
 def ncu_traffic(config):
+    """(dram bytes per step, source, bound counters) of the committed ncu
+    capture of this config's kernel (profiles/ncu_<config>.json)."""
     p = os.path.join(ROOT, "profiles", f"ncu_{config}.json")
     try:
         with open(p) as f:
             d = json.load(f)
-        return d.get("dram_bytes_per_step"), d.get("source")
+        return d.get("dram_bytes_per_step"), d.get("source"), d.get("bound_counters")
     except (OSError, ValueError):
-        return None, None
+        return None, None, None
 
 
 # ---------------------------------------------------------------------------
@@ -492,7 +494,7 @@ def run_ours(args, cfg):
     my_ms = float(np.mean(per_step_ms))
     achieved = alg_bytes / (my_ms * 1e-3) / 1e9
     peak, peak_src = hbm_peak()
-    traffic, traffic_src = ncu_traffic(args.config)
+    traffic, traffic_src, bound_counters = ncu_traffic(args.config)
 
     # gather ceilings on this box, now (outside the timed region): the same
     # index stream through gespmm_diag_gather (one 512-B B row per nonzero into
@@ -624,6 +626,9 @@ def run_ours(args, cfg):
                          "unit": "GB/s", "frac": round(achieved / peak, 4),
                          "traffic": traffic, "traffic_source": traffic_src,
                          "peak_source": peak_src,
+                         # what actually binds the kernel (ncu): the L2->SM return
+                         # path and the L1 data pipe, not HBM
+                         "bound_counters": bound_counters,
                          "kernel": "gespmm tuned SpMM step (warp-row kernel k_warp; hub "
                                    "rows, if any, through k_hub alongside)",
                          "algorithmic_bytes": alg_bytes, "unique_cols": uniq,

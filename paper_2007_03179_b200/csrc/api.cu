@@ -574,6 +574,7 @@ gespmm_status_t plan_execute_impl(Plan& p, const float* b, float* c, int32_t* ar
   args.c = c;
   args.arg = arg;
   args.n = p.n;
+  args.kb = p.a.n_cols;
   args.arg_col = p.o.arg_kind == GESPMM_ARG_COLUMN;
   args.skip_tail = p.o.fault_skip_tail;
   args.hints = p.o.l2_hints;
@@ -1189,6 +1190,7 @@ gespmm_status_t gespmm_spmm_host(const gespmm_csr_t* a, const float* b, uint32_t
     args.c = d_c + uint64_t(lo) * n;
     args.arg = d_arg ? d_arg + uint64_t(lo) * n : nullptr;
     args.n = n;
+    args.kb = a->n_cols;
     args.ld = args.ldb = n;
     args.arg_col = o.arg_kind == GESPMM_ARG_COLUMN;
     args.skip_tail = o.fault_skip_tail;

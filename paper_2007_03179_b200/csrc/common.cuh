@@ -317,6 +317,7 @@ struct SpmmArgs {
   uint32_t ld;            // row stride of C and arg in elements (>= n)
   uint32_t ldb;           // row stride of B in elements (>= n): ld, or the plan's re-pitched copy
   uint32_t n_tiles;       // column tiles per row
+  uint32_t kb;            // rows of B (the gathered operand; A's n_cols), 0 = not given
   int arg_col;            // arg = col_ind[p] instead of p
   int skip_tail;
   int hints;              // 0 off, 1 B evict_last / CSR,C evict_first, 2 = 1 with cold B evict_normal

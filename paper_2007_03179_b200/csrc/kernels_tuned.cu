@@ -27,8 +27,11 @@
 #include <atomic>
 #include <cstdlib>
 #include <mutex>
+#include <string>
 #include <utility>
 #include <vector>
+
+#include <cuda.h>  // CUtensorMap (the type only; encoded through the runtime's driver entry point)
 
 #include "common.cuh"
 #include "launch.h"
@@ -684,6 +687,183 @@ k_hub(SpmmArgs a) {
   }
 }
 
+// k_hub_g4 — the same ring fed by the tensor-memory accelerator instead of
+//   LDGSTS: one producer warp, and per stage G/4 lanes each issue one
+//   cp.async.bulk.tensor.2d ... tile::gather4 (four B rows, the tile's TW
+//   columns each, straight into the stage; a tensor map over B, box {TW, 1})
+//   with mbarrier complete_tx accounting.  The staged bytes enter shared memory
+//   through the TMA unit, not the LSU pipe, and the four LDGSTS producer warps
+//   (and their per-lane address math) go away.  Columns past the slice width
+//   and rows past K are zero-filled by the unit (never folded: colok / cnt).
+//   The consumer side and with it the per-element ascending fold are k_hub's.
+template <int OP, bool FAST, int VEC, bool BIG, int C>
+__global__ void __launch_bounds__(32 * (C + 1))
+k_hub_g4(SpmmArgs a, const __grid_constant__ CUtensorMap tmap) {
+  using R = Reduce<OP>;
+  using H = HubGeom<VEC, BIG, C>;
+  constexpr int S = H::STAGES, G = H::G;
+  constexpr uint32_t OP_BYTES = 4u * uint32_t(H::ROW_BYTES);  // one gather4: 4 B slices
+  static_assert(G % 4 == 0 && G / 4 <= 32, "a stage is whole gather4 ops, one per lane");
+  extern __shared__ __align__(128) unsigned char hub_smem[];
+  float* ring = reinterpret_cast<float*>(hub_smem);                       // [S][G][TW]
+  float* s_val = reinterpret_cast<float*>(hub_smem + H::RING);            // [S*G]
+  uint32_t* s_col = reinterpret_cast<uint32_t*>(s_val + S * G);           // [S*G]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(s_col + S * G);            // full[S], empty[S]
+
+  __shared__ uint32_t s_unit;
+  if (aborted(a)) {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    return;
+  }
+  const Policies pol = args_policies(a);
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t full0 = smem_addr(bars), empty0 = smem_addr(bars + S);
+  const uint32_t n_units = a.n_sched * a.n_tiles;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < S; ++i) {
+      // full: the producer's arrive.expect_tx (+ the stage's bytes); empty:
+      // one arrival per consumer warp
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(full0 + 8 * i));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(empty0 + 8 * i), "r"(C));
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == uint32_t(C) && lane == 0)
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+
+  uint32_t gbase = 0;
+  for (uint32_t iter = 0;; ++iter) {
+    if (threadIdx.x == 0)
+      s_unit = a.work ? atomicAdd(a.work, 1u) : (iter == 0 ? blockIdx.x : 0xffffffffu);
+    __syncthreads();
+    const uint32_t unit = s_unit;
+    if (unit >= n_units) break;
+    const uint32_t sidx = unit / a.n_tiles;
+    const uint32_t tile = unit - sidx * a.n_tiles;
+    const uint32_t row = a.order ? a.order[sidx] : sidx;
+    const uint32_t start = a.row_ptr[row];
+    const uint32_t full_end = a.row_ptr[row + 1];
+    const uint32_t len = faulted_end(start, full_end, a.skip_tail) - start;
+    const uint32_t col0 = tile * uint32_t(H::TW);
+    const uint32_t tw = min(uint32_t(H::TW), a.n - col0);
+    const uint32_t groups = (len + G - 1) / G;
+
+    if (warp == uint32_t(C)) {
+      // ---- producer warp: group q's (col, val) are loaded one group ahead
+      const uint32_t* ci = a.col_ind + start;
+      const float* vs = a.vals + start;
+      uint32_t kn = 0;
+      float vn = 0.0f;
+      if (groups && lane < uint32_t(G) && lane < len) {
+        kn = ld_stream_u32(ci + lane, pol.stream);
+        vn = ld_stream_f32(vs + lane, pol.stream);
+      }
+      for (uint32_t q = 0; q < groups; ++q) {
+        const uint32_t kcur = kn;
+        const float vcur = vn;
+        const uint32_t nx = (q + 1) * uint32_t(G) + lane;
+        kn = 0;
+        vn = 0.0f;
+        if (lane < uint32_t(G) && nx < len) {
+          kn = ld_stream_u32(ci + nx, pol.stream);
+          vn = ld_stream_f32(vs + nx, pol.stream);
+        }
+        const uint32_t ga = gbase + q;
+        const uint32_t st = ga % S, round = ga / S;
+        if (round > 0) mbar_wait(empty0 + 8 * st, (round - 1) & 1u);
+        const uint32_t cnt = min(uint32_t(G), len - q * G);
+        const uint32_t e0 = st * G;
+        if (lane < cnt) {
+          s_val[e0 + lane] = vcur;
+          s_col[e0 + lane] = kcur;
+        }
+        __syncwarp();
+        // slots past the row end gather the group's first row again (never folded)
+        const uint32_t k_first = __shfl_sync(kFull, kcur, 0);
+        const uint32_t kk = lane < cnt ? kcur : k_first;
+        const uint32_t r0 = __shfl_sync(kFull, kk, int(4 * (lane & 7u) + 0));
+        const uint32_t r1 = __shfl_sync(kFull, kk, int(4 * (lane & 7u) + 1));
+        const uint32_t r2 = __shfl_sync(kFull, kk, int(4 * (lane & 7u) + 2));
+        const uint32_t r3 = __shfl_sync(kFull, kk, int(4 * (lane & 7u) + 3));
+        const uint32_t n_ops = (cnt + 3u) / 4u;
+        if (lane == 0)
+          asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(full0 + 8 * st),
+                       "r"(n_ops * OP_BYTES)
+                       : "memory");
+        __syncwarp();
+        if (lane < n_ops) {
+          const uint32_t dst = smem_addr(ring + size_t(e0 + 4 * lane) * H::TW);
+          asm volatile(
+              "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+              ".L2::cache_hint [%0], [%1, {%2, %3, %4, %5, %6}], [%7], %8;" ::"r"(dst),
+              "l"(reinterpret_cast<uint64_t>(&tmap)), "r"(col0), "r"(r0), "r"(r1), "r"(r2), "r"(r3),
+              "r"(full0 + 8 * st), "l"(pol.keep)
+              : "memory");
+        }
+      }
+    } else {
+      // ---- consumer warps (k_hub's): thread t owns columns col0 + t*VEC .. +VEC
+      const uint32_t t = threadIdx.x;
+      const bool colok = t * uint32_t(VEC) < tw;
+      float acc[VEC];
+      int32_t who[VEC];
+#pragma unroll
+      for (int e = 0; e < VEC; ++e) {
+        acc[e] = R::init();
+        who[e] = -1;
+      }
+      for (uint32_t q = 0; q < groups; ++q) {
+        const uint32_t ga = gbase + q;
+        const uint32_t st = ga % S;
+        mbar_wait(full0 + 8 * st, (ga / S) & 1u);
+        const uint32_t cnt = min(uint32_t(G), len - q * G);
+        const float* slot = ring + size_t(st) * G * H::TW + t * VEC;
+        if (colok) {
+          if (cnt == uint32_t(G)) {
+            Vec<VEC> bv[G];
+            float vv[G];
+#pragma unroll
+            for (int e = 0; e < G; ++e) {
+              bv[e] = lds_vec<VEC>(slot + e * H::TW);
+              vv[e] = s_val[st * G + e];
+            }
+#pragma unroll
+            for (int e = 0; e < G; ++e) {
+              const int32_t pos =
+                  a.arg_col ? int32_t(s_col[st * G + e]) : int32_t(start + q * G + e);
+              fold_vec<OP, FAST, VEC>(acc, who, vv[e], bv[e].x, pos);
+            }
+          } else {
+            for (uint32_t e = 0; e < cnt; ++e) {
+              const Vec<VEC> bv = lds_vec<VEC>(slot + e * H::TW);
+              const float v = s_val[st * G + e];
+              const int32_t pos =
+                  a.arg_col ? int32_t(s_col[st * G + e]) : int32_t(start + q * G + e);
+              fold_vec<OP, FAST, VEC>(acc, who, v, bv.x, pos);
+            }
+          }
+        }
+        __syncwarp();
+        if (lane == 0)
+          asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(empty0 + 8 * st) : "memory");
+      }
+      if (colok) {
+        float out[VEC];
+#pragma unroll
+        for (int e = 0; e < VEC; ++e) out[e] = finish<OP>(acc[e], full_end - start);
+        const uint64_t o = uint64_t(row) * a.ld + col0 + t * VEC;
+        st_stream<VEC>(a.c + o, out, pol.stream);
+        if (R::kHasArg && a.arg) st_stream_i32<VEC>(a.arg + o, who, pol.stream);
+        if (a.n_peer || a.c_mc) store_replicas<VEC, R::kHasArg>(a, o, out, who);
+      }
+    }
+    gbase += groups;
+    __syncthreads();
+  }
+}
+
 template <int VEC, bool BIG, int C>
 constexpr size_t hub_smem_bytes() {
   using H = HubGeom<VEC, BIG, C>;
@@ -838,6 +1018,48 @@ cudaError_t set_smem_once(K kernel, size_t bytes, bool* done) {
   return e;
 }
 
+// Hub ring feed: the LDGSTS producer warps (default) or TMA gather4
+// (GESPMM_HUB_FEED=g4).  gather4 measured at about half the LDGSTS feed's
+// rate: ~135 clk per 4-row op per SM whatever the row width, i.e. ~15 B/clk
+// per SM at 512-B slices (LDGSTS ~27); 8-way Reddit shard 0.594 vs 0.528 ms,
+// one 21,657-nonzero row 0.367 vs 0.213 ms (profiles/r2/hub_g4_ab.md).
+bool hub_feed_g4() {
+  static const bool v = [] {
+    const char* e = std::getenv("GESPMM_HUB_FEED");
+    return e && std::string(e) == "g4";
+  }();
+  return v;
+}
+
+// 2-D tensor map over B (rows of `n` floats at pitch `ldb`, kb rows) with a
+// {tw, 1} box: the gather4 source.  cuTensorMapEncodeTiled through the
+// runtime's driver entry point (no libcuda link dependency).
+bool encode_b_map(const float* b, uint32_t n, uint32_t ldb, uint32_t kb, uint32_t tw,
+                  CUtensorMap* out) {
+  using Encode = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                              const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                              const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                              CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+  static Encode enc = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      p = nullptr;
+    return reinterpret_cast<Encode>(p);
+  }();
+  if (!enc || tw == 0 || tw > 256 || (reinterpret_cast<uintptr_t>(b) & 15u) || (ldb % 4u) ||
+      n == 0 || kb == 0)
+    return false;
+  const cuuint64_t dims[2] = {n, kb};
+  const cuuint64_t strides[1] = {cuuint64_t(ldb) * 4u};
+  const cuuint32_t box[2] = {tw, 1};
+  const cuuint32_t estr[2] = {1, 1};
+  return enc(out, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(b), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 template <int OP, bool FAST>
 cudaError_t hub_dispatch(int vec, int cons, bool big, const SpmmArgs& a0, cudaStream_t st) {
   const uint64_t units = uint64_t(a0.n_sched) * a0.n_tiles;
@@ -859,13 +1081,25 @@ cudaError_t hub_dispatch(int vec, int cons, bool big, const SpmmArgs& a0, cudaSt
   } else {
     a.work = nullptr;
   }
+  // TMA gather4 feed when a tensor map over B can be encoded (B rows known,
+  // 16-byte row pitch and base: the caller's tma test)
+  CUtensorMap tmap;
+  const bool g4 = hub_feed_g4() && a.kb > 0 &&
+                  encode_b_map(a.b, a.n, a.ldb, a.kb, uint32_t(32 * cons * vec), &tmap);
 #define GESPMM_H(V, BIG, C)                                                                \
   if (vec == V && big == BIG && cons == C) {                                               \
     const size_t sm = hub_smem_bytes<V, BIG, C>();                                         \
-    static bool attr_done[64] = {};                                                        \
-    const cudaError_t e0 = set_smem_once(k_hub<OP, FAST, V, BIG, C>, sm, attr_done);       \
-    if (e0 != cudaSuccess) return e0;                                                      \
-    k_hub<OP, FAST, V, BIG, C><<<dim3(uint32_t(blocks)), dim3(32 * (C + kHubProducers)), sm, st>>>(a); \
+    if (g4) {                                                                              \
+      static bool attr_g4[64] = {};                                                        \
+      const cudaError_t e0 = set_smem_once(k_hub_g4<OP, FAST, V, BIG, C>, sm, attr_g4);    \
+      if (e0 != cudaSuccess) return e0;                                                    \
+      k_hub_g4<OP, FAST, V, BIG, C><<<dim3(uint32_t(blocks)), dim3(32 * (C + 1)), sm, st>>>(a, tmap); \
+    } else {                                                                               \
+      static bool attr_done[64] = {};                                                      \
+      const cudaError_t e0 = set_smem_once(k_hub<OP, FAST, V, BIG, C>, sm, attr_done);     \
+      if (e0 != cudaSuccess) return e0;                                                    \
+      k_hub<OP, FAST, V, BIG, C><<<dim3(uint32_t(blocks)), dim3(32 * (C + kHubProducers)), sm, st>>>(a); \
+    }                                                                                      \
     note_launch();                                                                         \
     return cudaGetLastError();                                                             \
   }
