@@ -439,7 +439,8 @@ def run_ours(args, cfg):
     ex = G.ExecOptions(hub_threshold=args.hub_threshold, exact=not args.fast,
                        l2_persist=args.l2_persist, l2_hints=hints, l2_hot_mb=args.l2_hot_mb,
                        tuned_cf=args.tuned_cf, col_slices=args.col_slices,
-                       rows_per_warp=args.rows_per_warp, cluster_hot=args.cluster_hot)
+                       rows_per_warp=args.rows_per_warp, cluster_hot=args.cluster_hot,
+                       hot_rows_mb=args.hot_rows_mb)
     variant = G.variant_by_name(args.variant, args.cf)
     plan = G.Plan(d, n, op, variant=variant, exec=ex)
     log(f"[bench] rank {rank}: rows [{info.lo},{info.hi}) nnz {shard.nnz()} plan: {plan.description}")
@@ -776,6 +777,8 @@ def main():
     p.add_argument("--no-flush", action="store_true", help="skip the L2 flush between steps")
     p.add_argument("--gcn-pad", type=int, default=0,
                    help="GCN: pad the class width to a multiple of this (default GCNConfig.pad_to)")
+    p.add_argument("--hot-rows-mb", type=int, default=0,
+                   help="relocated hot B rows budget (MB), experimental build; <=0 off")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--no-ceiling", action="store_true", help="skip the live gather-ceiling probe")

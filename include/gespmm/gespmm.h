@@ -9,7 +9,7 @@
  * Python host mirror (paper_2007_03179_b200/) are thin layers over these calls.
  *
  * Experimental options (l2_persist, l2_hot_mb > 0, col_slices > 1,
- * cluster_hot) were measured slower on B200 and are compiled only into the
+ * cluster_hot, hot_rows_mb > 0) were measured slower on B200 and are compiled only into the
  * GESPMM_EXPERIMENTAL build (gespmm_build_flags() & GESPMM_BUILD_EXPERIMENTAL);
  * the default library rejects them with GESPMM_EUNSUPPORTED.
  *
@@ -120,7 +120,16 @@ typedef struct {
   int32_t h2d_pack;   /* gespmm_spmm_host: send col_ind as 16-bit row-gap codes (lossless, escapes
                          for large gaps) and rebuild it on the device: 0 = auto (>= 8M nonzeros),
                          1 = on, -1 = off */
-  int32_t reserved[1];
+  int32_t hot_rows_mb; /* TUNED plans: relocate the most-gathered B rows (a byte budget of this
+                         many MB) into a plan-owned contiguous copy, refreshed from B at every
+                         execute, and gather them with evict_last while every other B row is
+                         gathered evict_first, so L2 holds the static top-by-frequency set
+                         instead of an LRU over B.  The plan keeps a remapped copy of col_ind (a
+                         SNAPSHOT, like cluster_hot; gespmm_spmm_device never caches such a
+                         plan).  Results are unchanged (positions and fold order are).
+                         Edge args only.  Experimental (measured slower on B200: fewer DRAM
+                         bytes, more instructions).  <=0 = off (default), >0 =
+                         budget in MB */
 } gespmm_options_t;
 
 void gespmm_options_default(gespmm_options_t* opts);

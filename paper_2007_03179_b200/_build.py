@@ -31,7 +31,7 @@ CXX_FLAGS = ["-O3", "-std=c++17", "-fPIC", "-ffp-contract=off", "-Wall", "-Wextr
 CU_SOURCES = ["api.cu", "validate.cu", "kernels_faithful.cu", "kernels_tuned.cu", "diag.cu",
               "transpose.cu", "peer.cu", "h2dpack.cu"]
 # measured slower on B200: only in the GESPMM_EXPERIMENTAL build
-EXPERIMENTAL_CU = ["hotcols.cu", "cluster.cu"]
+EXPERIMENTAL_CU = ["hotcols.cu", "cluster.cu", "hotrows.cu"]
 LIB_EXP = os.path.join(PKG, "libgespmm_exp.so")
 BUILD_EXP = os.path.join(ROOT, "build", "gespmm_exp")
 CXX_SOURCES = ["gen.cpp", "io.cpp", "h2dpack_host.cpp", "host_api.cpp"]

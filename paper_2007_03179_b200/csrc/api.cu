@@ -91,7 +91,8 @@ gespmm_status_t check_opts(const gespmm_options_t& o) {
   const char* exp_opt = o.cluster_hot ? "cluster_hot"
                         : o.l2_hot_mb > 0 ? "l2_hot_mb"
                         : o.col_slices > 1 ? "col_slices"
-                        : o.l2_persist ? "l2_persist" : nullptr;
+                        : o.l2_persist ? "l2_persist"
+                        : o.hot_rows_mb > 0 ? "hot_rows_mb" : nullptr;
   if (exp_opt)
     return fail(GESPMM_EUNSUPPORTED, std::string(exp_opt) +
                                          " is an experimental option (measured slower, DESIGN.md "
@@ -171,10 +172,14 @@ struct Plan {
   uint32_t max_degree = 0;
   double mean_degree = 0.0;
   ClusterHot ch;             // cluster-DSMEM hot-row cache (o.cluster_hot), col_ind copy
+  HotRows hr;                // relocated hot rows (o.hot_rows_mb), col_ind copy
 
   ~Plan() {
 #ifdef GESPMM_EXPERIMENTAL
     free_cluster_hot(&ch);
+#endif
+#ifdef GESPMM_EXPERIMENTAL
+    free_hot_rows(&hr);
 #endif
     if (d_order) cudaFree(d_order);
     if (d_work) cudaFree(d_work);
@@ -247,6 +252,25 @@ uint64_t hot_budget_bytes(const gespmm_options_t& o, uint32_t k, uint32_t n, int
   (void)dev;
   if (o.l2_hot_mb <= 0 || k >= 0x80000000u) return 0;  // bit 31 of a staged column is the mark
   return uint64_t(o.l2_hot_mb) << 20;
+}
+
+// Relocated hot rows (hotrows.cu): budget in bytes of B rows, 0 = off.
+// Opt-in (hot_rows_mb > 0, experimental build).  Measured on B200 (products
+// N=256 max+arg, profiles/r2/reloc_products.md): DRAM reads 71.4 -> 61.6 GB
+// per step, yet 12.3 -> 12.8-13.0 ms for every budget and L2 policy tried
+// (address-range evict_last, + evict_first outside, or one keep policy).
+// Column args would report the remapped ids, so edge args only.
+uint64_t hot_rows_budget(const gespmm_options_t& o, uint32_t k, uint32_t n, int dev) {
+  (void)n;
+  (void)dev;
+#ifndef GESPMM_EXPERIMENTAL
+  (void)o;
+  (void)k;
+  return 0;
+#else
+  if (o.hot_rows_mb <= 0 || k >= 0x80000000u || o.arg_kind == GESPMM_ARG_COLUMN) return 0;
+  return uint64_t(o.hot_rows_mb) << 20;
+#endif
 }
 
 // Column slices (slice-major traversal).  The kernels fold each output
@@ -336,11 +360,16 @@ gespmm_status_t launch_tuned_rows(const TunedShapes& t, int op, bool fast, const
       sa.arg_peer[q] = a.arg_peer[q] ? a.arg_peer[q] + off : nullptr;
     }
     sa.c_mc = a.c_mc ? a.c_mc + off : nullptr;
+    sa.b_hot = a.b_hot ? a.b_hot + off : nullptr;
     sa.arg_mc = a.arg_mc ? a.arg_mc + off : nullptr;
     sa.n = w;
     bool hub_then_pdl = false, side_used = false;
     if (n_hub) {
       SpmmArgs h = sa;
+      if (h.col_ind_orig) {  // hub kernels gather B directly through the caller's col_ind
+        h.col_ind = h.col_ind_orig;
+        h.b_hot = nullptr;
+      }
       h.order = order;
       h.n_sched = n_hub;
       h.work = work ? work + j : nullptr;  // caller-owned counter of this launch site
@@ -465,7 +494,14 @@ gespmm_status_t build_tuned(Plan& p, const uint32_t* host_rp, cudaStream_t st) {
                 "plan_create");
   }
 #endif
-  char buf[400];
+#ifdef GESPMM_EXPERIMENTAL
+  const uint64_t reloc = hot_rows_budget(p.o, p.a.n_cols, p.n, p.device);
+  if (reloc && p.a.nnz && p.n)
+    GESPMM_CUDA(build_hot_rows(p.a.col_ind, p.a.nnz, p.a.n_cols, p.n,
+                               reloc / (uint64_t(p.n) * sizeof(float)), st, &p.hr),
+                "plan_create");
+#endif
+  char buf[512];
   int len = std::snprintf(buf, sizeof buf,
                 "tuned: warp(vec=%d,lpr=%d,cf=%d) rows=%u; cta(vec=%d,warps=%d) hub_rows=%u "
                 "(deg>=%u); mean_deg=%.1f max_deg=%u",
@@ -486,6 +522,13 @@ gespmm_status_t build_tuned(Plan& p, const uint32_t* host_rp, cudaStream_t st) {
     std::snprintf(buf + len, sizeof buf - size_t(len),
                   "; cluster DSMEM cache: %u hot rows in clusters of %d = %.1f%% of gathers",
                   p.ch.n_hot, p.ch.cs, 100.0 * p.ch.hot_nnz_frac);
+    len = int(std::strlen(buf));
+  }
+  if (p.hr.n_hot && size_t(len) < sizeof buf) {
+    std::snprintf(buf + len, sizeof buf - size_t(len),
+                  "; relocated hot rows %.1f MB: %u cols (gathered>=%u) = %.1f%% of gathers",
+                  double(p.hr.n_hot) * p.hr.ldh * 4.0 / 1048576.0, p.hr.n_hot, p.hr.threshold,
+                  100.0 * p.hr.hot_nnz_frac);
     len = int(std::strlen(buf));
   }
   if (p.sh.slices > 1 && size_t(len) < sizeof buf)
@@ -624,6 +667,24 @@ gespmm_status_t plan_execute_impl(Plan& p, const float* b, float* c, int32_t* ar
       winp = &win;
     }
   }
+#ifdef GESPMM_EXPERIMENTAL
+  const float* b_hot = nullptr;
+  int32_t hot_off = 0;
+  if (p.hr.n_hot && place_hot_rows(p.hr, b, args.ldb, &b_hot, &hot_off)) {
+    // relocated hot rows: refresh the copy from this B, gather through the remap
+    GESPMM_CUDA(refresh_hot_rows(p.hr, b, args.ldb, p.n, b_hot, st), "spmm");
+    args.col_ind_orig = args.col_ind;
+    args.col_ind = p.hr.col_ind;
+    args.b_hot = b_hot;
+    args.hot_off = hot_off;
+    args.hot_bytes = uint32_t(uint64_t(p.hr.n_hot) * args.ldb * sizeof(float));
+    static const int mode = [] {
+      const char* e = std::getenv("GESPMM_RELOC_POLICY");  // A/B: 0 keep, 1 range+evict_first, 2 range
+      return e ? std::atoi(e) : 1;
+    }();
+    args.reloc_mode = mode;
+  }
+#endif
   return launch_tuned_rows(p.sh, p.op, fast, args, p.d_order, p.n_hub, p.a.n_rows - p.n_hub, st,
                            p.side, p.ev_fork, p.ev_join, winp, p.hub_pdl, p.d_work);
 }
@@ -901,7 +962,7 @@ int32_t gespmm_plan_launches(gespmm_plan_t plan) {
   // launch, or per column slice a hub launch and a warp launch
   if (p->ch.col_ind) return 1;
   const int32_t per_slice = (p->n_hub ? 1 : 0) + (p->a.n_rows > p->n_hub ? 1 : 0);
-  return per_slice * int32_t(p->sh.slices);
+  return per_slice * int32_t(p->sh.slices) + (p->hr.n_hot ? 1 : 0);  // + the hot-row refresh
 }
 
 void gespmm_plan_destroy(gespmm_plan_t plan) { delete reinterpret_cast<Plan*>(plan); }
@@ -924,7 +985,7 @@ gespmm_status_t gespmm_spmm_device(const gespmm_csr_t* a, const float* b, uint32
   if (a->n_rows == 0) return GESPMM_OK;
   if (n == 0) return fail(GESPMM_EINVAL, "native_spmm: N must be >= 1");
   o.validate = 0;  // not part of the plan identity
-  if (o.cluster_hot > 0) {  // snapshots col_ind: a fresh plan per call, never cached
+  if (o.cluster_hot > 0 || o.hot_rows_mb > 0) {  // snapshots col_ind: a fresh plan per call, never cached
     Plan* fresh = nullptr;
     s = plan_create_impl(a, n, op, &o, st, nullptr, &fresh);
     if (s != GESPMM_OK) return s;

@@ -322,6 +322,13 @@ struct SpmmArgs {
   int skip_tail;
   int hints;              // 0 off, 1 B evict_last / CSR,C evict_first, 2 = 1 with cold B evict_normal
   const uint32_t* hot;    // hot-column bitmap (nullable): cold B rows use the cold policy
+  // Relocated hot rows (nullable): the plan's contiguous copy of the most-gathered
+  // B rows (row stride ldh), addressed by col_ind entries with bit 31 set.
+  const float* b_hot;   // start of the copy (row stride ldb, congruent to b modulo the stride)
+  int32_t hot_off;      // (b_hot - b) / row stride
+  uint32_t hot_bytes;   // bytes of the copy (< 4 GiB)
+  int reloc_mode;       // L2 policy of the gathers: 1 range (copy evict_last), 0 keep for all
+  const uint32_t* col_ind_orig;  // host-side: the caller's col_ind when col_ind is the remap
   // L2 policies resolved once on the device (resolve_policies) and passed as
   // launch parameters: they then live in uniform registers, so a per-gather
   // choice between two of them is a uniform select, not a per-load descriptor

@@ -40,6 +40,14 @@ namespace gespmm {
 namespace {
 
 constexpr unsigned kFull = 0xffffffffu;
+enum : int { kHotOff = 0, kHotMap = 1, kHotReloc = 2 };  // k_warp's B-row placement modes
+// the hot-row modes were measured slower: compiled only into the
+// experimental library
+#ifdef GESPMM_EXPERIMENTAL
+constexpr bool kExpBuild = true;
+#else
+constexpr bool kExpBuild = false;
+#endif
 
 template <int N>
 struct Pack;  // staged-entry read width: N consecutive (col) or (val) words
@@ -112,6 +120,30 @@ struct WarpGeom {
                 "batch geometry");
 };
 
+// Relocated hot rows: a remapped column with bit 31 set is slot s of the plan's
+// copy, which starts hot_off rows (of B's stride) from B; the staged index
+// becomes that signed row offset, so the gather needs no select.
+__device__ __forceinline__ uint32_t reloc_index(const SpmmArgs& a, uint32_t k) {
+  return (k & 0x80000000u) ? uint32_t(int32_t(k & 0x7fffffffu) + a.hot_off) : k;
+}
+// One L2 policy for every gather: rows inside the copy evict_last, by address
+// range (createpolicy.range); the rest of B as the range's outside default
+// (GESPMM reloc_mode 1), or the select-free fractional keep (mode 0, A/B).
+__device__ __forceinline__ uint64_t reloc_policy(const SpmmArgs& a, const Policies& pol) {
+  if (a.reloc_mode == 0) return pol.keep;
+  uint64_t p;
+  const uint32_t bytes = a.hot_bytes;
+  if (a.reloc_mode == 1)
+    asm("createpolicy.range.global.L2::evict_last.L2::evict_first.b64 %0, [%1], %2, %3;"
+        : "=l"(p)
+        : "l"(a.b_hot), "r"(bytes), "r"(bytes));
+  else
+    asm("createpolicy.range.global.L2::evict_last.b64 %0, [%1], %2, %3;"
+        : "=l"(p)
+        : "l"(a.b_hot), "r"(bytes), "r"(bytes));
+  return p;
+}
+
 // Row metadata of one (sub)warp unit for this lane: the row, its CSR range,
 // and this lane's entry of the row's first staged chunk.
 struct UnitMeta {
@@ -135,7 +167,7 @@ __device__ __forceinline__ void unit_rows(const SpmmArgs& a, uint32_t group, Uni
 
 // Issues this lane's chunk-0 (col, val) loads; slots past the row end hold
 // column 0 (a valid row).
-template <int LPR, int E, bool HOT>
+template <int LPR, int E, int HOT>
 __device__ __forceinline__ void unit_chunk0(const SpmmArgs& a, const Policies& pol, UnitMeta& m) {
   const uint32_t sl = (threadIdx.x & 31) % LPR;
   const uint32_t len = faulted_end(m.start, m.full_end, a.skip_tail) - m.start;
@@ -147,7 +179,8 @@ __device__ __forceinline__ void unit_chunk0(const SpmmArgs& a, const Policies& p
     if (i < len) {
       m.k0[j] = ld_stream_u32(a.col_ind + m.start + i, pol.stream);
       m.v0[j] = ld_stream_f32(a.vals + m.start + i, pol.stream);
-      if (HOT) m.k0[j] |= cold_mark(a.hot, m.k0[j]);
+      if (HOT == kHotMap) m.k0[j] |= cold_mark(a.hot, m.k0[j]);
+      if (HOT == kHotReloc) m.k0[j] = reloc_index(a, m.k0[j]);
     }
   }
 }
@@ -155,10 +188,16 @@ __device__ __forceinline__ void unit_chunk0(const SpmmArgs& a, const Policies& p
 // One (row group, column tile) unit: Coalesced Row Caching of the row's
 // sparse segment through the per-warp double-buffered shared tile, CF column
 // sub-tiles per lane (warp merging), U gathers in flight, ordered fold.
-// HOT: the plan carries a hot-column map (bit 31 of a staged column marks a
-// cold B row, loaded with the cold policy).  Without it every gather uses one
-// policy register, so no per-load descriptor selection is emitted.
-template <int OP, bool FAST, int VEC, int LPR, int CF, bool HOT>
+// HOT = kHotMap: the plan carries a hot-column map (bit 31 of a staged column
+// marks a cold B row, loaded with the cold policy).  HOT = kHotReloc: the
+// plan relocated the most-gathered B rows into its own contiguous copy
+// (a.b_hot, refreshed every execute) and a.col_ind is its remapped copy, where
+// bit 31 marks a relocated row and the low bits are its slot; those rows are
+// gathered from the copy with evict_last, every other row from B with the cold
+// policy, so L2 keeps the static top-by-frequency set instead of LRU's.
+// HOT = kHotOff: every gather uses one policy register, so no per-load
+// descriptor selection is emitted.
+template <int OP, bool FAST, int VEC, int LPR, int CF, int HOT>
 __device__ __forceinline__ void warp_unit(const SpmmArgs& a, const Policies& pol, uint32_t tile,
                                           const UnitMeta& m, uint32_t* my_col, float* my_val) {
   using R = Reduce<OP>;
@@ -202,6 +241,8 @@ __device__ __forceinline__ void warp_unit(const SpmmArgs& a, const Policies& pol
   for (int c = 0; c < CF; ++c) all_cols = all_cols && colok[c];
   all_cols = __all_sync(kFull, all_cols);
   const uint32_t stride = a.ldb * 4u;  // bytes per B row (B < 4 GiB per row index * stride)
+  uint64_t pol_hot = pol.keep;
+  if constexpr (HOT == kHotReloc) pol_hot = reloc_policy(a, pol);
   const uint32_t* ci = a.col_ind + start;
   const float* vs = a.vals + start;
 
@@ -225,7 +266,8 @@ __device__ __forceinline__ void warp_unit(const SpmmArgs& a, const Policies& pol
       if (nxt < len) {
         kn[j] = ld_stream_u32(ci + nxt, pol.stream);
         vn[j] = ld_stream_f32(vs + nxt, pol.stream);
-        if (HOT) kn[j] |= cold_mark(a.hot, kn[j]);
+        if (HOT == kHotMap) kn[j] |= cold_mark(a.hot, kn[j]);
+        if (HOT == kHotReloc) kn[j] = reloc_index(a, kn[j]);
       }
     }
     __syncwarp();
@@ -253,7 +295,18 @@ __device__ __forceinline__ void warp_unit(const SpmmArgs& a, const Policies& pol
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         uint64_t pu = pol.keep;
-        if (HOT) {
+        if constexpr (HOT == kHotReloc) {
+          // staged index already relative to B (relocated rows: negative or
+          // past K, inside the plan's copy): signed row offset, one policy
+          // register (address-range policy: the copy evict_last)
+#pragma unroll
+          for (int c = 0; c < CF; ++c)
+            bv[u][c] = ld_keep<VEC>(reinterpret_cast<const float*>(
+                                        bbase[c] + int64_t(int32_t(k[u])) * int64_t(stride)),
+                                    pol_hot);
+          continue;
+        }
+        if (HOT == kHotMap) {
           // bit 31 of a staged column marks a cold B row (hot-column map).  With
           // one row per warp the mark is warp-uniform (vote), and with the
           // policies in launch parameters the choice is a uniform select.
@@ -310,7 +363,7 @@ __device__ __forceinline__ void warp_unit(const SpmmArgs& a, const Policies& pol
   }
 }
 
-template <int OP, bool FAST, int VEC, int LPR, int CF, bool HOT>
+template <int OP, bool FAST, int VEC, int LPR, int CF, int HOT>
 __global__ void __launch_bounds__(32 * kWarpBlock, warp_min_blocks<OP, CF, LPR>()) k_warp(SpmmArgs a) {
   // Staged sparse tile, double-buffered per warp: phase 1 writes E (col, val)
   // per lane, phase 2 reads them back with broadcast LDS of W entries — 2/W
@@ -922,14 +975,20 @@ cudaError_t warp_dispatch(const WarpShape& s, const SpmmArgs& a, cudaStream_t st
   if (blocks == 0) return cudaSuccess;
   if (blocks > 0x7fffffffull) return cudaErrorInvalidConfiguration;
   const dim3 b{32 * kWarpBlock};
+  // shapes without a hot-row mode gather B directly through the caller's col_ind
+  SpmmArgs plain = a;
+  if (plain.col_ind_orig) plain.col_ind = plain.col_ind_orig;
+  plain.b_hot = nullptr;
 #define GESPMM_W(V, L, F)                                                                    \
   if (s.vec == V && s.lpr == L && s.cf == F) {                                               \
-    constexpr bool kHotShape = L == 32; /* hot-column map on full-warp rows only */          \
+    constexpr int kMap = (kExpBuild && L == 32) ? kHotMap : kHotOff;   /* full-warp rows only */ \
+    constexpr int kReloc = (kExpBuild && L == 32) ? kHotReloc : kHotOff;                     \
     const dim3 g{uint32_t(blocks)};                                                          \
-    apply_carveout(k_warp<OP, FAST, V, L, F, false>);                                        \
+    apply_carveout(k_warp<OP, FAST, V, L, F, kHotOff>);                                      \
     const cudaError_t e =                                                                    \
-        (kHotShape && a.hot) ? launch_ex(k_warp<OP, FAST, V, L, F, kHotShape>, g, b, st, a, window, pdl) \
-                             : launch_ex(k_warp<OP, FAST, V, L, F, false>, g, b, st, a, window, pdl); \
+        (kReloc == kHotReloc && a.b_hot) ? launch_ex(k_warp<OP, FAST, V, L, F, kReloc>, g, b, st, a, window, pdl) \
+        : (kMap == kHotMap && a.hot) ? launch_ex(k_warp<OP, FAST, V, L, F, kMap>, g, b, st, a, window, pdl) \
+                             : launch_ex(k_warp<OP, FAST, V, L, F, kHotOff>, g, b, st, plain, window, pdl); \
     note_launch();                                                                           \
     return e;                                                                                \
   }

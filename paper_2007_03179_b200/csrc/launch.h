@@ -77,6 +77,30 @@ cudaError_t build_hot_bitmap(const uint32_t* col_ind, uint64_t nnz, uint32_t k,
                              uint64_t budget_rows, cudaStream_t st, uint32_t** out_bits,
                              HotStats* stats);
 
+// --- relocated hot rows (hotrows.cu) ---
+struct HotRows {
+  uint32_t* col_ind = nullptr;  // remapped col_ind: hot columns = (1 << 31) | slot (a snapshot)
+  uint32_t* list = nullptr;     // slot -> column
+  float* buf = nullptr;         // (n_hot + 1) rows of ldh floats: the copy, placed per execute
+  uint32_t n_hot = 0;
+  uint32_t ldh = 0;             // row stride of the copy = the plan's B stride
+  uint32_t threshold = 0;       // a column is hot when gathered >= threshold times
+  double hot_nnz_frac = 0.0;    // share of the gathers that hit relocated rows
+};
+// Counts the gathers per column and relocates the most-gathered ones whose rows
+// (n floats each) fit budget_rows.  Synchronises `st`.  k < 2^31.
+cudaError_t build_hot_rows(const uint32_t* col_ind, uint64_t nnz, uint32_t k, uint32_t n,
+                           uint64_t budget_rows, cudaStream_t st, HotRows* out);
+// Places the copy inside h.buf at the start congruent to b modulo the row
+// stride: b_hot = b + hot_off rows.  False when that offset does not fit int32
+// (or the copy is >= 4 GiB): the launch then gathers B directly.
+bool place_hot_rows(const HotRows& h, const float* b, uint32_t ldb, const float** b_hot,
+                    int32_t* hot_off);
+// Copies the relocated rows' first n columns of B (row stride ldb) to b_hot.
+cudaError_t refresh_hot_rows(const HotRows& h, const float* b, uint32_t ldb, uint32_t n,
+                             const float* b_hot, cudaStream_t st);
+void free_hot_rows(HotRows* h);
+
 // --- cluster-DSMEM hot-row cache (cluster.cu) ---
 struct ClusterHot {
   uint32_t* col_ind = nullptr;   // remapped col_ind: hot columns = (1 << 31) | slot

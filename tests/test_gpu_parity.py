@@ -332,6 +332,36 @@ def test_hot_column_map_keeps_bits(n, cuda):
             plan.close()
 
 
+@requires_experimental
+@pytest.mark.parametrize("n", [64, 128, 256, 130])
+def test_relocated_hot_rows_keep_bits(n, cuda):
+    """Relocated hot rows (hot_rows_mb): the plan gathers the most-gathered
+    B rows from its own copy through a remapped col_ind; positions and fold
+    order are unchanged, so every op is bit-identical to the oracle, also after
+    B moves and changes (the copy is re-placed and refreshed per execute) and
+    with hub rows (which gather B through the caller's col_ind)."""
+    import torch
+    a, b = _powerlaw(6000, 500000, 5000, 37, n)
+    d = G.DeviceCsr.from_host(a)
+    for op in OPS:
+        want_arg = op in ("max", "min")
+        plan = G.Plan(d, n, op, exec=G.ExecOptions(hot_rows_mb=1, hub_threshold=2000))
+        assert "relocated hot rows" in plan.description, plan.description
+        for seed in (0, 1):
+            bb = b.data if seed == 0 else -b.data[::-1].copy()
+            bt = torch.from_numpy(np.ascontiguousarray(bb)).to(cuda)
+            want, warg = O.spmm(a.n_rows, a.n_cols, a.row_ptr, a.col_ind, a.vals, bb, op,
+                                want_arg=want_arg)
+            c = torch.empty((a.n_rows, n), dtype=torch.float32, device=cuda)
+            arg = torch.empty((a.n_rows, n), dtype=torch.int32, device=cuda) if want_arg else None
+            plan.execute(bt, c, arg)
+            torch.cuda.synchronize()
+            assert first_divergence(c.cpu().numpy(), want) is None, (op, n, seed)
+            if want_arg:
+                assert np.array_equal(arg.cpu().numpy(), warg), (op, n, seed)
+        plan.close()
+
+
 def test_device_validate_flag(cuda):
     import torch
     a = G.gen_uniform_random(G.GraphGenSpec(100, 1000, 1))
