@@ -683,6 +683,8 @@ gespmm_status_t plan_execute_impl(Plan& p, const float* b, float* c, int32_t* ar
       return e ? std::atoi(e) : 1;
     }();
     args.reloc_mode = mode;
+    if (mode != 0)
+      GESPMM_CUDA(resolve_range_policy(b_hot, args.hot_bytes, mode, &args.pol_hot, st), "spmm");
   }
 #endif
   return launch_tuned_rows(p.sh, p.op, fast, args, p.d_order, p.n_hub, p.a.n_rows - p.n_hub, st,

@@ -328,6 +328,7 @@ struct SpmmArgs {
   int32_t hot_off;      // (b_hot - b) / row stride
   uint32_t hot_bytes;   // bytes of the copy (< 4 GiB)
   int reloc_mode;       // L2 policy of the gathers: 1 range (copy evict_last), 0 keep for all
+  uint64_t pol_hot;     // the range policy word (resolve_range_policy)
   const uint32_t* col_ind_orig;  // host-side: the caller's col_ind when col_ind is the remap
   // L2 policies resolved once on the device (resolve_policies) and passed as
   // launch parameters: they then live in uniform registers, so a per-gather

@@ -26,7 +26,9 @@
 #include <algorithm>
 #include <atomic>
 #include <cstdlib>
+#include <map>
 #include <mutex>
+#include <tuple>
 #include <string>
 #include <utility>
 #include <vector>
@@ -126,22 +128,11 @@ struct WarpGeom {
 __device__ __forceinline__ uint32_t reloc_index(const SpmmArgs& a, uint32_t k) {
   return (k & 0x80000000u) ? uint32_t(int32_t(k & 0x7fffffffu) + a.hot_off) : k;
 }
-// One L2 policy for every gather: rows inside the copy evict_last, by address
-// range (createpolicy.range); the rest of B as the range's outside default
-// (GESPMM reloc_mode 1), or the select-free fractional keep (mode 0, A/B).
+// One L2 policy for every gather, from the launch parameters (a uniform
+// register, no per-load move): the address-range policy resolved on the host
+// side (resolve_range_policy), or the fractional keep (reloc_mode 0, A/B).
 __device__ __forceinline__ uint64_t reloc_policy(const SpmmArgs& a, const Policies& pol) {
-  if (a.reloc_mode == 0) return pol.keep;
-  uint64_t p;
-  const uint32_t bytes = a.hot_bytes;
-  if (a.reloc_mode == 1)
-    asm("createpolicy.range.global.L2::evict_last.L2::evict_first.b64 %0, [%1], %2, %3;"
-        : "=l"(p)
-        : "l"(a.b_hot), "r"(bytes), "r"(bytes));
-  else
-    asm("createpolicy.range.global.L2::evict_last.b64 %0, [%1], %2, %3;"
-        : "=l"(p)
-        : "l"(a.b_hot), "r"(bytes), "r"(bytes));
-  return p;
+  return a.reloc_mode == 0 ? pol.keep : a.pol_hot;
 }
 
 // Row metadata of one (sub)warp unit for this lane: the row, its CSR range,
@@ -302,7 +293,7 @@ __device__ __forceinline__ void warp_unit(const SpmmArgs& a, const Policies& pol
 #pragma unroll
           for (int c = 0; c < CF; ++c)
             bv[u][c] = ld_keep<VEC>(reinterpret_cast<const float*>(
-                                        bbase[c] + int64_t(int32_t(k[u])) * int64_t(stride)),
+                                        bbase[c] + int64_t(int32_t(k[u])) * int32_t(stride)),
                                     pol_hot);
           continue;
         }
@@ -1173,6 +1164,19 @@ cudaError_t hub_dispatch(int vec, int cons, bool big, const SpmmArgs& a0, cudaSt
   return cudaErrorInvalidValue;
 }
 
+__global__ void k_range_policy(const void* base, uint32_t bytes, int mode, uint64_t* out) {
+  uint64_t p;
+  if (mode == 1)
+    asm("createpolicy.range.global.L2::evict_last.L2::evict_first.b64 %0, [%1], %2, %3;"
+        : "=l"(p)
+        : "l"(base), "r"(bytes), "r"(bytes));
+  else
+    asm("createpolicy.range.global.L2::evict_last.b64 %0, [%1], %2, %3;"
+        : "=l"(p)
+        : "l"(base), "r"(bytes), "r"(bytes));
+  out[0] = p;
+}
+
 __global__ void k_policies(int hints, uint64_t* out) {
   const Policies p = make_policies(hints);
   out[0] = p.keep;
@@ -1181,6 +1185,48 @@ __global__ void k_policies(int hints, uint64_t* out) {
 }
 
 }  // namespace
+
+cudaError_t resolve_range_policy(const void* base, uint32_t bytes, int mode, uint64_t* out,
+                                 cudaStream_t st) {
+  struct Key {
+    int dev;
+    const void* base;
+    uint32_t bytes;
+    int mode;
+    bool operator<(const Key& o) const {
+      return std::tie(dev, base, bytes, mode) < std::tie(o.dev, o.base, o.bytes, o.mode);
+    }
+  };
+  static std::mutex mu;
+  static std::map<Key, uint64_t> cache;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  const Key key{dev, base, bytes, mode};
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cache.find(key);
+    if (it != cache.end()) {
+      *out = it->second;
+      return cudaSuccess;
+    }
+  }
+  uint64_t* d = nullptr;
+  uint64_t v = 0;
+  if ((e = cudaMalloc(reinterpret_cast<void**>(&d), sizeof(v))) != cudaSuccess) return e;
+  k_range_policy<<<1, 1, 0, st>>>(base, bytes, mode, d);
+  note_launch();
+  e = cudaGetLastError();
+  if (e == cudaSuccess) e = cudaMemcpyAsync(&v, d, sizeof(v), cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  cudaFree(d);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lk(mu);
+  if (cache.size() > 64) cache.clear();
+  cache[key] = v;
+  *out = v;
+  return cudaSuccess;
+}
 
 cudaError_t resolve_policies(SpmmArgs* a, cudaStream_t st) {
   struct Entry {

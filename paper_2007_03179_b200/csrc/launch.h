@@ -22,6 +22,11 @@ void note_launch();
 // one-thread kernel, cached per device and hint mode) and stores them into
 // a->pol_* (pol_valid = 1).  Synchronous the first time only.
 cudaError_t resolve_policies(SpmmArgs* a, cudaStream_t st);
+// createpolicy.range word for [base, base + bytes) evict_last (mode 1: and
+// evict_first past it inside the range... sizes equal, so only the copy; mode 2:
+// primary only), cached per (device, base, bytes, mode).  Synchronous on a miss.
+cudaError_t resolve_range_policy(const void* base, uint32_t bytes, int mode, uint64_t* out,
+                                 cudaStream_t st);
 
 // --- faithful Algorithms 1-3 (kernels_faithful.cu) ---
 uint32_t faithful_tiles(int variant, uint32_t cf, uint32_t n);
