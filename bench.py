@@ -45,7 +45,12 @@ CONFIGS = {
                           "dense fp32 N=256, max + argmax"),
     "pubmed": dict(kind="uniform", rows=19_717, nnz=88_648, n=128, op="sum",
                    desc="Pubmed-shaped uniform CSR (19717 rows, 88648 nnz) x dense fp32 N=128, sum"),
+    "cora": dict(kind="uniform", rows=2_708, nnz=10_556, n=16, op="sum",
+                 desc="Cora-shaped uniform CSR (2708 rows, 10556 nnz) x dense fp32 N=16, sum"),
 }
+# BASELINE config 2 sweeps Pubmed over N in {32, 64, 128} x {sum, mean, max}:
+# --n / --op override a config's width and reduce op (the workload text follows)
+SMALL_BYTES = 64 << 20  # below this many algorithmic bytes a step is launch/latency-bound
 GEN_SEED, VAL_SEED, B_SEED = 1, 2, 42
 DATA_DESC = "synthetic (seeded power-law / uniform generator, reference value and B generators)"
 
@@ -392,6 +397,57 @@ def run_reference(args, cfg):
     return 0
 
 
+def small_step_timings(plan, bt, c, arg, l2_flush, stream, reps=25, graph_len=64):
+    """Launch/latency-bound configs (Pubmed, Cora): the step replayed from a
+    captured CUDA graph, cold (after the L2 flush, as the timed steps) and warm
+    (graph_len back-to-back SpMMs in one graph, per SpMM), next to two floors
+    timed the same way: an empty kernel and a device copy of the step's dense
+    bytes (B read, a B-sized write).  Event-timed on `stream`, medians in us."""
+    import torch
+
+    def timed(fn, cold, per=1):
+        ts = []
+        for i in range(reps + 5):
+            if cold:
+                l2_flush.zero_()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            fn()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            if i >= 5:
+                ts.append(e0.elapsed_time(e1) * 1e3 / per)
+        return round(float(statistics.median(ts)), 2)
+
+    cap = torch.cuda.Stream()
+    cap.wait_stream(stream)
+    with torch.cuda.stream(cap):
+        plan.execute(bt, c, arg)  # first-call setup (policies) outside the capture
+    torch.cuda.synchronize()
+    g1, gr = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g1, stream=cap):
+        plan.execute(bt, c, arg)
+    with torch.cuda.graph(gr, stream=cap):
+        for _ in range(graph_len):
+            plan.execute(bt, c, arg)
+    torch.cuda.synchronize()
+    one = torch.zeros(1, device=bt.device)
+    dst = torch.empty_like(bt)
+    with torch.cuda.stream(stream):
+        out = {
+            "cold_graph_us": timed(g1.replay, True),
+            "cold_launch_us": timed(lambda: plan.execute(bt, c, arg), True),
+            "warm_graph_us_per_spmm": timed(gr.replay, False, per=graph_len),
+            "floor_cold_empty_kernel_us": timed(lambda: one.add_(1.0), True),
+            "floor_cold_copy_us": timed(lambda: dst.copy_(bt), True),
+            "floor_copy_bytes": int(2 * bt.numel() * 4),
+            "note": "cold = after the 512 MB L2 flush (the timed steps' condition); warm = "
+                    f"{graph_len} SpMMs back to back in one CUDA graph, inputs L2-resident; "
+                    "floors: an empty kernel and a device copy of B, timed the same way",
+        }
+    return out
+
+
 def run_ours(args, cfg):
     import torch
     import paper_2007_03179_b200 as G
@@ -535,6 +591,10 @@ def run_ours(args, cfg):
             "note": "gespmm_diag_gather on the matrix's own col_ind (L2 flushed) and on an "
                     "all-zero index stream (every gather an L1 hit); ratio > 1 = kernel faster"}
 
+    small = None
+    if alg_bytes < SMALL_BYTES and rank == 0:
+        small = small_step_timings(plan, bt, c, arg, l2_flush, stream)
+
     # end to end: the C-ABI host-buffer call, pinned host buffers, H2D + D2H inside
     e2e = None
     if not args.no_e2e:
@@ -635,6 +695,7 @@ def run_ours(args, cfg):
                          "algorithmic_bytes": alg_bytes, "unique_cols": uniq,
                          "model": "4(M+1)+8nnz+4UN+4MN[+4MN arg], per step"},
             "gather_ceiling": gather_ceiling,
+            "small_step": small,
             "gpu_launches": int(launches),
             "step_ms": {"min": round(min(per_step_ms), 4),
                         "median": round(statistics.median(per_step_ms), 4),
@@ -779,6 +840,9 @@ def main():
                    help="GCN: pad the class width to a multiple of this (default GCNConfig.pad_to)")
     p.add_argument("--hot-rows-mb", type=int, default=0,
                    help="relocated hot B rows budget (MB), experimental build; <=0 off")
+    p.add_argument("--n", type=int, default=0, help="override the config's dense width N")
+    p.add_argument("--op", default="", choices=["", "sum", "mean", "max", "min"],
+                   help="override the config's reduce op (max/min carry the arg output)")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--no-ceiling", action="store_true", help="skip the live gather-ceiling probe")
@@ -798,7 +862,13 @@ def main():
         args.warmup = 3
     if args.config == "gcn":
         return run_gcn(args)
-    cfg = CONFIGS[args.config]
+    cfg = dict(CONFIGS[args.config])
+    if args.n or args.op:
+        n, op = args.n or cfg["n"], args.op or cfg["op"]
+        cfg["desc"] = cfg["desc"].replace(f"N={cfg['n']}, {cfg['op']}", f"N={n}, {op}")
+        if op in ("max", "min") and not cfg.get("arg"):
+            cfg["desc"] += f" + arg{op}"
+        cfg.update(n=n, op=op, arg=cfg.get("arg", False) or op in ("max", "min"))
     if args.impl == "reference":
         return run_reference(args, cfg)
     return run_ours(args, cfg)
