@@ -796,6 +796,131 @@ def run_gcn(args):
     return 0
 
 
+def run_propagate(args):
+    """Stacked SpMM layers: H_{t+1} = A H_t for --hops hops on
+    the Reddit shape (N=128, sum) over nnz-balanced row shards, with the
+    per-hop exchange either fused into the SpMM epilogue (`--exchange fused`:
+    every rank's kernel stores its rows into every rank's next-hop buffer
+    through peer mappings, then one device barrier; dist.fused_propagate's
+    loop) or unfused (`--exchange nccl`: local SpMM into the padded slot, then
+    one in-place all_gather_into_tensor; dist.nccl_propagate's loop).  A step
+    is one hop; value = 2*nnz*N*hops / time, max over ranks; the exchange
+    share is timed on the same stream."""
+    import torch
+    import paper_2007_03179_b200 as G
+    from paper_2007_03179_b200 import dist as D
+
+    world, rank, local = dist_env()
+    dev = init_dist(world, local)
+    cfg = dict(CONFIGS[args.base])
+    n = args.n or cfg["n"]
+    a = make_inputs(cfg)
+    m = a.n_rows
+    info = D.ShardInfo(rank, world, D.partition_rows(np.asarray(a.row_ptr), world))
+    x0 = torch.from_numpy(G.make_random_dense(m, n, B_SEED).data).to(dev)
+    ex = G.ExecOptions(exact=not args.fast)
+    st = torch.cuda.current_stream()
+    stamps = []  # (hop start, spmm done, exchange done) events
+
+    def ev():
+        e = torch.cuda.Event(enable_timing=True)
+        e.record(st)
+        return e
+
+    if args.exchange == "fused":
+        shard = D.shard_csr(a, info.lo, info.hi)
+        plan = G.Plan(G.DeviceCsr.from_host(shard, dev), n, "sum", exec=ex)
+        bufs = [D.PeerRows(m, n, info, dev), D.PeerRows(m, n, info, dev)]
+        bufs[0].full.copy_(x0)
+        dsts = [bf.dsts()[0] for bf in bufs]
+
+        def hop(t, timed):
+            src, dst = bufs[t % 2], bufs[(t + 1) % 2]
+            e0 = ev() if timed else None
+            if info.hi > info.lo:
+                plan.execute_gather(src.full, dsts[(t + 1) % 2])
+            e1 = ev() if timed else None
+            dst.barrier()
+            if timed:
+                stamps.append((e0, e1, ev()))
+
+        def result(t):
+            return bufs[t % 2].full
+    else:
+        pad = info.max_rows
+        shard = D.pad_columns(D.shard_csr(a, info.lo, info.hi), info) if world > 1 else a
+        plan = G.Plan(G.DeviceCsr.from_host(shard, dev), n, "sum", exec=ex)
+        idx = torch.from_numpy(D.padded_row(info, np.arange(m))).to(dev)
+        bufs = [torch.zeros((world * pad, n), dtype=torch.float32, device=dev) for _ in range(2)]
+        bufs[0].index_copy_(0, idx, x0)
+
+        def hop(t, timed):
+            src, dst = bufs[t % 2], bufs[(t + 1) % 2]
+            slot = dst[info.rank * pad:(info.rank + 1) * pad]
+            e0 = ev() if timed else None
+            if info.rows:
+                plan.execute(src, slot[:info.rows])
+            e1 = ev() if timed else None
+            if world > 1:
+                D.allgather_padded(slot, info, out=dst)
+            if timed:
+                stamps.append((e0, e1, ev()))
+
+        def result(t):
+            return bufs[t % 2].index_select(0, idx)
+
+    hops = args.hops
+    for t in range(args.warmup * hops):
+        hop(t, False)
+    torch.cuda.synchronize()
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+    launches0 = G.launch_count()
+    base = args.warmup * hops
+    for t in range(base, base + args.steps * hops):
+        hop(t, True)
+    torch.cuda.synchronize()
+    total = sum(s.elapsed_time(e) for s, _, e in stamps)
+    spmm = sum(s.elapsed_time(m1) for s, m1, _ in stamps)
+    launches = G.launch_count() - launches0
+    red = torch.tensor([total, spmm], dtype=torch.float64, device=dev)
+    if world > 1:
+        import torch.distributed as dist
+        dist.all_reduce(red, op=dist.ReduceOp.MAX)
+    total, spmm = float(red[0]), float(red[1])
+    out = result(base + args.steps * hops)
+    chk = int(G.checksum(G.DenseMatrix.of(out.cpu().numpy()))) if args.checksum else None
+    nh = args.steps * hops
+    if rank == 0:
+        print(json.dumps({
+            "metric": "stacked SpMM propagation H_{t+1} = A H_t (%s shape, N=%d, sum): "
+                      "GFLOP/s per hop incl. the per-hop exchange" % (args.base, n),
+            "value": round(2.0 * a.nnz() * n * nh / (total * 1e-3) / 1e9, 3), "unit": "GFLOP/s",
+            "n_gpus": world, "steps": nh, "warmup": args.warmup * hops,
+            "ms_per_step": round(total / nh, 4), "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f32", "data": DATA_DESC,
+            "config": {"workload": cfg["desc"].replace(f"N={cfg['n']}", f"N={n}") + f", {hops} hops",
+                       "parallelism": f"row-shard x{world}", "exchange": args.exchange,
+                       "backend": os.environ.get("GESPMM_DIST_BACKEND", "nccl") if world > 1 else None},
+            "exchange": {"kind": args.exchange,
+                         "spmm_ms_per_hop": round(spmm / nh, 4),
+                         "exchange_ms_per_hop": round((total - spmm) / nh, 4),
+                         "note": "fused: SpMM with replica stores, then the device barrier; "
+                                 "nccl: SpMM into the padded slot, then all_gather_into_tensor; "
+                                 "max over ranks of each sum"},
+            "checksum": chk, "gpu_launches": launches}), flush=True)
+    if args.exchange == "fused":
+        for bf in bufs:
+            bf.check()
+            bf.close()
+    plan.close()
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+    return 0
+
+
 def relaunch(args):
     """`bench.py --gpus N` outside torchrun: start N ranks (one process per GPU)
     under torch.distributed.run on this node and return rank 0's exit code.
@@ -818,7 +943,13 @@ def main():
     p.add_argument("--steps", type=int, default=50)
     p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    p.add_argument("--config", choices=sorted(CONFIGS) + ["gcn"], default="reddit")
+    p.add_argument("--config", choices=sorted(CONFIGS) + ["gcn", "propagate"], default="reddit")
+    p.add_argument("--hops", type=int, default=3, help="propagate: SpMM hops per step")
+    p.add_argument("--base", choices=["reddit", "pubmed"], default="reddit",
+                   help="propagate: the square graph to propagate over")
+    p.add_argument("--exchange", choices=["fused", "nccl"], default="fused",
+                   help="propagate: per-hop exchange fused into the SpMM epilogue, or NCCL all-gather")
+    p.add_argument("--checksum", action="store_true", help="propagate: print the result checksum")
     p.add_argument("--variant", default="tuned", choices=["tuned", "naive", "crc", "crc-cwm"])
     p.add_argument("--cf", type=int, default=2)
     p.add_argument("--hub-threshold", type=int, default=0)
@@ -862,6 +993,8 @@ def main():
         args.warmup = 3
     if args.config == "gcn":
         return run_gcn(args)
+    if args.config == "propagate":
+        return run_propagate(args)
     cfg = dict(CONFIGS[args.config])
     if args.n or args.op:
         n, op = args.n or cfg["n"], args.op or cfg["op"]

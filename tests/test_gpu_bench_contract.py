@@ -84,3 +84,43 @@ def test_bench_gpus2_launches_two_ranks_and_matches_oracle(tmp_path):
     want, _ = O.spmm(19717, 19717, rp, ci, v, b, "sum")
     assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
 
+
+
+def _propagate(gpus, exchange, backend=None):
+    env = dict(os.environ)
+    env.pop("WORLD_SIZE", None)
+    if backend:
+        env["GESPMM_DIST_BACKEND"] = backend
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", str(gpus),
+                          "--config", "propagate", "--base", "pubmed", "--hops", "2",
+                          "--steps", "2", "--warmup", "3", "--exchange", exchange, "--checksum"],
+                         cwd=ROOT, capture_output=True, text=True, timeout=900, env=env)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.strip().startswith("{")]
+    assert len(lines) == 1, out.stdout
+    return json.loads(lines[0])
+
+
+def test_propagate_fused_and_nccl_exchange_equal_oracle():
+    """`bench.py --config propagate`: stacked hops H_{t+1} = A H_t with the
+    exchange fused into the SpMM epilogue (peer stores + device barrier) or as
+    an all-gather, at 1 and 2 ranks (2 ranks share the one GPU: CUDA IPC
+    mappings for fused, gloo for the all-gather).  Every line's final H is
+    bit-identical to the oracle's 10 hops (3 warm-up + 2 timed steps of 2)."""
+    import numpy as np
+    import oracle as O
+    import paper_2007_03179_b200 as G
+    rp, ci, v = O.ref_gen_uniform(19717, 88648, 1)
+    v = np.ascontiguousarray(v, np.float32)
+    O.randomize_values(v, 2)
+    h = O.make_random_dense(19717, 128, 42)
+    for _ in range(10):
+        h, _ = O.spmm(19717, 19717, rp, ci, v, h, "sum")
+    want = int(G.checksum(G.DenseMatrix.of(h)))
+    lines = [_propagate(1, "fused"), _propagate(1, "nccl"), _propagate(2, "fused", "gloo"),
+             _propagate(2, "nccl", "gloo")]
+    for d in lines:
+        assert d["checksum"] == want, d
+        assert d["steps"] == 4 and d["exchange"]["spmm_ms_per_hop"] > 0
+        assert d["gpu_launches"] >= 4
+    assert [d["n_gpus"] for d in lines] == [1, 1, 2, 2]
