@@ -199,6 +199,25 @@ class GCN:
         return loss.detach()
 
 
+def sgc_features(a: CsrMatrix, x0, hops: int, info: Optional[D.ShardInfo], device,
+                 exchange: str = "fused", group=None, exec: Optional[ExecOptions] = None):
+    """SGC-style propagated features S^K X (Wu et al. 2019: the K stacked
+    aggregations of a GCN without the per-layer transforms, then one linear
+    layer).  The hops are stacked SpMM layers whose outputs are the next hop's
+    gathered operand, so the per-hop exchange can be fused into the SpMM
+    epilogue: ``exchange="fused"`` runs dist.fused_propagate (peer stores over
+    NVLink + one device barrier per hop), ``"nccl"`` dist.nccl_propagate (SpMM
+    into the padded slot + in-place all-gather).  Both return the full M x F
+    result on every rank, bit-identical (each element is folded by one thread
+    in CSR order either way).  x0: the full M x F input on `device`."""
+    info = info or D.ShardInfo(0, 1, [0, a.n_rows])
+    if exchange == "fused":
+        return D.fused_propagate(a, x0, hops, info, device, "sum", group=group, exec=exec)
+    if exchange == "nccl":
+        return D.nccl_propagate(a, x0, hops, info, device, "sum", group=group, exec=exec)
+    raise ValueError(f"exchange must be 'fused' or 'nccl', not {exchange!r}")
+
+
 def normalize_adjacency(a: CsrMatrix, add_self_loops: bool = True) -> CsrMatrix:
     """GCN propagation matrix D^-1/2 (A + I) D^-1/2 on A's pattern (values
     ignored), as a canonical CSR (Kipf & Welling; the normalisation GE-SpMM's

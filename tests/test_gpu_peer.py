@@ -103,6 +103,19 @@ def test_fused_propagate_single_rank_equals_oracle():
     assert np.array_equal(got.cpu().numpy().view(np.uint32), want.view(np.uint32))
 
 
+@pytest.mark.parametrize("exchange", ["fused", "nccl"])
+def test_sgc_features_equal_oracle(exchange):
+    """gcn.sgc_features: the K stacked aggregations of an SGC model through
+    either exchange, on the GCN-normalised adjacency, bit-identical to the
+    oracle's hops."""
+    from paper_2007_03179_b200 import gcn
+    a = gcn.normalize_adjacency(G.gen_powerlaw(2500, 40000, 600, 1.0, 7))
+    x = G.make_random_dense(2500, 64, 8).data
+    got = gcn.sgc_features(a, torch.from_numpy(x).to(DEV), 2, None, DEV, exchange=exchange)
+    want = _oracle_hops(a, x, 2)
+    assert np.array_equal(got.cpu().numpy().view(np.uint32), want.view(np.uint32))
+
+
 def test_peer_barrier_times_out_instead_of_hanging():
     L = _lib.lib()
     mine = torch.zeros(2, dtype=torch.int32, device=DEV)    # rank 0's signal words
