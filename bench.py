@@ -397,7 +397,8 @@ def run_reference(args, cfg):
     return 0
 
 
-def small_step_timings(plan, bt, c, arg, l2_flush, stream, reps=25, graph_len=64):
+def small_step_timings(plan, bt, c, arg, l2_flush, stream, reps=25, graph_len=64,
+                       plan_overlap=None):
     """Launch/latency-bound configs (Pubmed, Cora): the step replayed from a
     captured CUDA graph, cold (after the L2 flush, as the timed steps) and warm
     (graph_len back-to-back SpMMs in one graph, per SpMM), next to two floors
@@ -430,6 +431,15 @@ def small_step_timings(plan, bt, c, arg, l2_flush, stream, reps=25, graph_len=64
     with torch.cuda.graph(gr, stream=cap):
         for _ in range(graph_len):
             plan.execute(bt, c, arg)
+    go = None
+    if plan_overlap is not None:  # the same chain, each SpMM a programmatic dependent launch
+        with torch.cuda.stream(cap):
+            plan_overlap.execute(bt, c, arg)
+        torch.cuda.synchronize()
+        go = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(go, stream=cap):
+            for _ in range(graph_len):
+                plan_overlap.execute(bt, c, arg)
     torch.cuda.synchronize()
     one = torch.zeros(1, device=bt.device)
     dst = torch.empty_like(bt)
@@ -438,12 +448,16 @@ def small_step_timings(plan, bt, c, arg, l2_flush, stream, reps=25, graph_len=64
             "cold_graph_us": timed(g1.replay, True),
             "cold_launch_us": timed(lambda: plan.execute(bt, c, arg), True),
             "warm_graph_us_per_spmm": timed(gr.replay, False, per=graph_len),
+            "warm_graph_overlap_us_per_spmm": (timed(go.replay, False, per=graph_len)
+                                               if go is not None else None),
             "floor_cold_empty_kernel_us": timed(lambda: one.add_(1.0), True),
             "floor_cold_copy_us": timed(lambda: dst.copy_(bt), True),
             "floor_copy_bytes": int(2 * bt.numel() * 4),
             "note": "cold = after the 512 MB L2 flush (the timed steps' condition); warm = "
                     f"{graph_len} SpMMs back to back in one CUDA graph, inputs L2-resident; "
-                    "floors: an empty kernel and a device copy of B, timed the same way",
+                    "floors: an empty kernel and a device copy of B, timed the same way; "
+                    "overlap = the plan with overlap_prev (each SpMM a programmatic dependent "
+                    "launch of the previous one: its CTAs start and read A while it drains)",
         }
     return out
 
@@ -593,7 +607,12 @@ def run_ours(args, cfg):
 
     small = None
     if alg_bytes < SMALL_BYTES and rank == 0:
-        small = small_step_timings(plan, bt, c, arg, l2_flush, stream)
+        import dataclasses
+        ov = (G.Plan(d, n, op, variant=variant, exec=dataclasses.replace(ex, overlap_prev=True))
+              if variant.kind == G.KernelVariant.tuned().kind else None)
+        small = small_step_timings(plan, bt, c, arg, l2_flush, stream, plan_overlap=ov)
+        if ov is not None:
+            ov.close()
 
     # end to end: the C-ABI host-buffer call, pinned host buffers, H2D + D2H inside
     e2e = None

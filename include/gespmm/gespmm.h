@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define GESPMM_ABI_VERSION 1
+#define GESPMM_ABI_VERSION 2
 
 /* Reduce ops.  Replaces spmm::ReduceOp / ops::sum / ops::max
  * (reference include/spmm/reduce_op.hpp:14-28): a host function pointer cannot
@@ -130,6 +130,16 @@ typedef struct {
                          Edge args only.  Experimental (measured slower on B200: fewer DRAM
                          bytes, more instructions).  <=0 = off (default), >0 =
                          budget in MB */
+  int32_t overlap_prev; /* TUNED plans whose execute is one kernel (no hub rows, one column
+                         slice; gespmm_plan_launches == 1): launch it as a programmatic
+                         dependent of the preceding kernel on the stream, so its CTAs start
+                         while that kernel drains and read the row schedule, row_ptr and the
+                         first staged (col_ind, vals) chunk before waiting for it
+                         (griddepcontrol.wait precedes every B read and C/arg write).
+                         Contract: the preceding kernel must not write A's arrays, and must
+                         itself be a single-kernel plan execute or a plain kernel (not a
+                         two-kernel hub execute).  For back-to-back SpMMs over a small graph
+                         (stacked hops, CUDA-graph replay).  Default 0. */
 } gespmm_options_t;
 
 void gespmm_options_default(gespmm_options_t* opts);

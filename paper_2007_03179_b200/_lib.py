@@ -64,7 +64,7 @@ class Options(C.Structure):
                 ("l2_hot_mb", C.c_int32), ("tuned_cf", C.c_int32),
                 ("col_slices", C.c_int32), ("rows_per_warp", C.c_int32),
                 ("cluster_hot", C.c_int32), ("h2d_pack", C.c_int32),
-                ("hot_rows_mb", C.c_int32)]
+                ("hot_rows_mb", C.c_int32), ("overlap_prev", C.c_int32)]
 
 
 _lock = threading.Lock()

@@ -366,6 +366,8 @@ class ExecOptions:
     cluster_hot: int = 0            # N = 128 plans: hot B rows in cluster DSMEM (cluster size), 0 off
     h2d_pack: int = 0               # host entry: 16-bit gap codes for col_ind upload; 0 auto, 1 on, -1 off
     hot_rows_mb: int = 0            # relocated hot B rows (plan-owned copy), MB; <=0 off (experimental)
+    overlap_prev: bool = False      # single-kernel plans: programmatic dependent launch onto the
+                                    # previous kernel (A prologue before the wait; gespmm.h contract)
 
 
 def _options(variant: KernelVariant, ex: ExecOptions, validate: bool = True) -> _lib.Options:
@@ -377,7 +379,8 @@ def _options(variant: KernelVariant, ex: ExecOptions, validate: bool = True) -> 
                            l2_persist=int(ex.l2_persist), l2_hot_mb=int(ex.l2_hot_mb),
                            tuned_cf=int(ex.tuned_cf), col_slices=int(ex.col_slices),
                            rows_per_warp=int(ex.rows_per_warp), cluster_hot=int(ex.cluster_hot),
-                           h2d_pack=int(ex.h2d_pack), hot_rows_mb=int(ex.hot_rows_mb))
+                           h2d_pack=int(ex.h2d_pack), hot_rows_mb=int(ex.hot_rows_mb),
+                           overlap_prev=int(ex.overlap_prev))
 
 
 # ---------------------------------------------------------------------------

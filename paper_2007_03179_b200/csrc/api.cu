@@ -332,8 +332,10 @@ gespmm_status_t launch_tuned_rows(const TunedShapes& t, int op, bool fast, const
                                   const uint32_t* order, uint32_t n_hub, uint32_t n_rest,
                                   cudaStream_t st, cudaStream_t side, cudaEvent_t fork,
                                   cudaEvent_t join, const cudaAccessPolicyWindow* winp,
-                                  bool hub_pdl, uint32_t* work) {
+                                  bool hub_pdl, uint32_t* work, bool chain = false) {
   SpmmArgs a = a0;
+  // overlap_prev: only a single-kernel execute chains onto the previous kernel
+  chain = chain && n_hub == 0 && t.slices == 1;
   GESPMM_CUDA(resolve_policies(&a, st), "spmm");
   const bool v_ok = aligned(a.b, 16) && aligned(a.c, 16) && (!a.arg || aligned(a.arg, 16));
   const bool v2_ok = aligned(a.b, 8) && aligned(a.c, 8) && (!a.arg || aligned(a.arg, 8));
@@ -408,7 +410,9 @@ gespmm_status_t launch_tuned_rows(const TunedShapes& t, int op, bool fast, const
     sa.order = order + n_hub;
     sa.n_sched = n_rest;
     sa.n_tiles = (w + wsel.tile_width() - 1) / wsel.tile_width();
-    if (n_rest) GESPMM_CUDA(launch_tuned_warp(wsel, op, fast, sa, st, winp, hub_then_pdl), "spmm");
+    sa.pdl_wait = chain ? 1 : 0;
+    if (n_rest)
+      GESPMM_CUDA(launch_tuned_warp(wsel, op, fast, sa, st, winp, hub_then_pdl || chain), "spmm");
     if (side_used) GESPMM_CUDA(cudaStreamWaitEvent(st, join, 0), "spmm");
   }
   return GESPMM_OK;
@@ -688,7 +692,8 @@ gespmm_status_t plan_execute_impl(Plan& p, const float* b, float* c, int32_t* ar
   }
 #endif
   return launch_tuned_rows(p.sh, p.op, fast, args, p.d_order, p.n_hub, p.a.n_rows - p.n_hub, st,
-                           p.side, p.ev_fork, p.ev_join, winp, p.hub_pdl, p.d_work);
+                           p.side, p.ev_fork, p.ev_join, winp, p.hub_pdl, p.d_work,
+                           p.o.overlap_prev != 0 && !winp);
 }
 
 // Small LRU of plans for the plan-less device entry point: keyed by the CSR

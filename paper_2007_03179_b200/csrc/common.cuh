@@ -350,6 +350,11 @@ struct SpmmArgs {
   // this key (the first violation found so far, ~0 = none) is set, so
   // non-canonical columns are never dereferenced.  Null: no check.
   const unsigned long long* abort_if;
+  // overlap_prev plans: launched as a programmatic dependent of the previous
+  // kernel; every warp executes griddepcontrol.wait after its A-side prologue
+  // and before its first B gather (1), or never waits (0: the hub-then-warp
+  // pair, whose rows are disjoint and whose B was complete before either ran).
+  int pdl_wait;
 };
 
 __device__ __forceinline__ bool aborted(const SpmmArgs& a) {

@@ -364,6 +364,10 @@ __global__ void __launch_bounds__(32 * kWarpBlock, warp_min_blocks<OP, CF, LPR>(
   const uint32_t wib = threadIdx.x >> 5;
   const uint64_t unit = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const uint64_t groups = (uint64_t(a.n_sched) + WarpGeom<LPR, CF>::RPW - 1) / WarpGeom<LPR, CF>::RPW;
+  // dependents (an overlap_prev plan next on the stream) may launch once every
+  // CTA of this grid has started; they wait for its completion before their
+  // first B read (griddepcontrol.wait below), so this only overlaps launches
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   if (unit >= groups * a.n_tiles) return;  // warp-uniform exit
   if (aborted(a)) return;
   const Policies pol = args_policies(a);
@@ -382,6 +386,9 @@ __global__ void __launch_bounds__(32 * kWarpBlock, warp_min_blocks<OP, CF, LPR>(
   UnitMeta m;
   unit_rows<LPR>(a, group, m);
   unit_chunk0<LPR, WarpGeom<LPR, CF>::E, HOT>(a, pol, m);
+  // overlap_prev: row schedule, row_ptr and the first (col, val) chunk are in
+  // flight; B and C belong to the previous kernel until it has completed
+  if (a.pdl_wait) asm volatile("griddepcontrol.wait;" ::: "memory");
   warp_unit<OP, FAST, VEC, LPR, CF, HOT>(a, pol, tile, m, &s_col[wib][0][0], &s_val[wib][0][0]);
 }
 

@@ -40,7 +40,7 @@ def test_library_is_sm100a():
 
 
 def test_abi_version_and_defaults():
-    assert _lib.lib().gespmm_abi_version() == 1
+    assert _lib.lib().gespmm_abi_version() == 2
     o = _lib.default_options()
     assert (o.variant, o.cf, o.exact, o.arg_kind, o.validate, o.l2_hints) == (0, 2, 1, 0, 1, 1)
 
