@@ -300,7 +300,11 @@ TunedShapes make_shapes(const gespmm_options_t& o, uint32_t k, uint32_t n, int d
   t.slices = (n + t.slice_w - 1) / t.slice_w;
   const uint32_t sw = t.slice_w;
   const bool n4 = n % 4 == 0, n2 = n % 2 == 0;
-  t.rpw = o.rows_per_warp > 0 ? o.rows_per_warp : (mean_degree <= 16.0 ? 4 : 1);
+  // low-degree matrices share a warp between rows: 2 rows at N >= 64, 4 below
+  // (Pubmed, warm graph replay per SpMM, tools/r2_rpw.sh: N=128 8.62 -> 8.13 us
+  // at 2 rows (lpr 16, cf 2) vs 4 (lpr 8, cf 4); N=64 6.27 -> 6.08; N=256 equal;
+  // N=32 best at 4 rows, lpr 8: 4.47 vs 6.01 us at 2)
+  t.rpw = o.rows_per_warp > 0 ? o.rows_per_warp : (mean_degree <= 16.0 ? (sw >= 64 ? 2 : 4) : 1);
   t.warp_v = pick_warp_shape(sw, n4, !n4 && n2, t.rpw);
   t.warp_s = pick_warp_shape(sw, false, false);
   if (o.tuned_cf > 0) {  // explicit CWM merge factor for the warp kernel (tuning)
