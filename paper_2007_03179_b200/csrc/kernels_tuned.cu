@@ -104,6 +104,9 @@ template <int LPR, int CF>
 #ifndef GESPMM_U_NARROW
 #define GESPMM_U_NARROW 8
 #endif
+#ifndef GESPMM_U_WIDE
+#define GESPMM_U_WIDE 8  // gather batch of full-warp CF=1 rows (A/B builds: 16 with fewer CTAs/SM)
+#endif
 #ifndef GESPMM_STAGE_MIN
 #define GESPMM_STAGE_MIN 8  // staged entries per row per chunk, at least
 #endif
@@ -115,7 +118,7 @@ struct WarpGeom {
   // (scalar 1- and 2-lane rows, N < 4, keep one entry per lane)
   static constexpr int E = (LPR >= GESPMM_STAGE_MIN || LPR < 4) ? 1 : GESPMM_STAGE_MIN / LPR;
   static constexpr int CH = LPR * E;                       // entries per row per chunk
-  static constexpr int U0 = (LPR == 16 ? GESPMM_U_NARROW : 8) / CF;
+  static constexpr int U0 = (LPR == 16 ? GESPMM_U_NARROW : (LPR == 32 && CF == 1 ? GESPMM_U_WIDE : 8)) / CF;
   static constexpr int U = U0 < CH ? U0 : CH;              // gather batch; CH % U == 0
   static constexpr int W = U < 4 ? U : 4;                  // LDS width (entries per read)
   static_assert(CH % U == 0 && U % W == 0 && E <= (GESPMM_STAGE_MIN / 4 > 1 ? GESPMM_STAGE_MIN / 4 : 1),
