@@ -288,6 +288,23 @@ gespmm_status_t gespmm_from_coo(uint32_t n_rows, uint32_t n_cols, uint64_t count
                                 int32_t policy, uint32_t* row_ptr, uint32_t* col_ind,
                                 float* out_vals, uint64_t* nnz);
 
+/* from_coo on DEVICE arrays (the same semantics, bit for bit): bounds check
+ * (first offending triple in input order, the reference's message), stable
+ * (row, col) order, duplicate runs folded in input order (Sum: v = v + next in
+ * fp32; Last: the final occurrence).  row_ptr[n_rows+1], col_ind[count] and
+ * out_vals[count] are caller-allocated device buffers (count is the capacity
+ * bound); *nnz (host) receives the canonical length.  Synchronous with respect
+ * to the host (it returns *nnz); ~20 B per triple of device temporaries. */
+gespmm_status_t gespmm_from_coo_device(uint32_t n_rows, uint32_t n_cols, uint64_t count,
+                                       const uint32_t* rows, const uint32_t* cols,
+                                       const float* vals, int32_t policy, uint32_t* row_ptr,
+                                       uint32_t* col_ind, float* out_vals, uint64_t* nnz,
+                                       void* stream);
+/* to_coo on device (csr.hpp:95-104): rows[nnz] expanded from row_ptr, cols and
+ * vals copied; asynchronous on `stream`. */
+gespmm_status_t gespmm_to_coo_device(const gespmm_csr_t* a, uint32_t* rows, uint32_t* cols,
+                                     float* vals, void* stream);
+
 /* validate (csr.hpp:107-153) on host arrays of the given lengths: returns the
  * number of violations and writes their messages, '\n'-separated, in the
  * reference's order and wording into msgs (truncated to msgs_cap; the full

@@ -107,7 +107,7 @@ def _load_ref():
         lib.ref_select_variant.argtypes = [cu, C.POINTER(C.c_int), C.POINTER(cu)]
         lib.ref_from_coo.restype = C.c_longlong
         lib.ref_from_coo.argtypes = [cu, cu, cull, _u32p, _u32p, _f32p, _u32p, _u32p, _f32p,
-                                     cp, cu]
+                                     cp, cu, C.c_int]
         lib.ref_sim_metrics.restype = C.c_int
         lib.ref_sim_metrics.argtypes = [cu, cu, cull, _u32p, _u32p, _f32p, _f32p, cu, cp,
                                         C.c_int, cu, C.POINTER(cull), cp, cu]
@@ -371,14 +371,15 @@ def ref_select_variant(n):
     return {0: "naive", 1: "crc", 2: "crc-cwm"}[kind.value], cf.value
 
 
-def ref_from_coo(rows, cols, r, c, v):
+def ref_from_coo(rows, cols, r, c, v, policy="sum"):
     cnt = len(r)
     rp = np.zeros(rows + 1, np.uint32)
     ci = np.zeros(max(cnt, 1), np.uint32)
     vv = np.zeros(max(cnt, 1), np.float32)
     e = _err()
     nnz = _load_ref().ref_from_coo(rows, cols, cnt, _nz(r, np.uint32), _nz(c, np.uint32),
-                                   _nz(v, np.float32), rp, ci, vv, e, 1024)
+                                   _nz(v, np.float32), rp, ci, vv, e, 1024,
+                                   0 if policy == "sum" else 1)
     if nnz < 0:
         raise RefError(e.value.decode())
     return rp, ci[:nnz].copy(), vv[:nnz].copy()

@@ -199,18 +199,18 @@ void ref_select_variant(unsigned n, int* kind, unsigned* cf) {
   *cf = v.cf;
 }
 
-// COO -> canonical CSR (sum dedup); out arrays sized to the COO length,
-// returns the canonical nnz or -1 on error.
+// COO -> canonical CSR (policy 0 = DedupPolicy::Sum, 1 = Last); out arrays
+// sized to the COO length, returns the canonical nnz or -1 on error.
 long long ref_from_coo(unsigned rows, unsigned cols, unsigned long long count, const unsigned* r,
                        const unsigned* c, const float* v, unsigned* row_ptr, unsigned* col_ind,
-                       float* vals, char* err, unsigned err_len) {
+                       float* vals, char* err, unsigned err_len, int policy) {
   try {
     CooEntries coo;
     coo.n_rows = rows;
     coo.n_cols = cols;
     coo.entries.reserve(count);
     for (unsigned long long i = 0; i < count; ++i) coo.entries.push_back({r[i], c[i], v[i]});
-    const CsrMatrix a = from_coo(coo, DedupPolicy::Sum);
+    const CsrMatrix a = from_coo(coo, policy ? DedupPolicy::Last : DedupPolicy::Sum);
     std::memcpy(row_ptr, a.row_ptr.data(), sizeof(unsigned) * a.row_ptr.size());
     if (a.nnz()) {
       std::memcpy(col_ind, a.col_ind.data(), sizeof(unsigned) * a.nnz());

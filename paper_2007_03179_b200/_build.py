@@ -29,7 +29,7 @@ CXX_FLAGS = ["-O3", "-std=c++17", "-fPIC", "-ffp-contract=off", "-Wall", "-Wextr
              "-I", INCLUDE, "-I", CSRC, "-I", "/usr/local/cuda/include"]
 
 CU_SOURCES = ["api.cu", "validate.cu", "kernels_faithful.cu", "kernels_tuned.cu", "diag.cu",
-              "transpose.cu", "peer.cu", "h2dpack.cu"]
+              "transpose.cu", "peer.cu", "h2dpack.cu", "coo.cu"]
 # measured slower on B200: only in the GESPMM_EXPERIMENTAL build
 EXPERIMENTAL_CU = ["hotcols.cu", "cluster.cu", "hotrows.cu"]
 LIB_EXP = os.path.join(PKG, "libgespmm_exp.so")

@@ -45,7 +45,7 @@ EXPORTS = [
     "gespmm_peer_barrier", "gespmm_peer_alloc", "gespmm_peer_free", "gespmm_ipc_get_handle",
     "gespmm_ipc_open_handle", "gespmm_ipc_close", "gespmm_multicast_alloc",
     "gespmm_multicast_free", "gespmm_build_flags", "gespmm_from_coo", "gespmm_validate_host",
-    "gespmm_mtx_parse",
+    "gespmm_mtx_parse", "gespmm_from_coo_device", "gespmm_to_coo_device",
 ]
 BUILD_EXPERIMENTAL = 1
 MAX_GATHER_DSTS = 8
@@ -160,6 +160,11 @@ def lib():
         L.gespmm_diag_gather_mode.restype = C.c_int
         L.gespmm_csr_transpose_device.argtypes = [C.POINTER(Csr), vp, vp, vp, vp]
         L.gespmm_csr_transpose_device.restype = C.c_int
+        L.gespmm_from_coo_device.argtypes = [u32, u32, u64, vp, vp, vp, i32, vp, vp, vp,
+                                             C.POINTER(u64), vp]
+        L.gespmm_from_coo_device.restype = C.c_int
+        L.gespmm_to_coo_device.argtypes = [C.POINTER(Csr), vp, vp, vp, vp]
+        L.gespmm_to_coo_device.restype = C.c_int
         L.gespmm_csr1_write.argtypes = [C.c_char_p, C.POINTER(Csr)]
         L.gespmm_csr1_write.restype = C.c_int
         L.gespmm_csr1_header.argtypes = [C.c_char_p, C.POINTER(u32), C.POINTER(u32),

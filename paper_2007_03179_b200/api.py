@@ -616,6 +616,49 @@ class DeviceCsr:
                                                  v.data_ptr(), int(validate), _stream_ptr(stream)))
         return cls(rows, cols, rp, ci[:nnz], v[:nnz])
 
+    @classmethod
+    def from_coo(cls, n_rows: int, n_cols: int, rows, cols, vals, policy: str = "sum",
+                 stream=None) -> "DeviceCsr":
+        """from_coo (csr.hpp:58-93) on device triples (torch int32/uint32 and
+        float32 tensors on one CUDA device) through gespmm_from_coo_device:
+        bit-identical to the host from_coo, errors worded like the reference."""
+        import torch
+        if policy not in ("sum", "last"):
+            raise Error(f"from_coo: unknown dedup policy '{policy}' (sum, last)")
+        n = int(rows.numel())
+        if int(cols.numel()) != n or int(vals.numel()) != n:
+            raise Error("from_coo: rows, cols and vals must have the same length")
+        for t, dt, what in ((rows, (torch.int32,), "rows"), (cols, (torch.int32,), "cols"),
+                            (vals, (torch.float32,), "vals")):
+            if not t.is_cuda or t.dtype not in dt or not t.is_contiguous():
+                raise Error(f"from_coo: {what} must be a contiguous CUDA {dt[0]} tensor")
+        dev = rows.device
+        rp = torch.empty(n_rows + 1, dtype=torch.int32, device=dev)
+        ci = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+        v = torch.empty(max(n, 1), dtype=torch.float32, device=dev)
+        nnz = C.c_uint64()
+        with torch.cuda.device(dev):
+            _check(lib().gespmm_from_coo_device(
+                n_rows, n_cols, n, rows.data_ptr() if n else None, cols.data_ptr() if n else None,
+                vals.data_ptr() if n else None, 0 if policy == "sum" else 1, rp.data_ptr(),
+                ci.data_ptr(), v.data_ptr(), C.byref(nnz), _stream_ptr(stream)))
+        z = int(nnz.value)
+        return cls(n_rows, n_cols, rp, ci[:z], v[:z])
+
+    def to_coo(self, stream=None):
+        """(rows, cols, vals) device tensors in row-major order (csr.hpp:95-104)."""
+        import torch
+        dev = self.row_ptr.device
+        n = self.nnz()
+        r = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+        c = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+        v = torch.empty(max(n, 1), dtype=torch.float32, device=dev)
+        csr = self.c_struct()
+        with torch.cuda.device(dev):
+            _check(lib().gespmm_to_coo_device(C.byref(csr), r.data_ptr(), c.data_ptr(),
+                                              v.data_ptr(), _stream_ptr(stream)))
+        return r[:n], c[:n], v[:n]
+
     def nnz(self) -> int:
         return int(self.col_ind.numel())
 
