@@ -601,11 +601,10 @@ k_hub(SpmmArgs a) {
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < S; ++i) {
-      // full: one cp.async-completion arrival per producer lane; empty: one
-      // arrival per consumer warp
+      // full: one arrival per producer lane; empty: one arrival per consumer lane
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 32;" ::"r"(full0 + 8 * i));
       asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(empty0 + 8 * i),
-                   "r"(C));
+                   "r"(32 * C));
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -675,8 +674,19 @@ k_hub(SpmmArgs a) {
           if (e < cnt && piece < chunks)
             cp_async16(slot + c * 16u, bsrc + uint64_t(k) * stride + piece * 16u, pol.keep);
         }
+#ifdef GESPMM_HUB_ASYNC_ARRIVE
+        // the stage completes when every lane's copies land (no producer stall)
         asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(full0 + 8 * st)
                      : "memory");
+#else
+        // each lane waits for its own copies, then arrives with release
+        // semantics: the same completion point (a producer warp has nothing
+        // else to issue until the ring frees its next stage), expressed as an
+        // ordinary barrier handoff that compute-sanitizer's racecheck can follow
+        asm volatile("cp.async.wait_all;" ::: "memory");
+        asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(full0 + 8 * st)
+                     : "memory");
+#endif
       }
     } else {
       // ---- consumer warps: thread t owns columns col0 + t*VEC .. +VEC
@@ -722,9 +732,13 @@ k_hub(SpmmArgs a) {
             }
           }
         }
-        __syncwarp();
-        if (lane == 0)
-          asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(empty0 + 8 * st) : "memory");
+        // every consumer lane releases its own reads of the stage (32 * C
+        // arrivals): the producer's acquire then orders each lane's reads
+        // before the next round's copies directly, which compute-sanitizer's
+        // racecheck verifies (with one arrival per warp after __syncwarp it
+        // could not follow lanes 1..31 and reported every stage)
+        asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(empty0 + 8 * st)
+                     : "memory");
       }
       if (colok) {
         float out[VEC];
@@ -777,9 +791,9 @@ k_hub_g4(SpmmArgs a, const __grid_constant__ CUtensorMap tmap) {
   if (threadIdx.x == 0) {
     for (int i = 0; i < S; ++i) {
       // full: the producer's arrive.expect_tx (+ the stage's bytes); empty:
-      // one arrival per consumer warp
+      // one arrival per consumer lane
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(full0 + 8 * i));
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(empty0 + 8 * i), "r"(C));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(empty0 + 8 * i), "r"(32 * C));
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -899,9 +913,13 @@ k_hub_g4(SpmmArgs a, const __grid_constant__ CUtensorMap tmap) {
             }
           }
         }
-        __syncwarp();
-        if (lane == 0)
-          asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(empty0 + 8 * st) : "memory");
+        // every consumer lane releases its own reads of the stage (32 * C
+        // arrivals): the producer's acquire then orders each lane's reads
+        // before the next round's copies directly, which compute-sanitizer's
+        // racecheck verifies (with one arrival per warp after __syncwarp it
+        // could not follow lanes 1..31 and reported every stage)
+        asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(empty0 + 8 * st)
+                     : "memory");
       }
       if (colok) {
         float out[VEC];
