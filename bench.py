@@ -520,10 +520,13 @@ def run_ours(args, cfg):
     def step():
         plan.execute(bt, c, arg)
 
+    nvtx = torch.cuda.nvtx
+    nvtx.range_push("bench: warmup")
     for _ in range(max(args.warmup, 1)):
         l2_flush.zero_()
         step()
     torch.cuda.synchronize()
+    nvtx.range_pop()
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     sampler = ClockSampler(local) if rank == 0 else None
@@ -537,13 +540,17 @@ def run_ours(args, cfg):
     launches0 = G.launch_count()
     if sampler:
         sampler.mark_start()
+    nvtx.range_push("bench: timed steps")
     for i in range(args.steps):
         if not args.no_flush:
             l2_flush.zero_()  # outside the events: L2 flushed between steps
         starts[i].record(stream)
+        nvtx.range_push(f"step {i}")
         step()
+        nvtx.range_pop()
         ends[i].record(stream)
     torch.cuda.synchronize()
+    nvtx.range_pop()
     if sampler:
         sampler.mark_end()
     launches = G.launch_count() - launches0

@@ -9,6 +9,7 @@
 //   check_config        include/spmm/kernel.hpp:83-92  (cf in {2,4,8})
 //   select_variant      include/spmm/kernel.hpp:96-98
 //   reduce_op_by_name   include/spmm/reduce_op.hpp:32-36
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX3: ranges for nsys/ncu timelines
 #include <algorithm>
 #include <atomic>
 #include <chrono>
@@ -803,6 +804,14 @@ Workspace* workspace() {
 }
 
 // GESPMM_TRACE=1: host-side phase timestamps of the host entry point (stderr).
+// NVTX range for the lifetime of a scope (nsys / ncu --nvtx timelines)
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
+
 struct Trace {
   bool on = false;
   std::chrono::steady_clock::time_point t0;
@@ -812,6 +821,7 @@ struct Trace {
     t0 = std::chrono::steady_clock::now();
   }
   void mark(const char* what) const {
+    nvtxMarkA(what);  // a no-op unless a profiler is attached
     if (!on) return;
     const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
     std::fprintf(stderr, "[gespmm] %8.3f ms  %s\n", ms, what);
@@ -921,6 +931,7 @@ gespmm_status_t gespmm_plan_create(const gespmm_csr_t* a, uint32_t n, gespmm_red
 gespmm_status_t gespmm_plan_execute(gespmm_plan_t plan, const float* b, float* c, int32_t* arg,
                                     void* stream) {
   if (!plan) return fail(GESPMM_EINVAL, "null plan");
+  const NvtxRange nvtx("gespmm_plan_execute");
   return plan_execute_impl(*reinterpret_cast<Plan*>(plan), b, c, arg,
                            static_cast<cudaStream_t>(stream));
 }
@@ -1019,6 +1030,7 @@ gespmm_status_t gespmm_spmm_host(const gespmm_csr_t* a, const float* b, uint32_t
   // the D2H hide under the CSR upload.  On an error status the contents of c
   // (and arg) are unspecified.
   if (!a) return fail(GESPMM_EINVAL, "null csr");
+  const NvtxRange nvtx("gespmm_spmm_host");
   const Trace tr;
   gespmm_options_t o;
   if (opts) o = *opts; else gespmm_options_default(&o);
