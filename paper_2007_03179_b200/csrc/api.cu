@@ -1311,6 +1311,11 @@ gespmm_status_t gespmm_spmm_host(const gespmm_csr_t* a, const float* b, uint32_t
   }
   tr.dev("all C rows copied out", ws->out);
   tr.mark("all blocks enqueued");
+  {
+    void* drain[2] = {ws->stream, ws->out};
+    host_poll(drain, 2);
+  }
+  tr.mark("streams drained");
   if (cc) {
     uint64_t key = ~0ull;
     uint32_t brow = 0, bcol = 0;

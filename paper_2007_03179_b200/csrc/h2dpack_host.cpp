@@ -1,8 +1,12 @@
 // Packed column indices for the host entry's PCIe upload (host side; the
 // device side and the format are described in h2dpack.cu).  Encoding runs on
 // most host threads (OpenMP) while the copy engine moves the previous block.
+#include <cuda_runtime_api.h>
+#include <immintrin.h>
 #include <omp.h>
 #include <stdint.h>
+
+#include <atomic>
 
 #include <algorithm>
 #include <cstdlib>
@@ -68,19 +72,13 @@ PackRows pick_pack_rows() {
 
 }  // namespace
 
-// Encodes positions [row_ptr[lo], row_ptr[hi]) of rows [lo, hi) into enc
-// (relative positions) and appends escaped (relative position, value) pairs to
-// exc in position order.  Returns the number of exceptions, or UINT64_MAX when
-// they exceed max_exc (the caller then sends the block raw).
-uint64_t pack_cols_block(const uint32_t* row_ptr, const uint32_t* col_ind, uint32_t lo,
-                         uint32_t hi, uint16_t* enc, uint32_t* exc /* pairs */, uint64_t max_exc) {
-  const uint64_t ps = row_ptr[lo];
-  // three quarters of the host threads unless OMP_NUM_THREADS says otherwise:
-  // with every core packing, the packing contends with the copy engine's reads
-  // of host memory and with the CUDA driver threads (Reddit, 16 cores: 17.9 ms
-  // at 16 threads, 16.3 ms at 12, 16.7-19.3 ms at 8; tools/e2e_threads.py)
-  // GESPMM_PACK_THREADS overrides; under torchrun (LOCAL_WORLD_SIZE set, which
-  // also forces OMP_NUM_THREADS=1) the host's threads are split between ranks
+// three quarters of the host threads unless OMP_NUM_THREADS says otherwise:
+// with every core packing, the packing contends with the copy engine's reads
+// of host memory and with the CUDA driver threads (Reddit, 16 cores: 17.9 ms
+// at 16 threads, 16.3 ms at 12, 16.7-19.3 ms at 8; tools/e2e_threads.py)
+// GESPMM_PACK_THREADS overrides; under torchrun (LOCAL_WORLD_SIZE set, which
+// also forces OMP_NUM_THREADS=1) the host's threads are split between ranks
+int pack_threads() {
   static const int nt = [] {
     if (const char* e = std::getenv("GESPMM_PACK_THREADS")) return std::max(1, std::atoi(e));
     const char* lws = std::getenv("LOCAL_WORLD_SIZE");
@@ -89,6 +87,45 @@ uint64_t pack_cols_block(const uint32_t* row_ptr, const uint32_t* col_ind, uint3
     const int mine = std::max(1, hw > 4 ? hw * 3 / 4 : hw);
     return lws ? std::max(1, mine / std::max(1, std::atoi(lws))) : mine;
   }();
+  return nt;
+}
+
+// Keeps the packing threads busy until every stream in `streams` has drained.
+// Measured on the box (tools/e2e_env.py, Reddit host call, 3 processes each):
+// when the packer finishes (~10 ms into a ~17 ms call) and the host goes idle,
+// the remaining H2D/D2H copies and kernels slow down (the last block lands
+// ~2.3 ms after the previous one instead of ~1.1 ms), 17.3-17.8 ms per call;
+// with the OpenMP threads spinning (OMP_WAIT_POLICY=active) 16.2-16.5 ms.  So
+// after the last block is enqueued the pool polls the streams instead of
+// sleeping.  GESPMM_HOST_POLL=0 turns it off, =N polls with N threads.
+void host_poll(void* const* streams, int n) {
+  static const int np = [] {
+    const char* e = std::getenv("GESPMM_HOST_POLL");
+    return e ? std::max(0, std::atoi(e)) : -1;
+  }();
+  const int threads = np < 0 ? pack_threads() : np;
+  if (threads == 0 || n == 0) return;
+  std::atomic<bool> done{false};
+#pragma omp parallel num_threads(threads)
+  {
+    if (omp_get_thread_num() == 0) {
+      for (int i = 0; i < n; ++i)
+        while (cudaStreamQuery(static_cast<cudaStream_t>(streams[i])) == cudaErrorNotReady) _mm_pause();
+      done.store(true, std::memory_order_release);
+    } else {
+      while (!done.load(std::memory_order_acquire)) _mm_pause();
+    }
+  }
+}
+
+// Encodes positions [row_ptr[lo], row_ptr[hi]) of rows [lo, hi) into enc
+// (relative positions) and appends escaped (relative position, value) pairs to
+// exc in position order.  Returns the number of exceptions, or UINT64_MAX when
+// they exceed max_exc (the caller then sends the block raw).
+uint64_t pack_cols_block(const uint32_t* row_ptr, const uint32_t* col_ind, uint32_t lo,
+                         uint32_t hi, uint16_t* enc, uint32_t* exc /* pairs */, uint64_t max_exc) {
+  const uint64_t ps = row_ptr[lo];
+  const int nt = pack_threads();
   // rows split by nnz across threads
   std::vector<uint32_t> cut(size_t(nt) + 1, hi);
   cut[0] = lo;

@@ -127,6 +127,10 @@ cudaError_t launch_cluster_warp(const ClusterHot& h, int op, bool fast, const Sp
 uint64_t pack_cols_block(const uint32_t* row_ptr, const uint32_t* col_ind, uint32_t lo,
                          uint32_t hi, uint16_t* enc, uint32_t* exc, uint64_t max_exc);
 size_t unpack_temp_bytes(uint64_t max_len);
+int pack_threads();
+// host entry: the packing threads poll `streams` until they drain (idle host
+// cores slow the tail copies on the boxes; h2dpack_host.cpp)
+void host_poll(void* const* streams, int n);
 // rows [0, m_block) of row_ptr_block own positions [ps, pe); bits: zeroed
 // row-start bitmap over all nnz positions (shared with the column check).
 // bad_key (nullable): also check the rebuilt columns (bounds k_cols, strictly
