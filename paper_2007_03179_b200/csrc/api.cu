@@ -1110,12 +1110,14 @@ gespmm_status_t gespmm_spmm_host(const gespmm_csr_t* a, const float* b, uint32_t
     const int v = std::atoi(e);
     if (v >= 1 && v <= kMaxChunks && nnz >= uint64_t(v)) chunks = v;
   }
-  // GESPMM_TAPER=1: the last two blocks carry half a block's nonzeros each, so
-  // less is left after the final copy — measured best case 15.82 vs 15.97 ms
-  // but a noisier median (16.4-16.7 vs 16.0), so equal blocks stay the default
+  // taper: the last two blocks carry half a block's nonzeros each, so less is
+  // left after the final copy.  Round 1 measured it within the noise; with the
+  // host polling through the tail (host_poll) the noise is gone and it is
+  // 0.1-0.2 ms faster (Reddit: 16.16/16.28 vs 16.40/16.46 ms median,
+  // profiles/r2/e2e_taper.txt).  GESPMM_TAPER=0 turns it off.
   static const bool taper = [] {
     const char* e = std::getenv("GESPMM_TAPER");
-    return e && e[0] == '1';
+    return !(e && e[0] == '0');
   }();
   double wsum = 0.0, wcum[kMaxChunks + 1] = {0.0};
   for (int i = 0; i < chunks; ++i) {
