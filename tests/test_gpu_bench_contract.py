@@ -54,7 +54,8 @@ def test_reference_arm_line_contract():
     assert d["cpu_baseline"]["kind"] in ("reference", "port")
 
 
-def test_bench_gpus2_launches_two_ranks_and_matches_oracle(tmp_path):
+@pytest.mark.parametrize("gpus", [2, 4])
+def test_bench_gpus2_launches_two_ranks_and_matches_oracle(tmp_path, gpus):
     """`bench.py --gpus 2` outside torchrun starts two ranks itself (gloo here:
     the box has one GPU, both ranks share it); the line reports n_gpus 2, the
     one-time B broadcast apart from the step, and the two C shards together
@@ -64,7 +65,7 @@ def test_bench_gpus2_launches_two_ranks_and_matches_oracle(tmp_path):
     env = dict(os.environ, GESPMM_DIST_BACKEND="gloo")
     env.pop("WORLD_SIZE", None)
     dump = str(tmp_path / "c")
-    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2",
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", str(gpus),
                           "--config", "pubmed", "--steps", "3", "--warmup", "3", "--no-cpu",
                           "--dump-c", dump], cwd=ROOT, capture_output=True, text=True,
                          timeout=900, env=env)
@@ -72,11 +73,11 @@ def test_bench_gpus2_launches_two_ranks_and_matches_oracle(tmp_path):
     lines = [ln for ln in out.stdout.splitlines() if ln.strip().startswith("{")]
     assert len(lines) == 1, out.stdout
     d = json.loads(lines[0])
-    assert d["n_gpus"] == 2 and d["config"]["parallelism"] == "row-shard x2"
+    assert d["n_gpus"] == gpus and d["config"]["parallelism"] == f"row-shard x{gpus}"
     assert d["setup"]["b_broadcast_bytes"] == 19717 * 128 * 4 and d["setup"]["backend"] == "gloo"
     bounds = json.load(open(dump + ".bounds.json"))["bounds"]
-    assert len(bounds) == 3 and bounds[0] == 0 and bounds[-1] == 19717
-    got = np.concatenate([np.load(f"{dump}.rank{r}.npy") for r in range(2)])
+    assert len(bounds) == gpus + 1 and bounds[0] == 0 and bounds[-1] == 19717
+    got = np.concatenate([np.load(f"{dump}.rank{r}.npy") for r in range(gpus)])
     rp, ci, v = O.ref_gen_uniform(19717, 88648, 1)
     v = np.ascontiguousarray(v, np.float32)
     O.randomize_values(v, 2)
