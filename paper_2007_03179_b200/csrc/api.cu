@@ -174,6 +174,16 @@ struct Plan {
   double mean_degree = 0.0;
   ClusterHot ch;             // cluster-DSMEM hot-row cache (o.cluster_hot), col_ind copy
   HotRows hr;                // relocated hot rows (o.hot_rows_mb), col_ind copy
+  // Split hub rows (max/min, or fast-mode sum/mean): each hub row's nonzeros
+  // cut into segments of seg_len, folded by k_warp into partial rows, then
+  // combined in segment order (k_split_combine) instead of the k_hub ring.
+  bool split = false;
+  uint32_t seg_len = 0, n_seg = 0, n_vrows = 0;
+  uint32_t* d_vptr = nullptr;       // virtual row_ptr over segments
+  uint32_t* d_seg_order = nullptr;  // the segments' virtual rows
+  uint32_t* d_hubs = nullptr;       // per hub row: (row, first virtual row, segments)
+  float* d_part = nullptr;          // partial rows [n_vrows][n]
+  int32_t* d_part_arg = nullptr;    // their arg (max/min)
 
   ~Plan() {
 #ifdef GESPMM_EXPERIMENTAL
@@ -184,6 +194,10 @@ struct Plan {
 #endif
     if (d_order) cudaFree(d_order);
     if (d_work) cudaFree(d_work);
+    for (void* q : {static_cast<void*>(d_vptr), static_cast<void*>(d_seg_order),
+                    static_cast<void*>(d_hubs), static_cast<void*>(d_part),
+                    static_cast<void*>(d_part_arg)})
+      if (q) cudaFree(q);
     if (d_hot) cudaFree(d_hot);
     if (ev_fork) cudaEventDestroy(ev_fork);
     if (ev_join) cudaEventDestroy(ev_join);
@@ -337,7 +351,8 @@ gespmm_status_t launch_tuned_rows(const TunedShapes& t, int op, bool fast, const
                                   const uint32_t* order, uint32_t n_hub, uint32_t n_rest,
                                   cudaStream_t st, cudaStream_t side, cudaEvent_t fork,
                                   cudaEvent_t join, const cudaAccessPolicyWindow* winp,
-                                  bool hub_pdl, uint32_t* work, bool chain = false) {
+                                  bool hub_pdl, uint32_t* work, bool chain = false,
+                                  bool pdl_overlap = false) {
   SpmmArgs a = a0;
   // overlap_prev: only a single-kernel execute chains onto the previous kernel
   chain = chain && n_hub == 0 && t.slices == 1;
@@ -417,10 +432,28 @@ gespmm_status_t launch_tuned_rows(const TunedShapes& t, int op, bool fast, const
     sa.n_tiles = (w + wsel.tile_width() - 1) / wsel.tile_width();
     sa.pdl_wait = chain ? 1 : 0;
     if (n_rest)
-      GESPMM_CUDA(launch_tuned_warp(wsel, op, fast, sa, st, winp, hub_then_pdl || chain), "spmm");
+      GESPMM_CUDA(launch_tuned_warp(wsel, op, fast, sa, st, winp,
+                                    hub_then_pdl || chain || pdl_overlap), "spmm");
     if (side_used) GESPMM_CUDA(cudaStreamWaitEvent(st, join, 0), "spmm");
   }
   return GESPMM_OK;
+}
+
+// Split hub rows instead of the k_hub ring when the fold does not depend on
+// the order of its partial results: max/min (strict compare + earliest
+// position among ties = the sequential fold's result) always; sum/mean only
+// in fast mode (the partial sums reassociate the fold within the tolerance).
+// Not with the SkipTail fault hook (per-row tail) or column slices.
+// GESPMM_HUB_SPLIT=0 keeps the ring (A/B).
+bool split_eligible(const Plan& p) {
+  static const bool off = [] {
+    const char* e = std::getenv("GESPMM_HUB_SPLIT");
+    return e && e[0] == '0';
+  }();
+  if (off || p.o.fault_skip_tail || p.sh.slices != 1 || p.o.variant != GESPMM_VARIANT_TUNED)
+    return false;
+  if (p.op == GESPMM_MAX || p.op == GESPMM_MIN) return true;
+  return p.o.exact == 0;
 }
 
 // Inspector: degree-descending row schedule (stable counting sort) so heavy
@@ -460,6 +493,40 @@ gespmm_status_t build_tuned(Plan& p, const uint32_t* host_rp, cudaStream_t st) {
   while (n_hub < m && deg[order[n_hub]] >= p.hub_threshold) hub_nnz += deg[order[n_hub++]];
   p.n_hub = n_hub;
   p.hub_pdl = host_rp[m] && double(hub_nnz) >= kHubPdlShare * double(host_rp[m]);
+  if (n_hub && split_eligible(p)) {
+    // segments of at most half the hub threshold: each one's single-warp time
+    // is then at most half of what made a row a hub row
+    const uint32_t t = p.hub_threshold == 0xffffffffu ? 4096u : p.hub_threshold;
+    p.seg_len = std::max<uint32_t>(256, (t / 2 + 63) & ~63u);
+    std::vector<uint32_t> vptr, seg, hubs;
+    for (uint32_t i = 0; i < n_hub; ++i) {
+      const uint32_t r = order[i], d = deg[r];
+      const uint32_t k = (d + p.seg_len - 1) / p.seg_len;
+      const uint32_t base = uint32_t(vptr.size());
+      for (uint32_t j = 0; j <= k; ++j) vptr.push_back(host_rp[r] + std::min(j * p.seg_len, d));
+      for (uint32_t j = 0; j < k; ++j) seg.push_back(base + j);
+      hubs.insert(hubs.end(), {r, base, k});
+    }
+    p.split = true;
+    p.n_seg = uint32_t(seg.size());
+    p.n_vrows = uint32_t(vptr.size());
+    const bool arg_op = p.op == GESPMM_MAX || p.op == GESPMM_MIN;
+    const auto up = [&](uint32_t** dst, const std::vector<uint32_t>& v) {
+      cudaError_t e = cudaMalloc(reinterpret_cast<void**>(dst), sizeof(uint32_t) * v.size());
+      if (e == cudaSuccess)
+        e = cudaMemcpyAsync(*dst, v.data(), sizeof(uint32_t) * v.size(), cudaMemcpyHostToDevice, st);
+      return e;
+    };
+    GESPMM_CUDA(up(&p.d_vptr, vptr), "plan_create");
+    GESPMM_CUDA(up(&p.d_seg_order, seg), "plan_create");
+    GESPMM_CUDA(up(&p.d_hubs, hubs), "plan_create");
+    GESPMM_CUDA(cudaMalloc(reinterpret_cast<void**>(&p.d_part),
+                           sizeof(float) * size_t(p.n_vrows) * p.n), "plan_create");
+    if (arg_op)
+      GESPMM_CUDA(cudaMalloc(reinterpret_cast<void**>(&p.d_part_arg),
+                             sizeof(int32_t) * size_t(p.n_vrows) * p.n), "plan_create");
+    GESPMM_CUDA(cudaStreamSynchronize(st), "plan_create");
+  }
 
   // Rows of at most two staged chunks gain nothing from the LPT schedule:
   // the identity order saves the schedule load in front of every row.
@@ -542,6 +609,11 @@ gespmm_status_t build_tuned(Plan& p, const uint32_t* host_rp, cudaStream_t st) {
   }
   if (p.sh.slices > 1 && size_t(len) < sizeof buf)
     std::snprintf(buf + len, sizeof buf - size_t(len), "; %u column slices of %u", p.sh.slices, sw);
+  len = int(std::strlen(buf));
+  if (p.split && size_t(len) < sizeof buf)
+    std::snprintf(buf + len, sizeof buf - size_t(len),
+                  "; hub rows split: %u segments of <= %u nonzeros, ordered combine", p.n_seg,
+                  p.seg_len);
   p.desc = buf;
   return GESPMM_OK;
 }
@@ -696,6 +768,32 @@ gespmm_status_t plan_execute_impl(Plan& p, const float* b, float* c, int32_t* ar
       GESPMM_CUDA(resolve_range_policy(b_hot, args.hot_bytes, mode, &args.pol_hot, st), "spmm");
   }
 #endif
+  if (p.split) {
+    // the hub rows' segments first (equal-length work units, the long pole of
+    // the row schedule) into partial rows; the rows below the threshold (LPT
+    // order) follow as a programmatic dependent launch (disjoint outputs,
+    // both run together); then the ordered combine (a normal launch: after
+    // both).  Rest-first put the segments behind the whole rest grid (its
+    // last CTA triggers the dependent launch): products 8 shards 1.81 ms.
+    SpmmArgs sg = args;
+    sg.row_ptr = p.d_vptr;
+    sg.c = p.d_part;
+    sg.arg = args.arg ? p.d_part_arg : nullptr;
+    sg.ld = p.n;
+    sg.n_peer = 0;
+    sg.c_mc = nullptr;
+    sg.arg_mc = nullptr;
+    const int seg_op = p.op == GESPMM_MEAN ? GESPMM_SUM : p.op;  // mean divides in the combine
+    gespmm_status_t s2 = launch_tuned_rows(p.sh, seg_op, fast, sg, p.d_seg_order, 0, p.n_seg, st,
+                                           nullptr, nullptr, nullptr, winp, false, nullptr);
+    if (s2 != GESPMM_OK) return s2;
+    s2 = launch_tuned_rows(p.sh, p.op, fast, args, p.d_order + p.n_hub, 0, p.a.n_rows - p.n_hub,
+                           st, nullptr, nullptr, nullptr, winp, false, nullptr, false, true);
+    if (s2 != GESPMM_OK) return s2;
+    GESPMM_CUDA(launch_split_combine(p.op, args, p.d_hubs, p.n_hub, p.d_part,
+                                     args.arg ? p.d_part_arg : nullptr, st), "spmm");
+    return GESPMM_OK;
+  }
   return launch_tuned_rows(p.sh, p.op, fast, args, p.d_order, p.n_hub, p.a.n_rows - p.n_hub, st,
                            p.side, p.ev_fork, p.ev_join, winp, p.hub_pdl, p.d_work,
                            p.o.overlap_prev != 0 && !winp);
@@ -983,6 +1081,7 @@ int32_t gespmm_plan_launches(gespmm_plan_t plan) {
   // the same branches as plan_execute_impl / launch_tuned_rows: one cluster
   // launch, or per column slice a hub launch and a warp launch
   if (p->ch.col_ind) return 1;
+  if (p->split) return (p->a.n_rows > p->n_hub ? 1 : 0) + 2;  // rows, segments, combine
   const int32_t per_slice = (p->n_hub ? 1 : 0) + (p->a.n_rows > p->n_hub ? 1 : 0);
   return per_slice * int32_t(p->sh.slices) + (p->hr.n_hot ? 1 : 0);  // + the hot-row refresh
 }

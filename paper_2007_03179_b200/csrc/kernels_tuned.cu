@@ -1212,6 +1212,52 @@ __global__ void k_policies(int hints, uint64_t* out) {
   out[2] = p.stream;
 }
 
+// Split hub rows (order-insensitive folds): a hub row's nonzeros were cut into
+// segments, each folded by k_warp into its own partial row (value, and the
+// position of the element that last replaced it for max/min).  One thread per
+// (hub row, column) folds the partials in segment order — for max/min with
+// the fold's own strict compare, so the earliest position among equal maxima
+// survives and the result is bit-identical to the sequential fold; for sum /
+// mean (fast mode only) in segment order (a different, tolerance-level
+// rounding).  Then the row's epilogue: mean's division, C, arg, replicas.
+// hubs[3h..3h+2] = (row, first partial row, partial rows).
+template <int OP>
+__global__ void __launch_bounds__(256) k_split_combine(SpmmArgs a, const uint32_t* __restrict__ hubs,
+                                                       uint32_t n_hub, const float* __restrict__ part,
+                                                       const int32_t* __restrict__ part_arg) {
+  using R = Reduce<OP>;
+  const uint64_t total = uint64_t(n_hub) * a.n;
+  for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
+       i += uint64_t(gridDim.x) * blockDim.x) {
+    const uint32_t h = uint32_t(i / a.n), col = uint32_t(i - uint64_t(h) * a.n);
+    const uint32_t row = hubs[3 * h], v0 = hubs[3 * h + 1], k = hubs[3 * h + 2];
+    float acc = R::init();
+    int32_t who = -1;
+    for (uint32_t j = 0; j < k; ++j) {
+      const uint64_t q = uint64_t(v0 + j) * a.n + col;
+      const float x = part[q];
+      if constexpr (OP == kSum || OP == kMean) {
+        acc = __fadd_rn(acc, x);
+      } else if constexpr (OP == kMax) {
+        if (acc < x) {
+          acc = x;
+          who = part_arg[q];
+        }
+      } else {
+        if (x < acc) {
+          acc = x;
+          who = part_arg[q];
+        }
+      }
+    }
+    const float out = finish<OP>(acc, a.row_ptr[row + 1] - a.row_ptr[row]);
+    const uint64_t o = uint64_t(row) * a.ld + col;
+    a.c[o] = out;
+    if (R::kHasArg && a.arg) a.arg[o] = who;
+    if (a.n_peer || a.c_mc) store_replicas<1, R::kHasArg>(a, o, &out, &who);
+  }
+}
+
 }  // namespace
 
 cudaError_t resolve_range_policy(const void* base, uint32_t bytes, int mode, uint64_t* out,
@@ -1415,6 +1461,22 @@ cudaError_t launch_tuned_hub(int op, bool fast, const SpmmArgs& a, cudaStream_t 
     case kMax: return hub_dispatch<kMax, false>(v, c, big, a, st);
     default: return hub_dispatch<kMin, false>(v, c, big, a, st);
   }
+}
+
+cudaError_t launch_split_combine(int op, const SpmmArgs& a, const uint32_t* hubs, uint32_t n_hub,
+                                 const float* part, const int32_t* part_arg, cudaStream_t st) {
+  if (!n_hub || !a.n) return cudaSuccess;
+  const uint64_t total = uint64_t(n_hub) * a.n;
+  const uint64_t want = (total + 255) / 256;
+  const uint32_t g = uint32_t(want < 148 * 8 ? want : 148 * 8);
+  switch (op) {
+    case kSum: k_split_combine<kSum><<<g, 256, 0, st>>>(a, hubs, n_hub, part, part_arg); break;
+    case kMean: k_split_combine<kMean><<<g, 256, 0, st>>>(a, hubs, n_hub, part, part_arg); break;
+    case kMax: k_split_combine<kMax><<<g, 256, 0, st>>>(a, hubs, n_hub, part, part_arg); break;
+    default: k_split_combine<kMin><<<g, 256, 0, st>>>(a, hubs, n_hub, part, part_arg); break;
+  }
+  note_launch();
+  return cudaGetLastError();
 }
 
 cudaError_t launch_tuned_cta(const CtaShape& s, int op, bool fast, const SpmmArgs& a,

@@ -68,6 +68,10 @@ uint32_t hub_tile_width(uint32_t n, uint32_t n_hub);
 // big: the 64 KB / 32-per-stage ring (hub kernel ahead of the warp kernel) or
 // the 32 KB / 16-per-stage one (side job next to it).
 cudaError_t launch_tuned_hub(int op, bool fast, const SpmmArgs& a, cudaStream_t st, bool big);
+// Split hub rows: fold each hub row's segment partials (k_warp outputs) in
+// segment order into C / arg (+ replicas); hubs = (row, first partial, count).
+cudaError_t launch_split_combine(int op, const SpmmArgs& a, const uint32_t* hubs, uint32_t n_hub,
+                                 const float* part, const int32_t* part_arg, cudaStream_t st);
 
 // --- frequency-aware L2 policy (hotcols.cu) ---
 struct HotStats {

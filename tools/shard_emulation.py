@@ -37,6 +37,7 @@ def main():
     p.add_argument("--reps", type=int, default=7)
     p.add_argument("--json", default=None)
     p.add_argument("--only-shard", type=int, default=None, help="time only this shard index")
+    p.add_argument("--fast", action="store_true", help="fast mode (FFMA sum, split hub rows)")
     args = p.parse_args()
     cfg = bench.CONFIGS[args.config]
     dev = torch.device("cuda", 0)
@@ -44,7 +45,7 @@ def main():
     n, op, want_arg = cfg["n"], cfg["op"], bool(cfg.get("arg"))
     b = torch.from_numpy(G.make_random_dense(a.n_cols, n, bench.B_SEED).data).to(dev)
     flush = torch.empty(128 * 1024 * 1024, dtype=torch.float32, device=dev)  # 512 MB
-    ex = G.ExecOptions(hub_threshold=args.hub_threshold)
+    ex = G.ExecOptions(hub_threshold=args.hub_threshold, exact=not args.fast)
     flops = 2 * a.nnz() * n
     out = {"config": args.config, "hub_threshold": args.hub_threshold, "runs": []}
     base = None
