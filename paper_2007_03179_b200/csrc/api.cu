@@ -406,11 +406,23 @@ gespmm_status_t launch_tuned_rows(const TunedShapes& t, int op, bool fast, const
                        aligned(sa.c, 16) && (!sa.arg || aligned(sa.arg, 16));
       const uint32_t tw = tma ? hub_tile_width(w, n_hub) : uint32_t(cs.vec * cs.warps * 32);
       h.n_tiles = (w + tw - 1) / tw;
+      // When the hub rows carry the launch (>= kHubPdlShare of its nonzeros:
+      // a 1/4 or 1/8 row shard of a power-law graph), the hub kernel runs
+      // first and alone, one CTA per unit, and the warp kernel follows in
+      // stream order.  Round 1 ran them together (the warp kernel as a
+      // programmatic dependent launch, the hub kernel capped at 2 persistent
+      // CTAs per SM); measured in round 2 (tools/r2_hubseq.sh, Reddit N=128,
+      // emulated shards): 4 shards 0.973 -> 0.833 ms, 8 shards 0.526 ->
+      // 0.499 ms — the ring's 128 KB of shared memory per SM took L1 and
+      // occupancy from the warp kernel next to it.  GESPMM_HUB_SEQ=0 restores
+      // the overlapped launch.
+      static const bool hub_seq = [] {
+        const char* e = std::getenv("GESPMM_HUB_SEQ");
+        return !(e && e[0] == '0');
+      }();
       if (tma && (hub_pdl || !side)) {
-        // same stream; the warp kernel follows as a programmatic dependent
-        // launch, so the hub CTAs are resident first and both run together
         GESPMM_CUDA(launch_tuned_hub(op, fast, h, st, true), "spmm");
-        hub_then_pdl = true;
+        hub_then_pdl = !hub_seq;
       } else {
         cudaStream_t hs = side ? side : st;
         if (side) {

@@ -1144,12 +1144,16 @@ cudaError_t hub_dispatch(int vec, int cons, bool big, const SpmmArgs& a0, cudaSt
   if (units == 0) return cudaSuccess;
   if (units > 0x7fffffffull) return cudaErrorInvalidConfiguration;
   SpmmArgs a = a0;
-  // persistent: kHubCtasPerSm CTAs per SM at most, so the warp kernel running
-  // alongside keeps most of each SM (GESPMM_HUB_PERSIST=0: one CTA per unit)
-  static const int per_sm = [] {
+  // persistent: at most 2 CTAs per SM when the hub kernel runs next to the
+  // warp kernel (side job), so the warp kernel keeps most of each SM; one CTA
+  // per unit (as many as fit) when it runs alone ahead of it (big: the hub
+  // rows carry the launch).  GESPMM_HUB_PERSIST=n forces n per SM (0 = one
+  // CTA per unit) in both modes.
+  static const int per_sm_env = [] {
     const char* e = std::getenv("GESPMM_HUB_PERSIST");
-    return e ? std::atoi(e) : 2;
+    return e ? std::atoi(e) : -1;
   }();
+  const int per_sm = per_sm_env >= 0 ? per_sm_env : (big ? 0 : 2);
   uint64_t blocks = units;
   if (per_sm > 0) {
     const cudaError_t ec = a0.work ? cudaMemsetAsync(a.work, 0, sizeof(uint32_t), st)
