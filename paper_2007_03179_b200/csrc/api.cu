@@ -456,10 +456,10 @@ gespmm_status_t launch_tuned_rows(const TunedShapes& t, int op, bool fast, const
 // position among ties = the sequential fold's result) always; sum/mean only
 // in fast mode (the partial sums reassociate the fold within the tolerance).
 // Not with the SkipTail fault hook (per-row tail) or column slices.
-// GESPMM_HUB_SPLIT=0 keeps the ring (A/B).
+// GESPMM_HUB_SEGMENTS=0 keeps the ring (A/B).
 bool split_eligible(const Plan& p) {
   static const bool off = [] {
-    const char* e = std::getenv("GESPMM_HUB_SPLIT");
+    const char* e = std::getenv("GESPMM_HUB_SEGMENTS");
     return e && e[0] == '0';
   }();
   if (off || p.o.fault_skip_tail || p.sh.slices != 1 || p.o.variant != GESPMM_VARIANT_TUNED)

@@ -1456,6 +1456,11 @@ uint32_t hub_tile_width(uint32_t n, uint32_t n_hub) {
 }
 
 cudaError_t launch_tuned_hub(int op, bool fast, const SpmmArgs& a, cudaStream_t st, bool big) {
+  static const int big_env = [] {  // GESPMM_HUB_BIG=0/1: ring geometry A/B
+    const char* e = std::getenv("GESPMM_HUB_BIG");
+    return e ? std::atoi(e) : -1;
+  }();
+  if (big_env >= 0) big = big_env != 0;
   const int w = hub_vec(a.n, a.n_sched);  // tile = 32 * w columns
   const int c = hub_split(w, big);
   const int v = w / c;
