@@ -91,9 +91,11 @@ def test_random_shapes_every_path_bit_exact(m, k, density, long_row, n, op, colu
        slices=st.sampled_from([0, 1, 2, 5]), tuned_cf=st.sampled_from([0, 1, 2, 4]),
        hot=st.sampled_from([0, 1]), replicas=st.sampled_from([1, 1, 3]),
        misalign=st.booleans(), exact=st.sampled_from([True, True, False]),
-       cluster=st.sampled_from([0, 0, 0, 2, 8]), data=st.integers(0, 1 << 30))
+       cluster=st.sampled_from([0, 0, 0, 2, 8]), overlap=st.booleans(),
+       data=st.integers(0, 1 << 30))
 def test_random_device_plans_bit_exact(m, k, density, long_row, n, op, column_arg, hub, rpw, slices,
-                                       tuned_cf, hot, replicas, misalign, exact, cluster, data):
+                                       tuned_cf, hot, replicas, misalign, exact, cluster, overlap,
+                                       data):
     """Device plans (tuned) over random shapes and options, executed plain or
     with the fused all-gather epilogue into extra replicas; B/C based 4 bytes
     off 16-byte alignment (scalar fallbacks); the cluster-DSMEM cache at N=128;
@@ -108,7 +110,7 @@ def test_random_device_plans_bit_exact(m, k, density, long_row, n, op, column_ar
             f.write(repr(dict(plan=1, m=m, k=k, density=density, long_row=long_row, n=n, op=op,
                               column_arg=column_arg, hub=hub, rpw=rpw, slices=slices,
                               tuned_cf=tuned_cf, hot=hot, replicas=replicas, misalign=misalign,
-                              exact=exact, cluster=cluster, data=data)) + "\n")
+                              exact=exact, cluster=cluster, overlap=overlap, data=data)) + "\n")
     rng = np.random.default_rng(data)
     a = _matrix(rng, m, k, density, long_row)
     b = G.make_random_dense(k, n, data + 1)
@@ -128,7 +130,7 @@ def test_random_device_plans_bit_exact(m, k, density, long_row, n, op, column_ar
     fast = not exact and op in ("sum", "mean")
     ex = G.ExecOptions(arg_kind="column" if column_arg else "edge", hub_threshold=hub,
                        rows_per_warp=rpw, col_slices=slices, tuned_cf=tuned_cf, l2_hot_mb=hot,
-                       exact=not fast, cluster_hot=cluster)
+                       exact=not fast, cluster_hot=cluster, overlap_prev=overlap)
     plan = G.Plan(d, n, op, exec=ex)
     cs = [buf((m, n), -3.0) for _ in range(replicas)]
     args = [buf((m, n), -5, torch.int32) for _ in range(replicas)] if want_arg else None
@@ -242,3 +244,45 @@ def test_random_transpose_matches_numpy_and_round_trips(m, k, density, long_row,
     assert np.array_equal(back.row_ptr, a.row_ptr)
     assert np.array_equal(back.col_ind[:a.nnz()], a.col_ind)
     assert np.array_equal(back.vals[:a.nnz()].view(np.uint32), a.vals.view(np.uint32))
+
+
+@seed(20261021)
+@settings(max_examples=int(os.environ.get("FUZZ_EXAMPLES", "60")), deadline=None,
+          suppress_health_check=[HealthCheck.too_slow])
+@given(rows=st.integers(0, 400), cols=st.integers(1, 5000), count=st.integers(0, 20000),
+       dup=st.floats(0.0, 0.9), policy=st.sampled_from(["sum", "last"]), bad=st.booleans(),
+       data=st.integers(0, 1 << 30))
+def test_random_from_coo_device_equals_host(rows, cols, count, dup, policy, bad, data):
+    """gespmm_from_coo_device on random triples (duplicate runs of any length,
+    empty rows, an out-of-bounds triple): the same CSR, bit for bit, or the
+    same error text, as the host from_coo (itself pinned to the reference's,
+    tests/test_host_api.py)."""
+    import torch
+    rng = np.random.default_rng(data)
+    if rows == 0:
+        count = 0
+    r = rng.integers(0, max(rows, 1), count).astype(np.uint32)
+    c = rng.integers(0, cols, count).astype(np.uint32)
+    if count and dup > 0:  # copy earlier coordinates forward: duplicate runs
+        idx = np.nonzero(rng.random(count) < dup)[0]
+        src = (rng.random(len(idx)) * np.maximum(idx, 1)).astype(np.int64)
+        r[idx], c[idx] = r[src], c[src]
+    v = rng.standard_normal(count).astype(np.float32)
+    if bad and count:
+        i = int(rng.integers(0, count))
+        if rng.random() < 0.5:
+            r[i] = rows + int(rng.integers(0, 7))
+        else:
+            c[i] = cols + int(rng.integers(0, 7))
+    t = lambda x: torch.from_numpy(x.view(np.int32) if x.dtype == np.uint32 else x).cuda()  # noqa: E731
+    try:
+        want = G.from_coo(rows, cols, (r, c, v), policy)
+    except G.Error as e:
+        with pytest.raises(G.Error) as ei:
+            G.DeviceCsr.from_coo(rows, cols, t(r), t(c), t(v), policy=policy)
+        assert str(ei.value) == str(e)
+        return
+    got = G.DeviceCsr.from_coo(rows, cols, t(r), t(c), t(v), policy=policy)
+    assert np.array_equal(got.row_ptr.cpu().numpy().view(np.uint32), want.row_ptr)
+    assert np.array_equal(got.col_ind.cpu().numpy().view(np.uint32), want.col_ind)
+    assert np.array_equal(got.vals.cpu().numpy().view(np.uint32), want.vals.view(np.uint32))
