@@ -519,10 +519,16 @@ constexpr int kHubProducers = GESPMM_HUB_PRODUCERS;  // producer (LDGSTS) warps
 // round trips per nonzero (8-way Reddit shard 0.69 -> 0.58 ms) but the larger
 // ring takes L1 capacity from a warp kernel running alongside (2-way shard 1.63
 // -> 1.82 ms, products 4-way 3.69 -> 4.01 ms; profiles/r1_shard_emulation.md).
+#ifndef GESPMM_HUB_BIG_GROUP
+#define GESPMM_HUB_BIG_GROUP 32  // A/B builds: nonzeros per stage of the big ring
+#endif
+#ifndef GESPMM_HUB_BIG_KB
+#define GESPMM_HUB_BIG_KB 64
+#endif
 template <bool BIG>
 struct HubRing {
-  static constexpr int GROUP = BIG ? 32 : 16;       // nonzeros per stage (one full/empty pair)
-  static constexpr int BYTES = (BIG ? 64 : 32) * 1024;
+  static constexpr int GROUP = BIG ? GESPMM_HUB_BIG_GROUP : 16;  // nonzeros per stage (one full/empty pair)
+  static constexpr int BYTES = (BIG ? GESPMM_HUB_BIG_KB : 32) * 1024;
 };
 
 template <int VEC, bool BIG, int C>
