@@ -179,7 +179,11 @@ gespmm_status_t gespmm_plan_create(const gespmm_csr_t* a, uint32_t n, gespmm_red
                                    const gespmm_options_t* opts, void* stream,
                                    gespmm_plan_t* out);
 /* Executions of one plan must not overlap on different streams (the plan owns
- * its side stream, events and work counters); use one plan per stream. */
+ * its side stream, events, work counters and, for split hub rows, the
+ * partial-row buffer); use one plan per stream.  A plan whose op is max/min,
+ * or sum/mean with exact = 0, splits rows at or above its hub threshold into
+ * segments folded into partial rows and combines them in order (bit-exact for
+ * max/min, arg included); exact sum/mean keep the row-per-CTA ring. */
 gespmm_status_t gespmm_plan_execute(gespmm_plan_t plan, const float* b, float* c, int32_t* arg,
                                     void* stream);
 /* Human-readable description of the chosen shape (static storage per plan). */
