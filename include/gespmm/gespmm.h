@@ -369,6 +369,12 @@ gespmm_status_t gespmm_gen_powerlaw(uint32_t rows, uint64_t nnz_target, uint32_t
                                     double exponent, uint64_t seed, int32_t threads,
                                     uint32_t* row_ptr, uint32_t* col_ind, float* vals);
 
+/* Frees the library's grow-only scratch on the current device — the host
+ * entry's staging buffers (pinned host + device, sized to the largest call so
+ * far) and the COO builder's temporaries (~28 B per triple) — once no call is
+ * in flight on it.  The next call reallocates what it needs. */
+void gespmm_release_workspace(void);
+
 /* Library / device facts for reports. */
 int32_t gespmm_abi_version(void);
 #define GESPMM_BUILD_EXPERIMENTAL 1

@@ -11,7 +11,7 @@ from .api import (  # noqa: F401
     gen_uniform_random, make_random_dense, native_spmm, native_spmm_arg, ops,
     randomize_values, reduce_op_by_name, select_variant, spmm, variant_by_name,
     save_csr_cache, read_csr_cache, load_matrix, to_coo, ValidationReport, validate,
-    require_canonical, parse_matrix_market,
+    require_canonical, parse_matrix_market, release_workspace,
 )
 from ._lib import LIB_PATH, experimental_built, launch_count  # noqa: F401
 

@@ -46,6 +46,7 @@ EXPORTS = [
     "gespmm_ipc_open_handle", "gespmm_ipc_close", "gespmm_multicast_alloc",
     "gespmm_multicast_free", "gespmm_build_flags", "gespmm_from_coo", "gespmm_validate_host",
     "gespmm_mtx_parse", "gespmm_from_coo_device", "gespmm_to_coo_device",
+    "gespmm_release_workspace",
 ]
 BUILD_EXPERIMENTAL = 1
 MAX_GATHER_DSTS = 8
@@ -165,6 +166,8 @@ def lib():
         L.gespmm_from_coo_device.restype = C.c_int
         L.gespmm_to_coo_device.argtypes = [C.POINTER(Csr), vp, vp, vp, vp]
         L.gespmm_to_coo_device.restype = C.c_int
+        L.gespmm_release_workspace.argtypes = []
+        L.gespmm_release_workspace.restype = None
         L.gespmm_csr1_write.argtypes = [C.c_char_p, C.POINTER(Csr)]
         L.gespmm_csr1_write.restype = C.c_int
         L.gespmm_csr1_header.argtypes = [C.c_char_p, C.POINTER(u32), C.POINTER(u32),

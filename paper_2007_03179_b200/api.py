@@ -707,6 +707,12 @@ def _stream_ptr(stream=None) -> Optional[int]:
     return s.cuda_stream
 
 
+def release_workspace():
+    """gespmm_release_workspace: free the library's grow-only scratch (host
+    entry staging, COO builder temporaries) on the current device."""
+    lib().gespmm_release_workspace()
+
+
 def spmm(a: DeviceCsr, b, op: ReduceOp | str = "sum", want_arg: bool = False,
          variant: KernelVariant = KernelVariant.tuned(), exec: ExecOptions = ExecOptions(),
          validate: bool = True, out=None, stream=None):

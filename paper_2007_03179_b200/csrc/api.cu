@@ -913,6 +913,32 @@ Workspace* workspace() {
   return g_ws[dev];
 }
 
+// Frees the host entry's grow-only buffers of the current device (the next
+// call reallocates them).
+void release_host_workspace() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  Workspace* w = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(g_ws_mu);
+    if (dev >= 0 && dev < 64) w = g_ws[dev];
+  }
+  if (!w) return;
+  std::lock_guard<std::mutex> lk(w->mu);  // no host-entry call in flight on this device
+  for (int i = 0; i < 13; ++i)
+    if (w->buf[i]) {
+      cudaFree(w->buf[i]);
+      w->buf[i] = nullptr;
+      w->cap[i] = 0;
+    }
+  for (int i = 0; i < 4; ++i)
+    if (w->hbuf[i]) {
+      cudaFreeHost(w->hbuf[i]);
+      w->hbuf[i] = nullptr;
+      w->hcap[i] = 0;
+    }
+}
+
 // GESPMM_TRACE=1: host-side phase timestamps of the host entry point (stderr).
 // NVTX range for the lifetime of a scope (nsys / ncu --nvtx timelines)
 struct NvtxRange {
@@ -1005,6 +1031,11 @@ void gespmm_options_default(gespmm_options_t* o) {
 const char* gespmm_last_error(void) { return t_err.c_str(); }
 
 int32_t gespmm_abi_version(void) { return GESPMM_ABI_VERSION; }
+
+void gespmm_release_workspace(void) {
+  release_host_workspace();
+  release_coo_scratch();
+}
 
 int32_t gespmm_build_flags(void) {
 #ifdef GESPMM_EXPERIMENTAL

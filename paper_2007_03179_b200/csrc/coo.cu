@@ -127,6 +127,25 @@ CooScratch* coo_scratch() {
   return g_coo[dev];
 }
 
+}  // namespace
+
+void release_coo_scratch() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  CooScratch* s = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(g_coo_mu);
+    if (dev >= 0 && dev < 64) s = g_coo[dev];
+  }
+  if (!s) return;
+  std::lock_guard<std::mutex> lk(s->mu);
+  if (s->buf) cudaFree(s->buf);
+  s->buf = nullptr;
+  s->cap = 0;
+}
+
+namespace {
+
 // carves aligned pieces out of one buffer
 struct Carve {
   char* base;

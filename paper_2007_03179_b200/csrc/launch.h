@@ -135,6 +135,8 @@ int pack_threads();
 // host entry: the packing threads poll `streams` until they drain (idle host
 // cores slow the tail copies on the boxes; h2dpack_host.cpp)
 void host_poll(void* const* streams, int n);
+// gespmm_release_workspace's halves (api.cu, coo.cu)
+void release_coo_scratch();
 // rows [0, m_block) of row_ptr_block own positions [ps, pe); bits: zeroed
 // row-start bitmap over all nnz positions (shared with the column check).
 // bad_key (nullable): also check the rebuilt columns (bounds k_cols, strictly

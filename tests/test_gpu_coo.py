@@ -77,3 +77,24 @@ def test_from_coo_device_rebuilds_the_benchmark_graph():
                                 v[perm].contiguous())
     _check(back, np.asarray(a.row_ptr, np.uint32), np.asarray(a.col_ind, np.uint32),
            np.asarray(a.vals, np.float32))
+
+
+@needs_ref
+def test_release_workspace_between_calls():
+    """gespmm_release_workspace frees the COO scratch and the host entry's
+    staging; the next calls reallocate and stay bit-exact."""
+    rng = np.random.default_rng(9)
+    r = rng.integers(0, 500, 40000).astype(np.uint32)
+    c = rng.integers(0, 700, 40000).astype(np.uint32)
+    v = rng.standard_normal(40000).astype(np.float32)
+    wrp, wci, wv = O.ref_from_coo(500, 700, r, c, v)
+    a = G.gen_powerlaw(3000, 200000, 2900, 1.0, 12)
+    G.randomize_values(a, 13)
+    b = G.make_random_dense(3000, 64, 14)
+    want, _ = O.spmm(a.n_rows, a.n_cols, a.row_ptr, a.col_ind, a.vals, b.data, "sum")
+    for _ in range(2):
+        _check(G.DeviceCsr.from_coo(500, 700, *_dev(r, c, v)), wrp, wci, wv)
+        got = G.native_spmm(a, b, G.KernelVariant.tuned(), G.ops.sum(),
+                            exec=G.ExecOptions(h2d_pack=1))
+        assert np.array_equal(got.data.view(np.uint32), want.view(np.uint32))
+        G.release_workspace()
