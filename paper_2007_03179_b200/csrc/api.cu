@@ -925,13 +925,13 @@ void release_host_workspace() {
   }
   if (!w) return;
   std::lock_guard<std::mutex> lk(w->mu);  // no host-entry call in flight on this device
-  for (int i = 0; i < 13; ++i)
+  for (size_t i = 0; i < sizeof(w->buf) / sizeof(w->buf[0]); ++i)
     if (w->buf[i]) {
       cudaFree(w->buf[i]);
       w->buf[i] = nullptr;
       w->cap[i] = 0;
     }
-  for (int i = 0; i < 4; ++i)
+  for (size_t i = 0; i < sizeof(w->hbuf) / sizeof(w->hbuf[0]); ++i)
     if (w->hbuf[i]) {
       cudaFreeHost(w->hbuf[i]);
       w->hbuf[i] = nullptr;
