@@ -555,6 +555,23 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
                  : "r"(bar), "r"(parity)
                  : "memory");
 }
+// The same wait with a suspend-time hint: the warp is parked in hardware (up
+// to hint_ns) instead of re-issuing try_wait.  The producers' wait for a free
+// stage was the hottest loop of the ring (ncu on the 8-way Reddit shard: 26%
+// of the stall samples, 11M try_wait retries — a fifth of the kernel's
+// instructions, issue slots taken from the consumers).
+#ifndef GESPMM_HUB_SUSPEND_NS
+#define GESPMM_HUB_SUSPEND_NS 0
+#endif
+__device__ __forceinline__ void mbar_wait_hint(uint32_t bar, uint32_t parity, uint32_t hint_ns) {
+  uint32_t done = 0;
+  while (!done)
+    asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+                 "selp.u32 %0, 1, 0, p;\n\t}"
+                 : "=r"(done)
+                 : "r"(bar), "r"(parity), "r"(hint_ns)
+                 : "memory");
+}
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, uint64_t pol) {
   asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(dst), "l"(src),
                "l"(pol)
@@ -662,7 +679,10 @@ k_hub(SpmmArgs a) {
           kn = ld_stream_u32(ci + qn * G + lane, pol.stream);
         const uint32_t ga = gbase + q;
         const uint32_t st = ga % S, round = ga / S;
-        if (round > 0) mbar_wait(empty0 + 8 * st, (round - 1) & 1u);
+        if (round > 0) {
+          if (GESPMM_HUB_SUSPEND_NS) mbar_wait_hint(empty0 + 8 * st, (round - 1) & 1u, GESPMM_HUB_SUSPEND_NS);
+          else mbar_wait(empty0 + 8 * st, (round - 1) & 1u);
+        }
         const uint32_t cnt = min(uint32_t(G), len - q * G);
         const uint32_t e0 = st * G;
         if (lane < cnt) {
@@ -846,7 +866,10 @@ k_hub_g4(SpmmArgs a, const __grid_constant__ CUtensorMap tmap) {
         }
         const uint32_t ga = gbase + q;
         const uint32_t st = ga % S, round = ga / S;
-        if (round > 0) mbar_wait(empty0 + 8 * st, (round - 1) & 1u);
+        if (round > 0) {
+          if (GESPMM_HUB_SUSPEND_NS) mbar_wait_hint(empty0 + 8 * st, (round - 1) & 1u, GESPMM_HUB_SUSPEND_NS);
+          else mbar_wait(empty0 + 8 * st, (round - 1) & 1u);
+        }
         const uint32_t cnt = min(uint32_t(G), len - q * G);
         const uint32_t e0 = st * G;
         if (lane < cnt) {
