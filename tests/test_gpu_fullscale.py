@@ -135,3 +135,43 @@ def test_cora_equals_reference_dense_oracle(cuda, op):
                     G.KernelVariant.crc_cwm(2), G.KernelVariant.crc_cwm(8)):
         c = G.native_spmm(a, G.DenseMatrix.of(b), variant, G.reduce_op_by_name(op))
         _assert_bits(c.data, want, f"Cora N=16 {op} {variant}")
+
+
+def _shard(a, g, world):
+    from paper_2007_03179_b200 import dist as D
+    bounds = D.partition_rows(a.row_ptr, world)
+    return D.shard_csr(a, bounds[g], bounds[g + 1])
+
+
+@pytest.mark.parametrize("g", [0, 7])
+def test_products_8way_shard_split_hub_rows_bit_exact(cuda, g):
+    """An 8-way products shard takes the split-hub-row path (segments through
+    k_warp + ordered combine): max and argmax over the whole shard equal the
+    restatement bit for bit."""
+    a = _shard(_matrix(PRODUCTS), g, 8)
+    b = G.make_random_dense(a.n_cols, 256, 42).data
+    d = G.DeviceCsr.from_host(a, "cuda:0")
+    plan = G.Plan(d, 256, "max")
+    assert "split" in plan.description, plan.description
+    plan.close()
+    got, arg = _gpu(a, b, "max", want_arg=True)
+    want, want_arg = O.spmm(a.n_rows, a.n_cols, a.row_ptr, a.col_ind, a.vals, b, "max",
+                            want_arg=True)
+    _assert_bits(got, want, f"products shard {g}/8 max")
+    assert np.array_equal(arg, want_arg)
+
+
+@pytest.mark.parametrize("g", [0, 3])
+def test_reddit_8way_shard_exact_ring_bit_exact(cuda, g):
+    """An 8-way Reddit shard, exact sum: its hub rows go through the ring
+    kernel run ahead of the warp kernel; the whole shard equals the
+    reference's fold bit for bit."""
+    a = _shard(_matrix(REDDIT), g, 8)
+    b = G.make_random_dense(a.n_cols, 128, 42).data
+    d = G.DeviceCsr.from_host(a, "cuda:0")
+    plan = G.Plan(d, 128, "sum")
+    assert "hub_rows=0 " not in plan.description and "split" not in plan.description
+    plan.close()
+    got, _ = _gpu(a, b, "sum")
+    want, _ = O.spmm(a.n_rows, a.n_cols, a.row_ptr, a.col_ind, a.vals, b, "sum")
+    _assert_bits(got, want, f"Reddit shard {g}/8 sum")
