@@ -254,6 +254,36 @@ uint32_t auto_hub_threshold(uint32_t n, uint64_t nnz, int cf, uint32_t k, int de
   return t >= 4294967295.0 ? 0xffffffffu : uint32_t(t);
 }
 
+// Hub threshold when the ring runs alone ahead of the warp kernel (exact
+// sum/mean plans whose hub rows carry >= kHubPdlShare of the nonzeros): the
+// step is then the ring phase plus the warp phase, and the warp phase ends
+// with its longest row (LPT), so rows stay on warps only while one of them
+// takes at most kSeqAlpha of the warp phase.  Scans the degree-descending
+// order for the first row that satisfies it.  Measured on Reddit shards
+// (tools/r2_floor.sh, profiles/r2/hubseq/thr_*): 8 shards best at ~1024
+// (0.466 ms; the launch-wide rule gave 2048: 0.503 ms), 4 shards flat between
+// 2800 and 4096 (0.843-0.831 ms).
+constexpr double kSeqAlpha = 0.5;
+uint32_t seq_hub_threshold(const std::vector<uint32_t>& deg, const std::vector<uint32_t>& order,
+                           uint64_t total, uint32_t n, uint32_t tile_cols, int cf, uint32_t k,
+                           int dev) {
+  const uint32_t moved = std::max(n, tile_cols);
+  int l2 = 0;
+  cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev);
+  const double b_bytes = double(k) * double(n) * 4.0;
+  const double rate = (l2 > 0 && b_bytes > 1.5 * double(l2)) ? 9.5e12 : 19e12;
+  const double t_nnz = 0.7e-6 * double(cf < 1 ? 1 : cf) / 8.0;
+  uint64_t cum = 0;
+  for (size_t i = 0; i < order.size(); ++i) {
+    const double rest = double(total - cum);
+    const double warp_phase = std::max(rest * 4.0 * double(moved) / rate, rest * 18e-12);
+    const uint32_t d = deg[order[i]];
+    if (double(d) * t_nnz <= kSeqAlpha * warp_phase) return std::max<uint32_t>(256u, d + 1u);
+    cum += d;
+  }
+  return 256u;
+}
+
 // Frequency-aware L2 policy budget (bytes of B rows kept evict_last), 0 = off.
 // Opt-in (l2_hot_mb > 0).  History on B200 (profiles/r1_hot_sweep.txt,
 // profiles/r1_kernel_v4.txt): with the per-load policy select of the first
@@ -505,6 +535,20 @@ gespmm_status_t build_tuned(Plan& p, const uint32_t* host_rp, cudaStream_t st) {
   while (n_hub < m && deg[order[n_hub]] >= p.hub_threshold) hub_nnz += deg[order[n_hub++]];
   p.n_hub = n_hub;
   p.hub_pdl = host_rp[m] && double(hub_nnz) >= kHubPdlShare * double(host_rp[m]);
+  static const bool seq_thr = [] {  // GESPMM_HUB_SEQ_THRESHOLD=0: keep the launch-wide rule (A/B)
+    const char* e = std::getenv("GESPMM_HUB_SEQ_THRESHOLD");
+    return !(e && e[0] == '0');
+  }();
+  if (ht == 0 && n_hub && p.hub_pdl && seq_thr && !split_eligible(p) && sw >= 8) {
+    // the ring will run alone first (launch_tuned_rows): re-pick the threshold
+    p.hub_threshold = seq_hub_threshold(deg, order, host_rp[m], sw, p.sh.warp_v.tile_width(),
+                                        p.sh.warp_v.cf, p.a.n_cols, p.device);
+    n_hub = 0;
+    hub_nnz = 0;
+    while (n_hub < m && deg[order[n_hub]] >= p.hub_threshold) hub_nnz += deg[order[n_hub++]];
+    p.n_hub = n_hub;
+    p.hub_pdl = double(hub_nnz) >= kHubPdlShare * double(host_rp[m]);
+  }
   if (n_hub && split_eligible(p)) {
     // segments of at most half the hub threshold: each one's single-warp time
     // is then at most half of what made a row a hub row
