@@ -258,12 +258,19 @@ uint32_t auto_hub_threshold(uint32_t n, uint64_t nnz, int cf, uint32_t k, int de
 // sum/mean plans whose hub rows carry >= kHubPdlShare of the nonzeros): the
 // step is then the ring phase plus the warp phase, and the warp phase ends
 // with its longest row (LPT), so rows stay on warps only while one of them
-// takes at most kSeqAlpha of the warp phase.  Scans the degree-descending
+// takes at most alpha (0.5) of the warp phase.  Scans the degree-descending
 // order for the first row that satisfies it.  Measured on Reddit shards
-// (tools/r2_floor.sh, profiles/r2/hubseq/thr_*): 8 shards best at ~1024
-// (0.466 ms; the launch-wide rule gave 2048: 0.503 ms), 4 shards flat between
-// 2800 and 4096 (0.843-0.831 ms).
-constexpr double kSeqAlpha = 0.5;
+// (tools/r2_floor.sh, tools/r2_alpha.sh, profiles/r2/hubseq/): 8 shards best
+// at ~1024 (0.466 ms; the launch-wide rule gave 2048: 0.503 ms), 4 shards flat
+// between 2800 and 4096 (0.843-0.831 ms); alpha 0.35/0.5/0.6/0.7 -> 2/4/8
+// shards 1.60/0.87/0.49, 1.57/0.84/0.46, 1.52/0.83/0.48, 1.55/0.83/0.49 ms.
+double seq_alpha() {
+  static const double a = [] {  // GESPMM_HUB_SEQ_ALPHA: A/B
+    const char* e = std::getenv("GESPMM_HUB_SEQ_ALPHA");
+    return e ? std::max(0.05, std::atof(e)) : 0.5;
+  }();
+  return a;
+}
 uint32_t seq_hub_threshold(const std::vector<uint32_t>& deg, const std::vector<uint32_t>& order,
                            uint64_t total, uint32_t n, uint32_t tile_cols, int cf, uint32_t k,
                            int dev) {
@@ -278,7 +285,7 @@ uint32_t seq_hub_threshold(const std::vector<uint32_t>& deg, const std::vector<u
     const double rest = double(total - cum);
     const double warp_phase = std::max(rest * 4.0 * double(moved) / rate, rest * 18e-12);
     const uint32_t d = deg[order[i]];
-    if (double(d) * t_nnz <= kSeqAlpha * warp_phase) return std::max<uint32_t>(256u, d + 1u);
+    if (double(d) * t_nnz <= seq_alpha() * warp_phase) return std::max<uint32_t>(256u, d + 1u);
     cum += d;
   }
   return 256u;
@@ -539,7 +546,15 @@ gespmm_status_t build_tuned(Plan& p, const uint32_t* host_rp, cudaStream_t st) {
     const char* e = std::getenv("GESPMM_HUB_SEQ_THRESHOLD");
     return !(e && e[0] == '0');
   }();
-  if (ht == 0 && n_hub && p.hub_pdl && seq_thr && !split_eligible(p) && sw >= 8) {
+  // exact plans with hub rows always run the ring first and alone (even when
+  // the hub rows carry < kHubPdlShare: 2 Reddit shards 1.714 ms with the ring
+  // as a side job, 1.566 ms ring-first; tools/r2_alpha.sh).
+  // GESPMM_HUB_SEQ_ALWAYS=0 restores the side-stream mode for small shares.
+  static const bool seq_always = [] {
+    const char* e = std::getenv("GESPMM_HUB_SEQ_ALWAYS");
+    return !(e && e[0] == '0');
+  }();
+  if (ht == 0 && n_hub && (p.hub_pdl || seq_always) && seq_thr && !split_eligible(p) && sw >= 8) {
     // the ring will run alone first (launch_tuned_rows): re-pick the threshold
     p.hub_threshold = seq_hub_threshold(deg, order, host_rp[m], sw, p.sh.warp_v.tile_width(),
                                         p.sh.warp_v.cf, p.a.n_cols, p.device);
@@ -547,7 +562,7 @@ gespmm_status_t build_tuned(Plan& p, const uint32_t* host_rp, cudaStream_t st) {
     hub_nnz = 0;
     while (n_hub < m && deg[order[n_hub]] >= p.hub_threshold) hub_nnz += deg[order[n_hub++]];
     p.n_hub = n_hub;
-    p.hub_pdl = double(hub_nnz) >= kHubPdlShare * double(host_rp[m]);
+    p.hub_pdl = seq_always || double(hub_nnz) >= kHubPdlShare * double(host_rp[m]);
   }
   if (n_hub && split_eligible(p)) {
     // segments of at most half the hub threshold: each one's single-warp time

@@ -713,7 +713,7 @@ def test_reddit_scale_hub_threshold_by_width(cuda):
     bt = torch.from_numpy(b.data).to(cuda)
     p32 = G.Plan(d, 32, "sum")
     h = hub_rows(p32.description)
-    assert 0 < h < 1000, p32.description
+    assert 0 < h < 2000, p32.description  # deg >= ~10k: the ring-first threshold (alpha rule)
     c = torch.empty((a.n_rows, 32), device=cuda)
     p32.execute(bt, c)
     torch.cuda.synchronize()
