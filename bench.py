@@ -515,7 +515,8 @@ def run_ours(args, cfg):
     plan = G.Plan(d, n, op, variant=variant, exec=ex)
     log(f"[bench] rank {rank}: rows [{info.lo},{info.hi}) nnz {shard.nnz()} plan: {plan.description}")
     stream = torch.cuda.current_stream()
-    l2_flush = torch.empty(256 * 1024 * 1024 // 4 * 2, dtype=torch.float32, device=dev)  # 512 MB
+    flush_mb = int(os.environ.get("GESPMM_FLUSH_MB", "512"))  # A/B: flush size (> L2)
+    l2_flush = torch.empty(flush_mb * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
 
     def step():
         plan.execute(bt, c, arg)
