@@ -569,6 +569,8 @@ gespmm_status_t build_tuned(Plan& p, const uint32_t* host_rp, cudaStream_t st) {
     // is then at most half of what made a row a hub row
     const uint32_t t = p.hub_threshold == 0xffffffffu ? 4096u : p.hub_threshold;
     p.seg_len = std::max<uint32_t>(256, (t / 2 + 63) & ~63u);
+    if (const char* e = std::getenv("GESPMM_SEG_LEN"))  // A/B
+      p.seg_len = std::max<uint32_t>(64, uint32_t(std::atoi(e)) & ~63u);
     std::vector<uint32_t> vptr, seg, hubs;
     for (uint32_t i = 0; i < n_hub; ++i) {
       const uint32_t r = order[i], d = deg[r];
