@@ -175,3 +175,21 @@ def test_reddit_8way_shard_exact_ring_bit_exact(cuda, g):
     got, _ = _gpu(a, b, "sum")
     want, _ = O.spmm(a.n_rows, a.n_cols, a.row_ptr, a.col_ind, a.vals, b, "sum")
     _assert_bits(got, want, f"Reddit shard {g}/8 sum")
+
+
+def test_reddit_8way_shard_fast_sum_split_within_tolerance(cuda):
+    """Fast mode on an 8-way Reddit shard: hub rows split into segments (the
+    partial sums reassociate the fold), everything FFMA; within the north_star
+    tolerance, |got - want| <= 1e-5 * max(|want|, sum |v * b|), on the whole
+    shard."""
+    a = _shard(_matrix(REDDIT), 0, 8)
+    b = G.make_random_dense(a.n_cols, 128, 42).data
+    d = G.DeviceCsr.from_host(a, "cuda:0")
+    plan = G.Plan(d, 128, "sum", exec=G.ExecOptions(exact=False))
+    assert "split" in plan.description, plan.description
+    plan.close()
+    got, _ = _gpu(a, b, "sum", exec=G.ExecOptions(exact=False))
+    want, _ = O.spmm(a.n_rows, a.n_cols, a.row_ptr, a.col_ind, a.vals, b, "sum")
+    mag, _ = O.spmm(a.n_rows, a.n_cols, a.row_ptr, a.col_ind, np.abs(a.vals), np.abs(b), "sum")
+    err = np.abs(got.astype(np.float64) - want)
+    assert np.all(err <= 1e-5 * np.maximum(np.abs(want), mag) + 1e-30), float(np.max(err / (mag + 1e-30)))
