@@ -573,9 +573,15 @@ __device__ __forceinline__ void mbar_wait_hint(uint32_t bar, uint32_t parity, ui
                  : "memory");
 }
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, uint64_t pol) {
+#ifdef GESPMM_HUB_CA  // A/B: stage through L1 (hub rows share hot columns)
+  asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(dst), "l"(src),
+               "l"(pol)
+               : "memory");
+#else
   asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(dst), "l"(src),
                "l"(pol)
                : "memory");
+#endif
 }
 __device__ __forceinline__ void cp_async4(uint32_t dst, const void* src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst), "l"(src) : "memory");
