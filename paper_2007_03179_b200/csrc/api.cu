@@ -264,13 +264,7 @@ uint32_t auto_hub_threshold(uint32_t n, uint64_t nnz, int cf, uint32_t k, int de
 // at ~1024 (0.466 ms; the launch-wide rule gave 2048: 0.503 ms), 4 shards flat
 // between 2800 and 4096 (0.843-0.831 ms); alpha 0.35/0.5/0.6/0.7 -> 2/4/8
 // shards 1.60/0.87/0.49, 1.57/0.84/0.46, 1.52/0.83/0.48, 1.55/0.83/0.49 ms.
-double seq_alpha() {
-  static const double a = [] {  // GESPMM_HUB_SEQ_ALPHA: A/B
-    const char* e = std::getenv("GESPMM_HUB_SEQ_ALPHA");
-    return e ? std::max(0.05, std::atof(e)) : 0.5;
-  }();
-  return a;
-}
+constexpr double kSeqAlpha = 0.5;
 uint32_t seq_hub_threshold(const std::vector<uint32_t>& deg, const std::vector<uint32_t>& order,
                            uint64_t total, uint32_t n, uint32_t tile_cols, int cf, uint32_t k,
                            int dev) {
@@ -285,7 +279,7 @@ uint32_t seq_hub_threshold(const std::vector<uint32_t>& deg, const std::vector<u
     const double rest = double(total - cum);
     const double warp_phase = std::max(rest * 4.0 * double(moved) / rate, rest * 18e-12);
     const uint32_t d = deg[order[i]];
-    if (double(d) * t_nnz <= seq_alpha() * warp_phase) return std::max<uint32_t>(256u, d + 1u);
+    if (double(d) * t_nnz <= kSeqAlpha * warp_phase) return std::max<uint32_t>(256u, d + 1u);
     cum += d;
   }
   return 256u;
@@ -542,10 +536,6 @@ gespmm_status_t build_tuned(Plan& p, const uint32_t* host_rp, cudaStream_t st) {
   while (n_hub < m && deg[order[n_hub]] >= p.hub_threshold) hub_nnz += deg[order[n_hub++]];
   p.n_hub = n_hub;
   p.hub_pdl = host_rp[m] && double(hub_nnz) >= kHubPdlShare * double(host_rp[m]);
-  static const bool seq_thr = [] {  // GESPMM_HUB_SEQ_THRESHOLD=0: keep the launch-wide rule (A/B)
-    const char* e = std::getenv("GESPMM_HUB_SEQ_THRESHOLD");
-    return !(e && e[0] == '0');
-  }();
   // exact plans with hub rows always run the ring first and alone (even when
   // the hub rows carry < kHubPdlShare: 2 Reddit shards 1.714 ms with the ring
   // as a side job, 1.566 ms ring-first; tools/r2_alpha.sh).
@@ -554,7 +544,7 @@ gespmm_status_t build_tuned(Plan& p, const uint32_t* host_rp, cudaStream_t st) {
     const char* e = std::getenv("GESPMM_HUB_SEQ_ALWAYS");
     return !(e && e[0] == '0');
   }();
-  if (ht == 0 && n_hub && (p.hub_pdl || seq_always) && seq_thr && !split_eligible(p) && sw >= 8) {
+  if (ht == 0 && n_hub && (p.hub_pdl || seq_always) && !split_eligible(p) && sw >= 8) {
     // the ring will run alone first (launch_tuned_rows): re-pick the threshold
     p.hub_threshold = seq_hub_threshold(deg, order, host_rp[m], sw, p.sh.warp_v.tile_width(),
                                         p.sh.warp_v.cf, p.a.n_cols, p.device);
@@ -569,8 +559,8 @@ gespmm_status_t build_tuned(Plan& p, const uint32_t* host_rp, cudaStream_t st) {
     // is then at most half of what made a row a hub row
     const uint32_t t = p.hub_threshold == 0xffffffffu ? 4096u : p.hub_threshold;
     p.seg_len = std::max<uint32_t>(256, (t / 2 + 63) & ~63u);
-    if (const char* e = std::getenv("GESPMM_SEG_LEN"))  // A/B
-      p.seg_len = std::max<uint32_t>(64, uint32_t(std::atoi(e)) & ~63u);
+    // (segment-length sweep, profiles/r2/split/seglen_*: 512 / half the
+    // threshold / 2048 within 2%, 4096 slower)
     std::vector<uint32_t> vptr, seg, hubs;
     for (uint32_t i = 0; i < n_hub; ++i) {
       const uint32_t r = order[i], d = deg[r];

@@ -555,33 +555,11 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
                  : "r"(bar), "r"(parity)
                  : "memory");
 }
-// The same wait with a suspend-time hint: the warp is parked in hardware (up
-// to hint_ns) instead of re-issuing try_wait.  The producers' wait for a free
-// stage was the hottest loop of the ring (ncu on the 8-way Reddit shard: 26%
-// of the stall samples, 11M try_wait retries — a fifth of the kernel's
-// instructions, issue slots taken from the consumers).
-#ifndef GESPMM_HUB_SUSPEND_NS
-#define GESPMM_HUB_SUSPEND_NS 0
-#endif
-__device__ __forceinline__ void mbar_wait_hint(uint32_t bar, uint32_t parity, uint32_t hint_ns) {
-  uint32_t done = 0;
-  while (!done)
-    asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
-                 "selp.u32 %0, 1, 0, p;\n\t}"
-                 : "=r"(done)
-                 : "r"(bar), "r"(parity), "r"(hint_ns)
-                 : "memory");
-}
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, uint64_t pol) {
-#ifdef GESPMM_HUB_CA  // A/B: stage through L1 (hub rows share hot columns)
-  asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(dst), "l"(src),
-               "l"(pol)
-               : "memory");
-#else
+  // .cg (L2 only): staging through L1 (.ca) measured much slower
   asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(dst), "l"(src),
                "l"(pol)
                : "memory");
-#endif
 }
 __device__ __forceinline__ void cp_async4(uint32_t dst, const void* src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst), "l"(src) : "memory");
@@ -685,10 +663,7 @@ k_hub(SpmmArgs a) {
           kn = ld_stream_u32(ci + qn * G + lane, pol.stream);
         const uint32_t ga = gbase + q;
         const uint32_t st = ga % S, round = ga / S;
-        if (round > 0) {
-          if (GESPMM_HUB_SUSPEND_NS) mbar_wait_hint(empty0 + 8 * st, (round - 1) & 1u, GESPMM_HUB_SUSPEND_NS);
-          else mbar_wait(empty0 + 8 * st, (round - 1) & 1u);
-        }
+        if (round > 0) mbar_wait(empty0 + 8 * st, (round - 1) & 1u);
         const uint32_t cnt = min(uint32_t(G), len - q * G);
         const uint32_t e0 = st * G;
         if (lane < cnt) {
@@ -872,10 +847,7 @@ k_hub_g4(SpmmArgs a, const __grid_constant__ CUtensorMap tmap) {
         }
         const uint32_t ga = gbase + q;
         const uint32_t st = ga % S, round = ga / S;
-        if (round > 0) {
-          if (GESPMM_HUB_SUSPEND_NS) mbar_wait_hint(empty0 + 8 * st, (round - 1) & 1u, GESPMM_HUB_SUSPEND_NS);
-          else mbar_wait(empty0 + 8 * st, (round - 1) & 1u);
-        }
+        if (round > 0) mbar_wait(empty0 + 8 * st, (round - 1) & 1u);
         const uint32_t cnt = min(uint32_t(G), len - q * G);
         const uint32_t e0 = st * G;
         if (lane < cnt) {
@@ -1491,11 +1463,6 @@ uint32_t hub_tile_width(uint32_t n, uint32_t n_hub) {
 }
 
 cudaError_t launch_tuned_hub(int op, bool fast, const SpmmArgs& a, cudaStream_t st, bool big) {
-  static const int big_env = [] {  // GESPMM_HUB_BIG=0/1: ring geometry A/B
-    const char* e = std::getenv("GESPMM_HUB_BIG");
-    return e ? std::atoi(e) : -1;
-  }();
-  if (big_env >= 0) big = big_env != 0;
   const int w = hub_vec(a.n, a.n_sched);  // tile = 32 * w columns
   const int c = hub_split(w, big);
   const int v = w / c;
