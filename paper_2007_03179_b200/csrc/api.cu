@@ -285,6 +285,16 @@ uint32_t seq_hub_threshold(const std::vector<uint32_t>& deg, const std::vector<u
   return 256u;
 }
 
+// Round-2 hub schedule for exact plans (ring first and alone, warp kernel
+// after it, seq_hub_threshold); GESPMM_HUB_SEQ=0 restores round 1's.
+bool hub_ring_first() {
+  static const bool on = [] {
+    const char* e = std::getenv("GESPMM_HUB_SEQ");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 // Frequency-aware L2 policy budget (bytes of B rows kept evict_last), 0 = off.
 // Opt-in (l2_hot_mb > 0).  History on B200 (profiles/r1_hot_sweep.txt,
 // profiles/r1_kernel_v4.txt): with the per-load policy select of the first
@@ -446,14 +456,11 @@ gespmm_status_t launch_tuned_rows(const TunedShapes& t, int op, bool fast, const
       // emulated shards): 4 shards 0.973 -> 0.833 ms, 8 shards 0.526 ->
       // 0.499 ms — the ring's 128 KB of shared memory per SM took L1 and
       // occupancy from the warp kernel next to it.  GESPMM_HUB_SEQ=0 restores
-      // the overlapped launch.
-      static const bool hub_seq = [] {
-        const char* e = std::getenv("GESPMM_HUB_SEQ");
-        return !(e && e[0] == '0');
-      }();
+      // the round-1 scheme (overlapped launch, side stream, launch-wide
+      // threshold).
       if (tma && (hub_pdl || !side)) {
         GESPMM_CUDA(launch_tuned_hub(op, fast, h, st, true), "spmm");
-        hub_then_pdl = !hub_seq;
+        hub_then_pdl = !hub_ring_first();
       } else {
         cudaStream_t hs = side ? side : st;
         if (side) {
@@ -538,13 +545,9 @@ gespmm_status_t build_tuned(Plan& p, const uint32_t* host_rp, cudaStream_t st) {
   p.hub_pdl = host_rp[m] && double(hub_nnz) >= kHubPdlShare * double(host_rp[m]);
   // exact plans with hub rows always run the ring first and alone (even when
   // the hub rows carry < kHubPdlShare: 2 Reddit shards 1.714 ms with the ring
-  // as a side job, 1.566 ms ring-first; tools/r2_alpha.sh).
-  // GESPMM_HUB_SEQ_ALWAYS=0 restores the side-stream mode for small shares.
-  static const bool seq_always = [] {
-    const char* e = std::getenv("GESPMM_HUB_SEQ_ALWAYS");
-    return !(e && e[0] == '0');
-  }();
-  if (ht == 0 && n_hub && (p.hub_pdl || seq_always) && !split_eligible(p) && sw >= 8) {
+  // as a side job, 1.566 ms ring-first; tools/r2_alpha.sh)
+  const bool seq_always = hub_ring_first();
+  if (ht == 0 && n_hub && seq_always && !split_eligible(p) && sw >= 8) {
     // the ring will run alone first (launch_tuned_rows): re-pick the threshold
     p.hub_threshold = seq_hub_threshold(deg, order, host_rp[m], sw, p.sh.warp_v.tile_width(),
                                         p.sh.warp_v.cf, p.a.n_cols, p.device);
