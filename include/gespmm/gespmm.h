@@ -155,7 +155,12 @@ const char* gespmm_last_error(void);
  * Asynchronous on `stream` (cudaStream_t, NULL = legacy default).  Replaces the
  * compute of spmm::native_spmm (native.hpp:101-143) / run_warp
  * (kernel.hpp:346-361).  B and C must not alias.  validate=1 runs the
- * canonical check on the device first and synchronises `stream` to report it. */
+ * canonical check on the device first and synchronises `stream` to report it.
+ * The library keeps a small per-(CSR, shape, op, options, device, stream) LRU
+ * of plans behind this call; results never depend on a cached entry (A may
+ * change between calls), but a CUDA graph that captures this call refers to
+ * the cached plan's buffers, which a later eviction frees: capture an
+ * explicit plan (gespmm_plan_execute) instead. */
 gespmm_status_t gespmm_spmm_device(const gespmm_csr_t* a, const float* b, uint32_t n,
                                    gespmm_reduce_t op, float* c, int32_t* arg,
                                    const gespmm_options_t* opts, void* stream);

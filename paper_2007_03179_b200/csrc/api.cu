@@ -866,17 +866,23 @@ gespmm_status_t plan_execute_impl(Plan& p, const float* b, float* c, int32_t* ar
 }
 
 // Small LRU of plans for the plan-less device entry point: keyed by the CSR
-// arrays, shape, op and options.  A cached plan keeps only a row schedule
-// derived from row_ptr, and every schedule covers every row exactly once, so
-// a stale entry (row_ptr mutated in place, or a new CSR at a recycled address)
-// can only cost speed.  Plans that snapshot col_ind (cluster_hot's remapped
-// copy) are never cached: the call builds and drops one each time.
+// arrays, shape, op, options, device and stream (a plan's hub counters and
+// split partials are per-execute scratch, so two streams never share one).
+// A cached plan keeps a row schedule derived from row_ptr, and every schedule
+// covers every row exactly once, so a stale entry (row_ptr mutated in place,
+// or a new CSR at a recycled address) can only cost speed; the one piece of
+// plan state that holds row_ptr values, a split plan's virtual row_ptr over
+// hub-row segments, is rebuilt from the live row_ptr on every cache hit
+// (launch_split_refresh).  Plans that snapshot col_ind (cluster_hot's
+// remapped copy, relocated hot rows) are never cached: the call builds and
+// drops one each time.
 struct CacheEntry {
   gespmm_csr_t a;
   uint32_t n;
   gespmm_reduce_t op;
   gespmm_options_t o;
   int device;
+  cudaStream_t stream;
   std::unique_ptr<Plan> plan;
 };
 std::mutex g_cache_mu;
@@ -890,17 +896,26 @@ Plan* cached_plan(const gespmm_csr_t* a, uint32_t n, gespmm_reduce_t op,
   cudaGetDevice(&dev);
   std::lock_guard<std::mutex> lk(g_cache_mu);
   for (auto it = g_cache.begin(); it != g_cache.end(); ++it) {
-    if (it->device == dev && it->n == n && it->op == op &&
+    if (it->device == dev && it->stream == st && it->n == n && it->op == op &&
         std::memcmp(&it->a, a, sizeof(*a)) == 0 && std::memcmp(&it->o, &o, sizeof(o)) == 0) {
       g_cache.splice(g_cache.begin(), g_cache, it);
+      Plan* hit = g_cache.front().plan.get();
       *status = GESPMM_OK;
-      return g_cache.front().plan.get();
+      if (hit->split) {
+        const cudaError_t e = launch_split_refresh(a->row_ptr, hit->d_hubs, hit->n_hub,
+                                                   hit->seg_len, hit->d_vptr, st);
+        if (e != cudaSuccess) {
+          *status = cuda_fail(e, "spmm");
+          return nullptr;
+        }
+      }
+      return hit;
     }
   }
   Plan* p = nullptr;
   *status = plan_create_impl(a, n, op, &o, st, host_rp, &p);
   if (*status != GESPMM_OK) return nullptr;
-  g_cache.push_front(CacheEntry{*a, n, op, o, dev, std::unique_ptr<Plan>(p)});
+  g_cache.push_front(CacheEntry{*a, n, op, o, dev, st, std::unique_ptr<Plan>(p)});
   if (g_cache.size() > kCacheCap) g_cache.pop_back();
   return p;
 }

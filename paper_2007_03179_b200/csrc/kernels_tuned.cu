@@ -1269,6 +1269,22 @@ __global__ void __launch_bounds__(256) k_split_combine(SpmmArgs a, const uint32_
   }
 }
 
+__global__ void __launch_bounds__(256) k_split_refresh(const uint32_t* __restrict__ row_ptr,
+                                                       const uint32_t* __restrict__ hubs,
+                                                       uint32_t n_hub, uint32_t seg_len,
+                                                       uint32_t* __restrict__ vptr) {
+  for (uint32_t h = blockIdx.x * blockDim.x + threadIdx.x; h < n_hub; h += gridDim.x * blockDim.x) {
+    const uint32_t row = hubs[3 * h], v0 = hubs[3 * h + 1], k = hubs[3 * h + 2];
+    const uint32_t lo = row_ptr[row], hi = row_ptr[row + 1];
+    const uint32_t d = hi - lo;
+    for (uint32_t j = 0; j < k; ++j) {
+      const uint64_t off = uint64_t(j) * seg_len;
+      vptr[v0 + j] = lo + uint32_t(off < d ? off : d);
+    }
+    vptr[v0 + k] = hi;
+  }
+}
+
 }  // namespace
 
 cudaError_t resolve_range_policy(const void* base, uint32_t bytes, int mode, uint64_t* out,
@@ -1486,6 +1502,15 @@ cudaError_t launch_split_combine(int op, const SpmmArgs& a, const uint32_t* hubs
     case kMax: k_split_combine<kMax><<<g, 256, 0, st>>>(a, hubs, n_hub, part, part_arg); break;
     default: k_split_combine<kMin><<<g, 256, 0, st>>>(a, hubs, n_hub, part, part_arg); break;
   }
+  note_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_split_refresh(const uint32_t* row_ptr, const uint32_t* hubs, uint32_t n_hub,
+                                 uint32_t seg_len, uint32_t* vptr, cudaStream_t st) {
+  if (!n_hub) return cudaSuccess;
+  const uint32_t g = (n_hub + 255) / 256;
+  k_split_refresh<<<g < 148 ? g : 148, 256, 0, st>>>(row_ptr, hubs, n_hub, seg_len, vptr);
   note_launch();
   return cudaGetLastError();
 }

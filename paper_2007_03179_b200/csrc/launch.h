@@ -72,6 +72,12 @@ cudaError_t launch_tuned_hub(int op, bool fast, const SpmmArgs& a, cudaStream_t 
 // segment order into C / arg (+ replicas); hubs = (row, first partial, count).
 cudaError_t launch_split_combine(int op, const SpmmArgs& a, const uint32_t* hubs, uint32_t n_hub,
                                  const float* part, const int32_t* part_arg, cudaStream_t st);
+// Rebuild the segments' virtual row_ptr from the live row_ptr (same segment
+// counts; the last segment absorbs any change of degree): a cached plan-less
+// split plan stays correct when row_ptr changed in place or a new CSR of the
+// same shape reuses its address.
+cudaError_t launch_split_refresh(const uint32_t* row_ptr, const uint32_t* hubs, uint32_t n_hub,
+                                 uint32_t seg_len, uint32_t* vptr, cudaStream_t st);
 
 // --- frequency-aware L2 policy (hotcols.cu) ---
 struct HotStats {

@@ -115,3 +115,35 @@ def test_split_replicas_equal_oracle():
         assert first_divergence(r.cpu().numpy(), want) is None
         assert np.array_equal(g.cpu().numpy(), warg)
     plan.close()
+
+
+@pytest.mark.parametrize("op", ["max", "sum"])
+def test_cached_split_plan_follows_row_ptr_changed_in_place(op):
+    """The plan-less entry caches plans by the CSR's pointers and shape; a
+    split plan's virtual row_ptr over hub-row segments holds row_ptr values,
+    so a cache hit must rebuild it from the live row_ptr.  Overwrite A in
+    place with another matrix of the same shape and nnz (what a recycled
+    allocation looks like) and check the second call against the oracle."""
+    a1, a2 = _graph(seed=61), _graph(seed=62)
+    assert a1.nnz() == a2.nnz() and not np.array_equal(a1.row_ptr, a2.row_ptr)
+    x = G.make_random_dense(a1.n_cols, 64, 63).data
+    xd = torch.from_numpy(np.ascontiguousarray(x)).to(DEV)
+    ex = G.ExecOptions(hub_threshold=300, exact=(op != "sum"))
+    d = G.DeviceCsr.from_host(a1, DEV)
+    for a in (a1, a2, a1):
+        src = G.DeviceCsr.from_host(a, DEV)
+        d.row_ptr.copy_(src.row_ptr)
+        d.col_ind.copy_(src.col_ind)
+        d.vals.copy_(src.vals)
+        c, arg = G.spmm(d, xd, op, want_arg=(op == "max"), exec=ex, validate=False)
+        torch.cuda.synchronize()
+        want, warg = O.spmm(a.n_rows, a.n_cols, a.row_ptr, a.col_ind, a.vals, x, op,
+                            want_arg=(op == "max"))
+        if op == "max":
+            assert first_divergence(c.cpu().numpy(), want) is None
+            assert np.array_equal(arg.cpu().numpy(), warg)
+        else:  # fast-mode sum: the north_star's 1e-5 relative tolerance
+            scale, _ = O.spmm(a.n_rows, a.n_cols, a.row_ptr, a.col_ind, np.abs(a.vals),
+                              np.abs(x), op)
+            err = np.abs(c.cpu().numpy().astype(np.float64) - want)
+            assert np.all(err <= 1e-5 * np.maximum(np.abs(want), scale) + 1e-30)
