@@ -883,13 +883,13 @@ struct CacheEntry {
   gespmm_options_t o;
   int device;
   cudaStream_t stream;
-  std::unique_ptr<Plan> plan;
+  std::shared_ptr<Plan> plan;  // shared: a caller keeps its plan alive past an eviction
 };
 std::mutex g_cache_mu;
 std::list<CacheEntry> g_cache;
 constexpr size_t kCacheCap = 16;
 
-Plan* cached_plan(const gespmm_csr_t* a, uint32_t n, gespmm_reduce_t op,
+std::shared_ptr<Plan> cached_plan(const gespmm_csr_t* a, uint32_t n, gespmm_reduce_t op,
                   const gespmm_options_t& o, cudaStream_t st, const uint32_t* host_rp,
                   gespmm_status_t* status) {
   int dev = 0;
@@ -899,7 +899,7 @@ Plan* cached_plan(const gespmm_csr_t* a, uint32_t n, gespmm_reduce_t op,
     if (it->device == dev && it->stream == st && it->n == n && it->op == op &&
         std::memcmp(&it->a, a, sizeof(*a)) == 0 && std::memcmp(&it->o, &o, sizeof(o)) == 0) {
       g_cache.splice(g_cache.begin(), g_cache, it);
-      Plan* hit = g_cache.front().plan.get();
+      std::shared_ptr<Plan> hit = g_cache.front().plan;
       *status = GESPMM_OK;
       if (hit->split) {
         const cudaError_t e = launch_split_refresh(a->row_ptr, hit->d_hubs, hit->n_hub,
@@ -915,9 +915,10 @@ Plan* cached_plan(const gespmm_csr_t* a, uint32_t n, gespmm_reduce_t op,
   Plan* p = nullptr;
   *status = plan_create_impl(a, n, op, &o, st, host_rp, &p);
   if (*status != GESPMM_OK) return nullptr;
-  g_cache.push_front(CacheEntry{*a, n, op, o, dev, st, std::unique_ptr<Plan>(p)});
+  std::shared_ptr<Plan> sp(p);
+  g_cache.push_front(CacheEntry{*a, n, op, o, dev, st, sp});
   if (g_cache.size() > kCacheCap) g_cache.pop_back();
-  return p;
+  return sp;
 }
 
 // Grow-only device staging for the host-buffer entry point: buffers, a
@@ -1227,7 +1228,7 @@ gespmm_status_t gespmm_spmm_device(const gespmm_csr_t* a, const float* b, uint32
     if (s == GESPMM_OK) GESPMM_CUDA(cudaStreamSynchronize(st), "spmm");  // before the free
     return s;
   }
-  Plan* p = cached_plan(a, n, op, o, st, nullptr, &s);
+  const std::shared_ptr<Plan> p = cached_plan(a, n, op, o, st, nullptr, &s);
   if (!p) return s;
   return plan_execute_impl(*p, b, c, arg, st);
 }

@@ -147,3 +147,27 @@ def test_cached_split_plan_follows_row_ptr_changed_in_place(op):
                               np.abs(x), op)
             err = np.abs(c.cpu().numpy().astype(np.float64) - want)
             assert np.all(err <= 1e-5 * np.maximum(np.abs(want), scale) + 1e-30)
+
+
+def test_plan_less_calls_on_two_streams_do_not_share_scratch():
+    """Back-to-back plan-less calls on two streams with the same CSR: each
+    stream gets its own cached plan (split partials and hub counters are
+    per-execute scratch), so concurrently running executes never mix."""
+    a = _graph(seed=81)
+    d = G.DeviceCsr.from_host(a, DEV)
+    ex = G.ExecOptions(hub_threshold=300)
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    xs = [G.make_random_dense(a.n_cols, 64, 90 + i).data for i in range(6)]
+    xds = [torch.from_numpy(np.ascontiguousarray(x)).to(DEV) for x in xs]
+    torch.cuda.synchronize()
+    outs = []
+    for i, xd in enumerate(xds):
+        s = streams[i % 2]
+        with torch.cuda.stream(s):
+            outs.append(G.spmm(d, xd, "max", want_arg=True, exec=ex, validate=False, stream=s))
+    torch.cuda.synchronize()
+    for x, (c, arg) in zip(xs, outs):
+        want, warg = O.spmm(a.n_rows, a.n_cols, a.row_ptr, a.col_ind, a.vals, x, "max",
+                            want_arg=True)
+        assert first_divergence(c.cpu().numpy(), want) is None
+        assert np.array_equal(arg.cpu().numpy(), warg)
