@@ -179,7 +179,12 @@ typedef struct gespmm_plan_s* gespmm_plan_t;
 
 /* Inspect a device CSR (degree distribution) and fix the kernel shape for this
  * n/op: sub-warp vs warp vs CTA per row class, merge factor, row schedule.  The
- * plan keeps pointers to A's arrays, which must stay valid.  Synchronous. */
+ * plan keeps pointers to A's arrays, which must stay valid.  Synchronous.
+ * The schedule only orders rows, so A's values and structure may change
+ * between executes (same shape) with correct results — except in a plan that
+ * splits hub rows (below), whose segment bounds are row_ptr values taken
+ * here: recreate it when row_ptr changes (gespmm_spmm_device does this
+ * itself for its cached plans). */
 gespmm_status_t gespmm_plan_create(const gespmm_csr_t* a, uint32_t n, gespmm_reduce_t op,
                                    const gespmm_options_t* opts, void* stream,
                                    gespmm_plan_t* out);
