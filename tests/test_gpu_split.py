@@ -171,3 +171,35 @@ def test_plan_less_calls_on_two_streams_do_not_share_scratch():
                             want_arg=True)
         assert first_divergence(c.cpu().numpy(), want) is None
         assert np.array_equal(arg.cpu().numpy(), warg)
+
+
+@pytest.mark.parametrize("explicit", [False, True])
+def test_low_degree_plan_stays_correct_when_a_gets_long_rows(explicit):
+    """A plan made for a low-degree matrix (identity row order, several rows
+    per warp) only orders rows: overwrite A in place with a power-law matrix of
+    the same shape and nnz (rows far longer than the plan saw) and both the
+    explicit plan and the plan-less call still match the oracle bit for bit."""
+    lo = G.gen_uniform_random(G.GraphGenSpec(3000, 30000, 5))
+    G.randomize_values(lo, 6)
+    hi = G.gen_powerlaw(3000, 30000, 2900, 1.0, 7)
+    G.randomize_values(hi, 8)
+    assert lo.nnz() == hi.nnz()
+    x = G.make_random_dense(3000, 128, 9).data
+    xd = torch.from_numpy(np.ascontiguousarray(x)).to(DEV)
+    d = G.DeviceCsr.from_host(lo, DEV)
+    plan = G.Plan(d, 128, "sum") if explicit else None
+    for a in (lo, hi):
+        src = G.DeviceCsr.from_host(a, DEV)
+        d.row_ptr.copy_(src.row_ptr)
+        d.col_ind.copy_(src.col_ind)
+        d.vals.copy_(src.vals)
+        if explicit:
+            c = torch.empty((3000, 128), device=DEV)
+            plan.execute(xd, c)
+        else:
+            c, _ = G.spmm(d, xd, "sum", validate=False)
+        torch.cuda.synchronize()
+        want, _ = O.spmm(a.n_rows, a.n_cols, a.row_ptr, a.col_ind, a.vals, x, "sum")
+        assert first_divergence(c.cpu().numpy(), want) is None
+    if plan is not None:
+        plan.close()
