@@ -30,6 +30,8 @@ def test_l1_sectors_equal_reference_simulator_transactions(tmp_path, cuda):
                         "-k", "regex:k_naive|k_crc", "--csv", "--log-file", str(out),
                         sys.executable, os.path.join(ROOT, "tools", "sector_parity.py"), "run"],
                        env=env, capture_output=True, text=True, timeout=600)
+    if "closed on this pool" in r.stdout + r.stderr:
+        pytest.skip("ncu is closed on this GPU pool")  # the pool's wrapper refused to run it
     assert r.returncode == 0, r.stderr[-2000:]
     os.environ["GESPMM_SECTOR_CASES"] = "small"
     try:
