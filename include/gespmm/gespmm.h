@@ -19,7 +19,9 @@
  *   exact mode.  sum: init +0, a+b.  max: init -FLT_MAX, (a < b ? b : a).
  *   min: init +FLT_MAX, (b < a ? b : a).  mean: sum / float(row length), empty
  *   row -> +0.  arg (max/min): CSR position p (or col_ind[p]) of the element that
- *   last replaced the accumulator (earliest p among ties), -1 if none.
+ *   last replaced the accumulator (earliest p among ties), -1 if none.  arg is
+ *   int32: a call with an arg whose indices cannot fit (nnz > 2^31 for CSR
+ *   positions, n_cols > 2^31 for columns) is refused with GESPMM_EINVAL.
  */
 #ifndef GESPMM_H_
 #define GESPMM_H_

@@ -126,6 +126,22 @@ gespmm_status_t check_op(gespmm_reduce_t op, const int32_t* arg) {
   return GESPMM_OK;
 }
 
+// arg is int32 (C ABI): an edge arg is a CSR position < nnz, a column arg a
+// column < n_cols; either must fit, or the call is refused rather than
+// writing wrapped indices.
+gespmm_status_t check_arg_range(const int32_t* arg, uint64_t nnz, uint32_t n_cols,
+                                int32_t arg_kind) {
+  if (!arg) return GESPMM_OK;
+  const bool column = arg_kind == GESPMM_ARG_COLUMN;
+  const uint64_t bound = column ? uint64_t(n_cols) : nnz;
+  if (bound > uint64_t(INT32_MAX) + 1)
+    return fail(GESPMM_EINVAL, std::string("arg: ") + (column ? "column" : "CSR position") +
+                                   " indices up to " + std::to_string(bound - 1) +
+                                   " do not fit the int32 arg" +
+                                   (column ? "" : " (use arg_kind = column)"));
+  return GESPMM_OK;
+}
+
 }  // namespace
 
 gespmm_status_t set_error(gespmm_status_t st, const std::string& msg) { return fail(st, msg); }
@@ -754,6 +770,7 @@ PersistLimits persist_limits(int dev) {
 gespmm_status_t plan_execute_impl(Plan& p, const float* b, float* c, int32_t* arg,
                                   cudaStream_t st, const SpmmArgs* rep = nullptr) {
   gespmm_status_t s = check_op(p.op, arg);
+  if (s == GESPMM_OK) s = check_arg_range(arg, p.a.nnz, p.a.n_cols, p.o.arg_kind);
   if (s != GESPMM_OK) return s;
   if (p.a.n_rows == 0) return GESPMM_OK;
   SpmmArgs args{};
@@ -1210,6 +1227,7 @@ gespmm_status_t gespmm_spmm_device(const gespmm_csr_t* a, const float* b, uint32
   gespmm_status_t s = check_opts(o);
   if (s != GESPMM_OK) return s;
   s = check_op(op, arg);
+  if (s == GESPMM_OK) s = check_arg_range(arg, a->nnz, a->n_cols, o.arg_kind);
   if (s != GESPMM_OK) return s;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (o.validate) {
@@ -1247,6 +1265,7 @@ gespmm_status_t gespmm_spmm_host(const gespmm_csr_t* a, const float* b, uint32_t
   gespmm_options_t o;
   if (opts) o = *opts; else gespmm_options_default(&o);
   gespmm_status_t s = check_op(op, arg);
+  if (s == GESPMM_OK) s = check_arg_range(arg, a->nnz, a->n_cols, o.arg_kind);
   if (s != GESPMM_OK) return s;
   if (a->n_cols != b_rows) {
     char buf[160];

@@ -176,3 +176,28 @@ def test_host_checks_before_any_device_work(golden):
         with pytest.raises(G.Error) as ei:
             G.native_spmm(a, b, G.select_variant(case["n"]), G.ops.sum())
         assert str(ei.value) == case["error"]
+
+
+def test_int32_arg_range_is_checked_before_device_work():
+    """arg is int32 in the C ABI: a max/min call whose CSR positions (edge
+    args) or columns (column args) would not fit is refused with EINVAL before
+    any device work, instead of writing wrapped indices."""
+    L = _lib.lib()
+    big = (1 << 31) + 5
+    csr = _lib.Csr(4, 8, big, None, None, None)       # never dereferenced
+    arg = ctypes.c_void_p(16)                          # never written
+    for entry in ("gespmm_spmm_device", "gespmm_spmm_host"):
+        o = _lib.default_options(validate=0)
+        if entry == "gespmm_spmm_device":
+            st = L.gespmm_spmm_device(ctypes.byref(csr), None, 4, _lib.MAX, None, arg,
+                                      ctypes.byref(o), None)
+        else:
+            st = L.gespmm_spmm_host(ctypes.byref(csr), None, 8, 4, _lib.MAX, None, arg,
+                                    ctypes.byref(o))
+        assert st == _lib.EINVAL
+        msg = L.gespmm_last_error().decode()
+        assert "do not fit the int32 arg" in msg and "arg_kind = column" in msg, msg
+    wide = _lib.Csr(4, (1 << 32) - 1, 10, None, None, None)
+    o = _lib.default_options(validate=0, arg_kind=_lib.ARG_COLUMN)
+    st = L.gespmm_spmm_device(ctypes.byref(wide), None, 4, _lib.MAX, None, arg, ctypes.byref(o), None)
+    assert st == _lib.EINVAL and "column indices" in L.gespmm_last_error().decode()
