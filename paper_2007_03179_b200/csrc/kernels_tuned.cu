@@ -23,6 +23,11 @@
 //   the nonzeros), keeping the per-element ascending fold and with it
 //   bit-exactness; a deeper gather batch (32 scalar or 8 vector loads per lane)
 //   gives the hub the latency hiding a single warp cannot.
+//
+// k_split_combine / k_split_refresh — split hub rows (max/min, fast-mode
+//   sum/mean): k_warp folds each hub row's segments into partial rows, the
+//   combine folds the partials in segment order; the refresh rebuilds the
+//   segments' virtual row_ptr from the live row_ptr for a cached plan.
 #include <algorithm>
 #include <atomic>
 #include <cstdlib>
